@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark: VGG-16 burst-parallel training, foreground samples/s.
+
+Contract (see task statement / DESIGN.md §Measurement):
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* our arm: ``plan(vgg_like, N, amp=2.0)`` at global batch 32 (BASELINE.json
+  configs[1]; at N=1 that plan is every layer on one GPU), executed by
+  ``BurstStep`` (libbpx sm_100a kernels) captured as one CUDA graph per
+  rank.  W untimed warm-up steps, then K steps bracketed by barrier +
+  synchronize, timed with CUDA events on the launching stream, max over
+  ranks.  ``value`` = 32 * K / time (whole job).  Inputs: the activation
+  working set (~2.2 GB at B=32) is far larger than L2, so no explicit flush.
+* ``e2e``: the same metric through the public API ``run()`` with pinned
+  HOST inputs: every step copies its input shard in and reads the loss back.
+* ``roofline``: the tensor-core GEMM work (conv + dense fwd/dgrad/wgrad) of
+  one step = 2.9647 TFLOP at B=32 over the GEMM kernels'
+  measured time (CUDA events captured inside the graph, last timed replay).
+* ``cpu_baseline``: the CPU oracle step (oracle/vgg_ref.py, torch fp32,
+  all host threads) on a bounded sample.
+* ``--impl reference``: the reference has no fwd/bwd implementation (it
+  prices ops, simulator.py:254-261), so its CPU path for this step is the
+  oracle port, timed on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GLOBAL_BATCH = 32
+AMP_LIMIT = 2.0
+METRIC = "VGG-16 fg samples/s at global batch 32 (burst-parallel plan)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+                "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_step_samples_per_s(batch, steps=1, warm=0):
+    """Oracle CPU step (torch fp32, all host threads); returns (samples/s,
+    threads, seconds)."""
+    from oracle import vgg_ref
+    from paper_2112_10065_b200.network import init_params, synthetic_batch, vgg16
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    net = vgg16()
+    params = init_params(net, 0)
+    x, y = synthetic_batch(net, batch, 0)
+    for _ in range(warm):
+        vgg_ref.forward_backward(net, params, x, y, torch.float32)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        vgg_ref.forward_backward(net, params, x, y, torch.float32)
+    dt = time.perf_counter() - t0
+    return batch * steps / dt, threads, dt
+
+
+def bench_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    sample = 4        # bounded sample per step (~1-2 s of CPU work)
+    thr, threads, dt = cpu_step_samples_per_s(sample, steps=args.steps, warm=args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": thr, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (x~N(0,1) NHWC, uniform labels, torchvision-style init)",
+        "config": {"workload": "VGG-16 global batch 32 fwd+bwd step, CPU path",
+                   "global_batch": GLOBAL_BATCH, "sample_batch_per_step": sample},
+        "cpu_baseline": {"value": thr, "unit": "samples/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{sample} samples per step x {args.steps} steps "
+                                   "(oracle/vgg_ref.py torch fp32; the reference "
+                                   "burstplan has no fwd/bwd, simulator.py:254-261)"},
+        "e2e": {"value": thr, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_ours(args):
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2112_10065_b200 import ops, synth
+    from paper_2112_10065_b200.executor import BurstStep, _dist_comm, run
+    from paper_2112_10065_b200.network import synthetic_batch
+    from paper_2112_10065_b200.planner import plan
+    from paper_2112_10065_b200.timeline import SimConfig
+
+    graph = synth.vgg_like(seed=0, global_batch=GLOBAL_BATCH)
+    p = plan(graph, world, AMP_LIMIT)
+    comm = _dist_comm({g for _, g in p.assignments})
+    st = BurstStep(p, graph, comm=comm, seed=0, lr=1e-3)
+    x, y = synthetic_batch(st.net, GLOBAL_BATCH, seed=0)
+    xh, yh = x.pin_memory(), y.pin_memory()
+    st.load(xh, yh)
+    torch.cuda.synchronize()
+
+    # launches per step (eager pass, host counter in libbpx)
+    c0 = ops.launch_count()
+    st.forward_backward()
+    st.sync_and_update()
+    torch.cuda.synchronize()
+    launches_per_step = ops.launch_count() - c0
+
+    # graph with per-op events for the roofline breakdown
+    st.op_events = []
+    st.capture(warmup=1)
+    marks = st.op_events
+    st.op_events = None
+
+    for _ in range(args.warmup):
+        st.step()
+    comm.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            st.step()
+        e1.record()
+        torch.cuda.synchronize()
+    comm.barrier()
+    ms = e0.elapsed_time(e1)
+    ms = comm.max_scalar(ms, st.device)
+    value = GLOBAL_BATCH * args.steps / (ms / 1000.0)
+
+    # per-op durations from the events captured in the graph (last replay)
+    op_ms = {}
+    starts = {}
+    for tag, ev in marks:
+        kind, idx, what = tag
+        key = (kind, idx)
+        if what in ("start", "bstart"):
+            starts[(key, what)] = ev
+        else:
+            s = starts.get((key, "start" if what == "end" else "bstart"))
+            if s is not None:
+                op_ms[key] = op_ms.get(key, 0.0) + s.elapsed_time(ev)
+    gemm_ms = sum(v for (k, i), v in op_ms.items()
+                  if k == "compute" and st.layers[i].spec.kind in ("conv", "dense"))
+    flops_step = 0
+    for L in st.layers:
+        if L.active and L.spec.kind in ("conv", "dense"):
+            f = L.spec.fwd_flops() * L.b
+            flops_step += f * (2 if L is st.layers[0] else 3)
+    peaks, peak_src = _peaks()
+    tf32_peak = peaks["bf16_tflops"] / 2.0
+    achieved = flops_step / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
+
+    # end to end through the public API with pinned host inputs
+    cfg = SimConfig(warmup_iterations=args.warmup)
+    trace, metrics = run(p, graph, world, None, cfg, args.warmup + args.steps,
+                         inputs=(xh, yh), step=st)
+    e2e = metrics.fg_throughput_samples_per_s
+    a, b = st.input_range()
+    h2d = (b - a) * x[0].numel() * 4 + (st.label_range()[1] - st.label_range()[0]) * 4
+    result = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            thr, threads, dt = cpu_step_samples_per_s(4, steps=2, warm=1)
+            cpu = {"value": thr, "unit": "samples/s", "cores": threads, "kind": "port",
+                   "sample": "2 steps x 4 samples of the VGG-16 step, oracle/vgg_ref.py "
+                             "torch fp32 on all host threads"}
+        dom = max(((v, k) for k, v in op_ms.items()), default=(0, None))
+        result = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (x~N(0,1) NHWC 3x224x224, uniform labels, "
+                    "torchvision-style random init)",
+            "config": {"workload": "VGG-16 global batch 32, burst-parallel plan "
+                                   f"plan(vgg_like, {world}, amp={AMP_LIMIT}) "
+                                   "(BASELINE.json configs[1]), fwd+bwd+allreduce+SGD",
+                       "global_batch": GLOBAL_BATCH,
+                       "gpus_per_layer": [g for _, g in p.assignments],
+                       "parallelism": f"burst{world}",
+                       "l2": "working set ~2.2 GB > 126 MB L2, no flush needed",
+                       "cuda_graph": True},
+            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {
+                "bound": "tensor", "kernel": "conv/dense implicit GEMM (fwd+dgrad+wgrad)",
+                "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": (achieved / tf32_peak) if achieved else None,
+                "frac_of_3xtf32": (achieved / (tf32_peak / 3)) if achieved else None,
+                "peak_source": f"{peak_src}: TF32 dense = bf16_tflops/2",
+                "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
+                "gemm_share_of_step": gemm_ms / (ms / args.steps),
+                "traffic": None},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "dominant_op": {"op": str(dom[1]), "ms": dom[0]},
+            "loss": trace.loss,
+        }
+        print(json.dumps(result), flush=True)
+        if args.breakdown:
+            with open(args.breakdown, "w") as fh:
+                json.dump({f"{k}:{i}:{st.layers[i].spec.name if k != 'allreduce' else i}": v
+                           for (k, i), v in sorted(op_ms.items(), key=lambda t: -t[1])},
+                          fh, indent=1)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--breakdown", default=None)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

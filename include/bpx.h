@@ -1,0 +1,166 @@
+/*
+ * libbpx -- C-ABI of the B200 burst-parallel training runtime.
+ *
+ * The reference (`burstplan`, /root/reference/pkg) has no FFI: it *models*
+ * each per-iteration op as an OpRecord with a priced duration
+ * (simulator.py:175-196, compile_timeline :211-298).  Each entry point below
+ * is the real sm_100a implementation of one of those modeled ops; the
+ * comment on each names the reference construct it replaces.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers + sizes; no torch / CUDA types in signatures
+ *     (`stream` is a cudaStream_t passed as void*; NULL = legacy stream);
+ *   - stream-ordered, asynchronous, no host synchronisation, no allocation:
+ *     scratch space is caller-provided (query sizes with *_workspace);
+ *     every call is CUDA-graph capturable;
+ *   - return BPX_OK (0) or a nonzero bpx_status_t, never abort/throw;
+ *   - fp32 storage, fp32-accurate arithmetic (tensor-core paths use a
+ *     3xTF32 split); activations are NHWC, conv weights OHWI
+ *     ([Cout][3][3][Cin]), dense weights [out][in];
+ *   - deterministic: fixed-order reductions, bitwise run-to-run stable.
+ */
+#ifndef BPX_H_
+#define BPX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BPX_API __attribute__((visibility("default")))
+#else
+#define BPX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int bpx_status_t;
+
+enum {
+  BPX_OK = 0,
+  BPX_ERR_INVALID_ARGUMENT = 1, /* bad shape / null pointer / alignment   */
+  BPX_ERR_LAUNCH = 2,           /* cudaGetLastError after launch != 0     */
+  BPX_ERR_UNSUPPORTED = 3,      /* shape outside what the kernels handle  */
+  BPX_ERR_WORKSPACE = 4,        /* caller workspace too small             */
+  BPX_ERR_ARCH = 5              /* device is not sm_100 (no fallback)     */
+};
+
+/* Human-readable name of a status code (static storage). */
+BPX_API const char* bpx_status_string(bpx_status_t status);
+/* ABI version, bumped on any signature change. */
+BPX_API int bpx_abi_version(void);
+/* Kernel launches this process issued through libbpx so far (host count;
+ * a CUDA-graph replay re-runs the captured launches without counting). */
+BPX_API long long bpx_launch_count(void);
+/* 1 if the current device is sm_100 (the only supported target). */
+BPX_API int bpx_device_supported(void);
+
+/* ---- per-layer compute: replaces the modeled `compute` OpRecord ------
+ * (simulator.py:254-261; cost = comp(i,g) from graph.py:352-385 at the
+ * per-GPU batch ceil(B/g)).  n = that per-GPU batch.                      */
+
+/* y = relu?(conv3x3_pad1(x, w) + bias).  x:[n,h,w,cin] y:[n,h,w,cout]     */
+BPX_API bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias,
+                             float* y, int n, int h, int w_, int cin, int cout,
+                             int relu, void* ws, size_t ws_bytes, void* stream);
+BPX_API size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout);
+
+/* dx = conv3x3_transpose(dz, w) [* (mask_src > 0) if mask_src != NULL].
+ * dz:[n,h,w,cout] dx,mask_src:[n,h,w,cin].  mask_src is the layer input
+ * when that input is a ReLU output: fuses the previous ReLU's backward.   */
+BPX_API bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w,
+                               const float* mask_src, float* dx, int n, int h,
+                               int w_, int cin, int cout, void* ws,
+                               size_t ws_bytes, void* stream);
+BPX_API size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout);
+
+/* dw[cout,3,3,cin] = sum_pixels dz (x) im2col(x);  dbias[cout] = sum dz.  */
+BPX_API bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw,
+                               float* dbias, int n, int h, int w_, int cin,
+                               int cout, void* ws, size_t ws_bytes,
+                               void* stream);
+BPX_API size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout);
+
+/* y[b,out] = relu?(x[b,in] . w[out,in]^T + bias)                           */
+BPX_API bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias,
+                            float* y, int b, int in, int out, int relu,
+                            void* ws, size_t ws_bytes, void* stream);
+BPX_API size_t bpx_linear_fwd_workspace(int b, int in, int out);
+/* dx[b,in] = dy[b,out] . w [* (mask_src > 0)]                              */
+BPX_API bpx_status_t bpx_linear_dgrad(const float* dy, const float* w,
+                              const float* mask_src, float* dx, int b, int in,
+                              int out, void* ws, size_t ws_bytes, void* stream);
+BPX_API size_t bpx_linear_dgrad_workspace(int b, int in, int out);
+/* dw[out,in] = dy^T . x ;  dbias[out] = sum_b dy                           */
+BPX_API bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw,
+                              float* dbias, int b, int in, int out, void* ws,
+                              size_t ws_bytes, void* stream);
+BPX_API size_t bpx_linear_wgrad_workspace(int b, int in, int out);
+
+/* 2x2/stride-2 max pool, NHWC; bwd routes dy to the first max of each
+ * window (PyTorch order) recomputed from x.                                */
+BPX_API bpx_status_t bpx_maxpool2x2_fwd(const float* x, float* y, int n, int h, int w_,
+                                int c, void* stream);
+BPX_API bpx_status_t bpx_maxpool2x2_bwd(const float* x, const float* dy, float* dx,
+                                int n, int h, int w_, int c, void* stream);
+
+/* Mean softmax cross-entropy over the GLOBAL batch: loss_out[0] =
+ * sum_{local rows} CE / b_global (fixed order); loss_out must hold
+ * b_local + 1 floats ([1..b_local] = per-row terms);
+ * dlogits = (softmax - onehot) / b_global.                                 */
+BPX_API bpx_status_t bpx_softmax_xent(const float* logits, const int32_t* labels,
+                              int b_local, int b_global, int classes,
+                              float* loss_out, float* dlogits, void* stream);
+
+/* w -= lr * g  (plain SGD, fp32)                                           */
+BPX_API bpx_status_t bpx_sgd_update(float* w, const float* g, size_t n, float lr,
+                            void* stream);
+
+/* ---- sample resharding: replaces the modeled `transfer` OpRecord ------
+ * (simulator.py:242-253; volume = moved_samples * act bytes, costs.py:85-118).
+ * Pull model: this rank copies each segment from a (peer-mapped) source
+ * pointer into its own buffer.  src_ptrs / src_offsets / dst_offsets /
+ * nbytes are HOST arrays of n_seg (<= 64) entries, one per contiguous run
+ * (host-side index map: costs.reshard_segments); they are captured by value
+ * into the launch, so the call is CUDA-graph safe.
+ * Pointers may be NVLink peer addresses (P2P loads) or local.              */
+BPX_API bpx_status_t bpx_reshard_pull(const void* const* src_ptrs,
+                              const size_t* src_offsets, void* dst,
+                              const size_t* dst_offsets, const size_t* nbytes,
+                              int n_seg, void* stream);
+
+/* ---- subset gradient allreduce: replaces the modeled `allreduce` ------
+ * (simulator.py:264-278; ring volume 2N(g-1)/g, costs.py:130-140).
+ * One-shot pull allreduce over ranks [0,g): out = sum_{r<g} peers[r][0:n]
+ * accumulated in rank order (bitwise identical on every rank).  `peers`
+ * is a host array of g device pointers (peer-mapped).                      */
+BPX_API bpx_status_t bpx_allreduce_sum_prefix(const float* const* peers, int g,
+                                      float* out, size_t n, void* stream);
+
+/* Cross-GPU flag barrier for graph-captured P2P phases: write `epoch` into
+ * slot `rank` of every peer's signal pad, then spin until all g slots of
+ * the local pad reach `epoch`.  pads[r] = rank r's pad (g uint32 slots).   */
+BPX_API bpx_status_t bpx_signal_barrier(uint32_t* const* pads, int rank, int g,
+                                uint32_t epoch, void* stream);
+
+/* ---- engine-pinned variants (tests / benchmarks): force the FFMA
+ * implicit-GEMM engine regardless of shape, same semantics as above.      */
+BPX_API bpx_status_t bpx_simt_conv3x3_fwd(const float* x, const float* w,
+                                          const float* bias, float* y, int n,
+                                          int h, int w_, int cin, int cout,
+                                          int relu, void* stream);
+BPX_API bpx_status_t bpx_simt_conv3x3_dgrad(const float* dz, const float* w,
+                                            const float* mask_src, float* dx,
+                                            int n, int h, int w_, int cin,
+                                            int cout, void* stream);
+BPX_API bpx_status_t bpx_simt_conv3x3_wgrad(const float* x, const float* dz,
+                                            float* dw, float* dbias, int n,
+                                            int h, int w_, int cin, int cout,
+                                            void* ws, size_t ws_bytes,
+                                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPX_H_ */

@@ -1,0 +1,97 @@
+"""CPU numerics oracle for one burst-parallel training step.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product.
+
+The reference toolkit has no forward/backward at all (it prices a
+`compute` op per layer: /root/reference/pkg/src/burstplan/simulator.py:254-261,
+synth.py:86-123), so this is a restatement of the *paper's* step
+ for the network `paper_2112_10065_b200.network.vgg16`:
+forward layer by layer, mean softmax cross-entropy over the global batch,
+backward, per-layer weight gradients.  Numerics parity is therefore
+"unpinned" against the reference (no golden vectors exist there); it is
+pinned against this oracle in fp64, with the tolerance stated in
+tests/test_step_gpu.py (SURVEY.md §8c gate).
+
+Layouts follow the product: NHWC activations, OHWI conv weights, dense
+weights [out][in], fc1 input in NHWC-flatten order.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+
+def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
+                     threads=None):
+    """Return (loss, grads) with grads[name] = (dW, db) in product layouts.
+
+    ``params``: dict name -> (w, b) CPU tensors; ``labels`` int tensor.
+    The loss is the mean over the batch given (= the global batch).
+    """
+    if threads:
+        torch.set_num_threads(threads)
+    leaves = {}
+    for name, (w, b) in params.items():
+        leaves[name] = (w.detach().to(dtype).clone().requires_grad_(True),
+                        b.detach().to(dtype).clone().requires_grad_(True))
+    h = x_nhwc.to(dtype).permute(0, 3, 1, 2).contiguous()       # NCHW
+    flat = False
+    for l in net.layers:
+        if l.kind == "conv":
+            w, b = leaves[l.name]
+            h = F.conv2d(h, w.permute(0, 3, 1, 2), b, padding=1)
+            if l.relu:
+                h = F.relu(h)
+        elif l.kind == "pool":
+            h = F.max_pool2d(h, 2, 2)
+        else:
+            if not flat:
+                h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)   # NHWC flatten
+                flat = True
+            w, b = leaves[l.name]
+            h = F.linear(h, w, b)
+            if l.relu:
+                h = F.relu(h)
+    loss = F.cross_entropy(h, labels.to(torch.int64))
+    loss.backward()
+    grads = {n: (w.grad.detach(), b.grad.detach()) for n, (w, b) in leaves.items()}
+    return float(loss.detach()), grads
+
+
+def layer_fwd(l, x, w=None, b=None, dtype=torch.float64):
+    """One layer forward on CPU (NHWC in/out) for kernel unit tests."""
+    x = x.to(dtype)
+    if l.kind == "conv":
+        y = F.conv2d(x.permute(0, 3, 1, 2), w.to(dtype).permute(0, 3, 1, 2),
+                     None if b is None else b.to(dtype), padding=1)
+        if l.relu:
+            y = F.relu(y)
+        return y.permute(0, 2, 3, 1).contiguous()
+    if l.kind == "pool":
+        return F.max_pool2d(x.permute(0, 3, 1, 2), 2, 2).permute(0, 2, 3, 1).contiguous()
+    y = F.linear(x, w.to(dtype), None if b is None else b.to(dtype))
+    return F.relu(y) if l.relu else y
+
+
+def conv_grads(x, w, dz, dtype=torch.float64):
+    """dx (unmasked), dw, db of a 3x3/pad-1 conv given dz (NHWC)."""
+    xx = x.to(dtype).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    ww = w.to(dtype).permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+    y = F.conv2d(xx, ww, None, padding=1)
+    y.backward(dz.to(dtype).permute(0, 3, 1, 2))
+    return (xx.grad.permute(0, 2, 3, 1).contiguous(),
+            ww.grad.permute(0, 2, 3, 1).contiguous(),
+            dz.to(dtype).sum(dim=(0, 1, 2)))
+
+
+def normwise_rel(a, ref):
+    """||a - ref|| / ||ref|| in fp64 (0 when both are 0)."""
+    a = a.detach().to(torch.float64).cpu()
+    ref = ref.detach().to(torch.float64).cpu()
+    den = torch.linalg.vector_norm(ref)
+    num = torch.linalg.vector_norm(a - ref)
+    if den == 0:
+        return float(num)
+    return float(num / den)

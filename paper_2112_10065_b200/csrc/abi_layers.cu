@@ -1,0 +1,119 @@
+// C-ABI entry points of the per-layer compute ops (conv3x3 / dense),
+// dispatching each call to the fastest engine that handles the shape.
+#include "common.cuh"
+#include "simt_api.h"
+#include "tc_api.h"
+
+using namespace bpx;
+
+extern "C" {
+
+size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
+  return tc_conv_fwd_ws(n, h, w_, cin, cout);
+}
+
+bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, float* y,
+                             int n, int h, int w_, int cin, int cout, int relu, void* ws,
+                             size_t ws_bytes, void* stream) {
+  BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
+  BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
+  cudaStream_t st = as_stream(stream);
+  if (tc_conv_fwd_ok(n, h, w_, cin, cout))
+    return tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+  return simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
+}
+
+size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
+  return tc_conv_dgrad_ws(n, h, w_, cin, cout);
+}
+
+bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mask_src,
+                               float* dx, int n, int h, int w_, int cin, int cout,
+                               void* ws, size_t ws_bytes, void* stream) {
+  BPX_CHECK_ARG(dz && w && dx && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
+  BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w));
+  cudaStream_t st = as_stream(stream);
+  if (tc_conv_dgrad_ok(n, h, w_, cin, cout))
+    return tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+  return simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st);
+}
+
+size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
+  size_t a = simt_conv_wgrad_ws(n, h, w_, cin, cout);
+  size_t b = tc_conv_wgrad_ws(n, h, w_, cin, cout);
+  return a > b ? a : b;
+}
+
+bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float* dbias,
+                               int n, int h, int w_, int cin, int cout, void* ws,
+                               size_t ws_bytes, void* stream) {
+  BPX_CHECK_ARG(x && dz && dw && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
+  BPX_CHECK_ARG(ws || ws_bytes == 0);
+  cudaStream_t st = as_stream(stream);
+  if (tc_conv_wgrad_ok(n, h, w_, cin, cout))
+    return tc_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+  return simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+}
+
+size_t bpx_linear_fwd_workspace(int b, int in, int out) {
+  size_t a = simt_linear_fwd_ws(b, in, out), c = tc_linear_fwd_ws(b, in, out);
+  return a > c ? a : c;
+}
+size_t bpx_linear_dgrad_workspace(int b, int in, int out) {
+  size_t a = simt_linear_dgrad_ws(b, in, out), c = tc_linear_dgrad_ws(b, in, out);
+  return a > c ? a : c;
+}
+size_t bpx_linear_wgrad_workspace(int b, int in, int out) {
+  size_t a = simt_linear_wgrad_ws(b, in, out), c = tc_linear_wgrad_ws(b, in, out);
+  return a > c ? a : c;
+}
+
+bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, float* y,
+                            int b, int in, int out, int relu, void* ws, size_t ws_bytes,
+                            void* stream) {
+  BPX_CHECK_ARG(x && w && y && b >= 0 && in > 0 && out > 0 && aligned16(w));
+  cudaStream_t st = as_stream(stream);
+  if (tc_linear_ok(b, in, out))
+    return tc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+  return simt_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+}
+
+bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask_src,
+                              float* dx, int b, int in, int out, void* ws, size_t ws_bytes,
+                              void* stream) {
+  BPX_CHECK_ARG(dy && w && dx && b >= 0 && in > 0 && out > 0 && aligned16(w));
+  cudaStream_t st = as_stream(stream);
+  if (tc_linear_ok(b, in, out))
+    return tc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+  return simt_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+}
+
+bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias,
+                              int b, int in, int out, void* ws, size_t ws_bytes,
+                              void* stream) {
+  BPX_CHECK_ARG(x && dy && dw && b >= 0 && in > 0 && out > 0 && aligned16(dw));
+  cudaStream_t st = as_stream(stream);
+  if (tc_linear_ok(b, in, out))
+    return tc_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+  return simt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+}
+
+// Engine-pinned variants for tests and benchmarks (same semantics).
+bpx_status_t bpx_simt_conv3x3_fwd(const float* x, const float* w, const float* bias,
+                                  float* y, int n, int h, int w_, int cin, int cout,
+                                  int relu, void* stream) {
+  return simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, as_stream(stream));
+}
+bpx_status_t bpx_simt_conv3x3_dgrad(const float* dz, const float* w, const float* mask,
+                                    float* dx, int n, int h, int w_, int cin, int cout,
+                                    void* stream) {
+  return simt_conv_dgrad(dz, w, mask, dx, n, h, w_, cin, cout, as_stream(stream));
+}
+bpx_status_t bpx_simt_conv3x3_wgrad(const float* x, const float* dz, float* dw,
+                                    float* dbias, int n, int h, int w_, int cin, int cout,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  return simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes,
+                         as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// Cross-GPU data movement of the burst-parallel step over NVLink peer
+// memory (pointers from CUDA IPC / torch symmetric memory, or local
+// pointers when peers are simulated on one device in tests).
+//
+//  * bpx_reshard_pull        -- the modeled `transfer` op
+//                               (/root/reference/pkg/src/burstplan/simulator.py:242-253)
+//  * bpx_allreduce_sum_prefix -- the modeled `allreduce` op (:264-278)
+//  * bpx_signal_barrier      -- ordering between the two sides of a P2P phase
+//
+// All copies are 16-byte vectorised when every segment is 16-byte aligned
+// (activation rows are multiples of 16 bytes for every VGG layer), else
+// byte-granular; CTAs stride the segment list so one launch moves all of it.
+#include "common.cuh"
+
+namespace bpx {
+
+constexpr int kMaxSeg = 64;
+constexpr int kMaxPeers = 16;
+
+struct SegTable {
+  const char* src[kMaxSeg];
+  char* dst[kMaxSeg];
+  unsigned long long bytes[kMaxSeg];
+  unsigned long long start[kMaxSeg + 1];   // prefix sums of bytes
+  int n;
+};
+
+template <bool VEC>
+__global__ void reshard_kernel(SegTable t) {
+  const unsigned long long total = t.start[t.n];
+  const unsigned long long step = (unsigned long long)gridDim.x * blockDim.x * (VEC ? 16 : 1);
+  unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * (VEC ? 16 : 1);
+  int seg = 0;
+  for (; i < total; i += step) {
+    while (i >= t.start[seg + 1]) ++seg;          // monotone in i
+    unsigned long long off = i - t.start[seg];
+    if (VEC) {
+      int4 v = *reinterpret_cast<const int4*>(t.src[seg] + off);
+      *reinterpret_cast<int4*>(t.dst[seg] + off) = v;
+    } else {
+      t.dst[seg][off] = t.src[seg][off];
+    }
+  }
+}
+
+struct PeerTable {
+  const float* p[kMaxPeers];
+  int g;
+};
+
+__global__ void allreduce_pull_kernel(PeerTable t, float4* __restrict__ out, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(t.p[0])[i];
+    for (int r = 1; r < t.g; ++r) {            // fixed rank order -> identical on every rank
+      float4 v = reinterpret_cast<const float4*>(t.p[r])[i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    out[i] = s;
+  }
+}
+__global__ void allreduce_pull_scalar(PeerTable t, float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = t.p[0][i];
+    for (int r = 1; r < t.g; ++r) s += t.p[r][i];
+    out[i] = s;
+  }
+}
+
+struct PadTable {
+  unsigned int* pad[kMaxPeers];
+  int g, rank;
+  unsigned int epoch;
+};
+
+__global__ void signal_barrier_kernel(PadTable t) {
+  int tid = threadIdx.x;
+  if (tid < t.g) {
+    // publish: every write this stream issued before us is visible system-wide
+    __threadfence_system();
+    volatile unsigned int* slot = t.pad[tid] + t.rank;
+    *slot = t.epoch;
+    volatile unsigned int* mine = t.pad[t.rank] + tid;
+    while ((int)(*mine - t.epoch) < 0) { }
+    __threadfence_system();
+  }
+}
+
+}  // namespace bpx
+
+using namespace bpx;
+
+extern "C" {
+
+bpx_status_t bpx_reshard_pull(const void* const* src_ptrs, const size_t* src_offsets,
+                              void* dst, const size_t* dst_offsets, const size_t* nbytes,
+                              int n_seg, void* stream) {
+  BPX_CHECK_ARG(n_seg >= 0 && n_seg <= kMaxSeg);
+  if (n_seg == 0) return BPX_OK;
+  BPX_CHECK_ARG(src_ptrs && src_offsets && dst && dst_offsets && nbytes);
+  SegTable t{};
+  bool vec = true;
+  unsigned long long acc = 0;
+  int k = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    if (nbytes[i] == 0) continue;
+    BPX_CHECK_ARG(src_ptrs[i] != nullptr);
+    t.src[k] = static_cast<const char*>(src_ptrs[i]) + src_offsets[i];
+    t.dst[k] = static_cast<char*>(dst) + dst_offsets[i];
+    t.bytes[k] = nbytes[i];
+    t.start[k] = acc;
+    acc += nbytes[i];
+    vec = vec && aligned16(t.src[k]) && aligned16(t.dst[k]) && nbytes[i] % 16 == 0;
+    ++k;
+  }
+  t.n = k;
+  t.start[k] = acc;
+  if (acc == 0) return BPX_OK;
+  long long units = vec ? (long long)(acc / 16) : (long long)acc;
+  int grid = (int)std::min<long long>(cdivll(units, 256), 4LL * num_sms());
+  if (vec) reshard_kernel<true><<<grid, 256, 0, as_stream(stream)>>>(t);
+  else reshard_kernel<false><<<grid, 256, 0, as_stream(stream)>>>(t);
+  return launch_status();
+}
+
+bpx_status_t bpx_allreduce_sum_prefix(const float* const* peers, int g, float* out,
+                                      size_t n, void* stream) {
+  BPX_CHECK_ARG(peers && out && g >= 1 && g <= kMaxPeers);
+  if (n == 0) return BPX_OK;
+  PeerTable t{};
+  bool vec = aligned16(out) && n % 4 == 0;
+  for (int r = 0; r < g; ++r) {
+    BPX_CHECK_ARG(peers[r] != nullptr);
+    t.p[r] = peers[r];
+    vec = vec && aligned16(peers[r]);
+  }
+  t.g = g;
+  cudaStream_t st = as_stream(stream);
+  if (vec) {
+    long long n4 = (long long)(n / 4);
+    int grid = (int)std::min<long long>(cdivll(n4, 256), 4LL * num_sms());
+    allreduce_pull_kernel<<<grid, 256, 0, st>>>(t, reinterpret_cast<float4*>(out), n4);
+  } else {
+    int grid = (int)std::min<long long>(cdivll((long long)n, 256), 4LL * num_sms());
+    allreduce_pull_scalar<<<grid, 256, 0, st>>>(t, out, (long long)n);
+  }
+  return launch_status();
+}
+
+bpx_status_t bpx_signal_barrier(uint32_t* const* pads, int rank, int g, uint32_t epoch,
+                                void* stream) {
+  BPX_CHECK_ARG(pads && g >= 1 && g <= kMaxPeers && rank >= 0 && rank < g);
+  PadTable t{};
+  for (int r = 0; r < g; ++r) {
+    BPX_CHECK_ARG(pads[r] != nullptr);
+    t.pad[r] = pads[r];
+  }
+  t.g = g; t.rank = rank; t.epoch = epoch;
+  signal_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+// Internal entry points of the FFMA implicit-GEMM engine (conv_simt.cu).
+#pragma once
+#include "common.cuh"
+
+namespace bpx {
+size_t simt_conv_wgrad_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t simt_conv_fwd(const float* x, const float* w, const float* bias, float* y,
+                           int n, int h, int w_, int cin, int cout, int relu,
+                           cudaStream_t st);
+bpx_status_t simt_conv_dgrad(const float* dz, const float* w, const float* mask,
+                             float* dx, int n, int h, int w_, int cin, int cout,
+                             cudaStream_t st);
+bpx_status_t simt_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias,
+                             int n, int h, int w_, int cin, int cout, void* ws,
+                             size_t ws_bytes, cudaStream_t st);
+size_t simt_linear_fwd_ws(int b, int in, int out);
+size_t simt_linear_dgrad_ws(int b, int in, int out);
+size_t simt_linear_wgrad_ws(int b, int in, int out);
+bpx_status_t simt_linear_fwd(const float* x, const float* w, const float* bias, float* y,
+                             int b, int in, int out, int relu, void* ws, size_t ws_bytes,
+                             cudaStream_t st);
+bpx_status_t simt_linear_dgrad(const float* dy, const float* w, const float* mask,
+                               float* dx, int b, int in, int out, void* ws,
+                               size_t ws_bytes, cudaStream_t st);
+bpx_status_t simt_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias,
+                               int b, int in, int out, void* ws, size_t ws_bytes,
+                               cudaStream_t st);
+}  // namespace bpx

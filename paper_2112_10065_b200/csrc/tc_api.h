@@ -1,0 +1,35 @@
+// tcgen05 / TMEM tensor-core engine (3xTF32 split, fp32-accurate) for the
+// conv3x3 and dense layers.  *_ok() says whether a shape is taken.
+#pragma once
+#include "common.cuh"
+
+namespace bpx {
+bool tc_conv_fwd_ok(int n, int h, int w, int cin, int cout);
+bool tc_conv_dgrad_ok(int n, int h, int w, int cin, int cout);
+bool tc_conv_wgrad_ok(int n, int h, int w, int cin, int cout);
+bool tc_linear_ok(int b, int in, int out);
+size_t tc_conv_fwd_ws(int n, int h, int w, int cin, int cout);
+size_t tc_conv_dgrad_ws(int n, int h, int w, int cin, int cout);
+size_t tc_conv_wgrad_ws(int n, int h, int w, int cin, int cout);
+size_t tc_linear_fwd_ws(int b, int in, int out);
+size_t tc_linear_dgrad_ws(int b, int in, int out);
+size_t tc_linear_wgrad_ws(int b, int in, int out);
+bpx_status_t tc_conv_fwd(const float* x, const float* w, const float* bias, float* y,
+                         int n, int h, int w_, int cin, int cout, int relu, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+bpx_status_t tc_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
+                           int n, int h, int w_, int cin, int cout, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
+bpx_status_t tc_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias,
+                           int n, int h, int w_, int cin, int cout, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
+bpx_status_t tc_linear_fwd(const float* x, const float* w, const float* bias, float* y,
+                           int b, int in, int out, int relu, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+bpx_status_t tc_linear_dgrad(const float* dy, const float* w, const float* mask,
+                             float* dx, int b, int in, int out, void* ws,
+                             size_t ws_bytes, cudaStream_t st);
+bpx_status_t tc_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias,
+                             int b, int in, int out, void* ws, size_t ws_bytes,
+                             cudaStream_t st);
+}  // namespace bpx

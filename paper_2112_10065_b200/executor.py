@@ -1,0 +1,382 @@
+"""B200 executor of a burst-parallel plan: the real counterpart of the
+reference's simulated execution model.
+
+The reference expands a plan into an op program (`compile_timeline`,
+/root/reference/pkg/src/burstplan/simulator.py:211-298) and *simulates* it
+(`simulate` :451-819).  ``BurstStep`` runs that program on the GPU(s):
+
+* layer i runs on ranks [0, g_i), each with the contiguous ceil-split
+  sample block ``shard_range(B, g_i, rank)`` (costs.py:85-104);
+* a g change between consecutive layers is a reshard of activations
+  (forward) and of their gradients (backward) -- the `transfer` op;
+* after the backward pass, weight gradients of every layer with g > 1 are
+  summed over ranks [0, g) -- the `allreduce` op -- bucketed per g (the
+  plan and the reference's serial, non-overlapped charging are unchanged);
+* plain SGD updates every replica identically.
+
+Every FLOP runs in libbpx (ops.py); torch provides device memory, streams,
+CUDA graphs and torch.distributed.  ``run`` / ``run_two_phase`` mirror the
+reference's ``simulate`` / ``run_two_phase`` signatures and return the same
+``(SimTrace, SimMetrics)`` types, filled from CUDA-event timestamps.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Iterable, Optional
+
+import torch
+
+from . import ops
+from .comm import LocalComm, TorchComm
+from .costs import shard_range
+from .errors import GraphFormatError
+from .graph import CompGraph
+from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
+from .planner import TrainingPlan
+from .timeline import (FG_TASK, SimConfig, SimMetrics, SimTrace, compile_timeline,
+                       feedback_update, metrics_from_trace, us_to_ticks)
+
+
+@dataclass
+class _Layer:
+    spec: LayerSpec
+    g: int
+    s0: int              # first global sample of this rank's shard
+    b: int               # local batch (0 if the ceil split ran out)
+    active: bool         # rank < g
+    x: Optional[torch.Tensor] = None       # input (g layout)
+    y: Optional[torch.Tensor] = None       # output
+    dy: Optional[torch.Tensor] = None      # grad wrt output (pre-ReLU for ReLU layers)
+    dx: Optional[torch.Tensor] = None      # grad wrt input (masked by the input's ReLU)
+    w: Optional[torch.Tensor] = None
+    bias: Optional[torch.Tensor] = None
+    dw: Optional[torch.Tensor] = None
+    dbias: Optional[torch.Tensor] = None
+    reshard_in: bool = False               # input arrives through a reshard
+
+
+class BurstStep:
+    """One rank's share of a burst-parallel training step on one device."""
+
+    def __init__(self, plan: TrainingPlan, graph: CompGraph, *, device=None,
+                 comm=None, seed: int = 0, lr: float = 0.01,
+                 params: Optional[dict] = None, net: Optional[NetSpec] = None):
+        self.net = net or net_for_graph(graph)
+        self.B = plan.global_batch
+        self.comm = comm or LocalComm()
+        self.rank = self.comm.rank
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        self.lr = lr
+        ops.load_library()
+        gs = [g for lid, g in plan.assignments if not graph.layer(lid).is_virtual]
+        if len(gs) != len(self.net.layers):
+            raise GraphFormatError("plan does not cover every executable layer")
+        if max(gs) > self.comm.world:
+            raise GraphFormatError(f"plan uses {max(gs)} GPUs, world is {self.comm.world}")
+        params = params if params is not None else init_params(self.net, seed)
+        dev = self.device
+        self.layers: list[_Layer] = []
+        for spec, g in zip(self.net.layers, gs):
+            s0, s1 = shard_range(self.B, g, self.rank)
+            self.layers.append(_Layer(spec, g, s0, s1 - s0, self.rank < g))
+
+        # ---- buckets of gradients per g (one flat buffer per g) ----------
+        self.buckets: dict[int, torch.Tensor] = {}
+        sizes: dict[int, int] = {}
+        for L in self.layers:
+            if L.active and L.spec.param_shapes():
+                sizes[L.g] = sizes.get(L.g, 0) + _pad4(L.spec.n_params())
+        for g, n in sizes.items():
+            self.buckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
+        cursor = {g: 0 for g in sizes}
+
+        ws_need = 0
+        for i, L in enumerate(self.layers):
+            sp = L.spec
+            if not L.active:
+                continue
+            prev = self.layers[i - 1] if i else None
+            L.reshard_in = prev is not None and prev.g != L.g
+            if prev is None or L.reshard_in:
+                L.x = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
+            else:
+                L.x = prev.y.view(sp.in_shape(L.b))
+            L.y = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+            L.dy = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+            if i > 0:
+                if L.reshard_in:
+                    L.dx = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
+                else:
+                    L.dx = prev.dy.view(sp.in_shape(L.b))
+            ps = sp.param_shapes()
+            if ps:
+                w, b = params[sp.name]
+                L.w = w.to(dev).contiguous()
+                L.bias = b.to(dev).contiguous()
+                flat = self.buckets[L.g]
+                c = cursor[L.g]
+                nw, nb = w.numel(), b.numel()
+                L.dw = flat[c:c + nw].view(ps[0])
+                L.dbias = flat[c + nw:c + nw + nb]
+                cursor[L.g] = c + _pad4(nw + nb)
+                if sp.kind == "conv":
+                    ws_need = max(ws_need, ops.conv_workspace_bytes(
+                        L.b, sp.hw, sp.hw, sp.cin, sp.cout))
+                else:
+                    ws_need = max(ws_need, ops.linear_workspace_bytes(L.b, sp.cin, sp.cout))
+        self.ws = ops.Workspace(dev)
+        self.ws.reserve(ws_need)
+        last = self.layers[-1]
+        self.loss_buf = torch.zeros(max(last.b, 0) + 1, dtype=torch.float32, device=dev)
+        self.labels = torch.zeros(max(last.b, 1), dtype=torch.int32, device=dev)
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+        self.op_events: Optional[list] = None
+
+    # ------------------------------------------------------------ data
+    @property
+    def input(self) -> Optional[torch.Tensor]:
+        L0 = self.layers[0]
+        return L0.x if L0.active else None
+
+    def input_range(self) -> tuple[int, int]:
+        L0 = self.layers[0]
+        return L0.s0, L0.s0 + L0.b
+
+    def label_range(self) -> tuple[int, int]:
+        L = self.layers[-1]
+        return L.s0, L.s0 + L.b
+
+    def load(self, x_global: torch.Tensor, labels_global: torch.Tensor) -> None:
+        """Copy this rank's shards (x: NHWC [B,...], labels [B]) to the
+        device; async when the sources are pinned host tensors."""
+        a, b = self.input_range()
+        if self.layers[0].active and b > a:
+            self.layers[0].x.copy_(x_global[a:b], non_blocking=True)
+        a, b = self.label_range()
+        if self.layers[-1].active and b > a:
+            self.labels[:b - a].copy_(labels_global[a:b], non_blocking=True)
+
+    # ------------------------------------------------------------ step
+    def _fwd(self, i: int) -> None:
+        L = self.layers[i]
+        sp = L.spec
+        if sp.kind == "conv":
+            ops.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+        elif sp.kind == "pool":
+            ops.maxpool2x2_fwd(L.x, L.y)
+        else:
+            ops.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
+
+    def _bwd(self, i: int) -> None:
+        L = self.layers[i]
+        sp = L.spec
+        mask = L.x if sp.in_relu else None
+        if sp.kind == "conv":
+            ops.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
+            if i > 0:
+                ops.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
+        elif sp.kind == "pool":
+            ops.maxpool2x2_bwd(L.x, L.dy, L.dx)
+        else:
+            x2 = L.x.view(L.b, sp.cin)
+            ops.linear_wgrad(x2, L.dy, L.dw, L.dbias, ws=self.ws)
+            if i > 0:
+                ops.linear_dgrad(L.dy, L.w, None if mask is None else x2,
+                                 L.dx.view(L.b, sp.cin), ws=self.ws)
+
+    def _reshard(self, i: int, backward: bool) -> None:
+        prev, L = self.layers[i - 1], self.layers[i]
+        bps = 4 * L.spec.in_elems()
+        if not backward:
+            self.comm.reshard(prev.y if prev.active else None, prev.g,
+                              L.x if L.active else None, L.g, self.B, bps)
+        else:
+            self.comm.reshard(L.dx if L.active else None, L.g,
+                              prev.dy if prev.active else None, prev.g, self.B, bps)
+
+    def _mark(self, tag):
+        if self.op_events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.op_events.append((tag, ev))
+
+    def forward_backward(self) -> None:
+        n = len(self.layers)
+        for i in range(n):
+            if i and self.layers[i - 1].g != self.layers[i].g:
+                self._mark(("transfer", i, "start"))
+                self._reshard(i, backward=False)
+                self._mark(("transfer", i, "end"))
+            if self.layers[i].active:
+                self._mark(("compute", i, "start"))
+                self._fwd(i)
+        last = self.layers[-1]
+        if last.active:
+            ops.softmax_xent(last.y, self.labels[:last.b], self.B, self.loss_buf, last.dy)
+        for i in reversed(range(n)):
+            L = self.layers[i]
+            if L.active:
+                self._bwd(i)
+                self._mark(("compute", i, "end"))
+            if i and self.layers[i - 1].g != L.g:
+                self._mark(("transfer", i, "bstart"))
+                self._reshard(i, backward=True)
+                self._mark(("transfer", i, "bend"))
+
+    def sync_and_update(self) -> None:
+        for g in sorted(self.buckets, reverse=True):
+            if g > 1:
+                self._mark(("allreduce", g, "start"))
+                self.comm.allreduce(self.buckets[g], g)
+                self._mark(("allreduce", g, "end"))
+        for L in self.layers:
+            if L.active and L.w is not None:
+                ops.sgd_update(L.w, L.dw, self.lr)
+                ops.sgd_update(L.bias, L.dbias, self.lr)
+
+    def step(self) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        self.forward_backward()
+        self.sync_and_update()
+
+    def capture(self, warmup: int = 2) -> None:
+        """Capture the whole step (kernels + NCCL) as one CUDA graph; the
+        warm-up runs on a side stream as torch requires."""
+        record = self.op_events is not None
+        self.op_events = None
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.forward_backward()
+                self.sync_and_update()
+        torch.cuda.current_stream().wait_stream(s)
+        if record:          # events become record nodes inside the graph
+            self.op_events = []
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward_backward()
+            self.sync_and_update()
+        self.graph = g
+
+    def loss(self) -> float:
+        """Global mean loss (sum of shard partials over the last layer's g)."""
+        last = self.layers[-1]
+        part = self.loss_buf[:1].clone() if last.active else torch.zeros(1, device=self.device)
+        if last.g > 1:
+            self.comm.allreduce(part, last.g)
+        return float(part.item())
+
+    def grads(self) -> dict:
+        return {L.spec.name: (L.dw, L.dbias) for L in self.layers
+                if L.active and L.w is not None}
+
+    def params(self) -> dict:
+        return {L.spec.name: (L.w, L.bias) for L in self.layers
+                if L.active and L.w is not None}
+
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped entry points
+
+
+def _dist_comm(plan_gs):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return TorchComm(dist.get_rank(), dist.get_world_size(), plan_gs)
+    return LocalComm()
+
+
+def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
+        bg_graph: Optional[CompGraph] = None, config: Optional[SimConfig] = None,
+        iterations: int = 4, sensitive: Iterable[str] = (),
+        baseline_fg_iteration_us: Optional[float] = None, *,
+        inputs=None, seed: int = 0, lr: float = 0.01, use_graphs: bool = True,
+        step: Optional[BurstStep] = None):
+    """Execute ``iterations`` training steps of ``plan`` on real GPUs.
+
+    Same call shape and return types as the reference's
+    ``simulate(compile_timeline(plan, graph, n_gpus, bg_graph, config), ...)``
+    (simulator.py:451-456): ``(SimTrace, SimMetrics)`` with ticks of 0.1 us
+    taken from CUDA events.  Launch one process per GPU (torchrun) for
+    n_gpus > 1.  ``inputs`` = (x NHWC [B,...], labels [B]) host tensors
+    (pinned for async copies); each iteration copies them in and reads the
+    loss back, end to end.  The background job (``bg_graph``) is scheduled
+    by the multiplexer (see ``multiplex.py``).
+    """
+    config = config or SimConfig()
+    tl = compile_timeline(plan, graph, n_gpus, bg_graph, config)
+    comm = _dist_comm({g for _, g in plan.assignments})
+    if comm.world != n_gpus and not (comm.world == 1 and n_gpus == 1):
+        raise GraphFormatError(f"n_gpus={n_gpus} but world size is {comm.world}")
+    st = step or BurstStep(plan, graph, comm=comm, seed=seed, lr=lr)
+    if inputs is None:
+        x, y = synthetic_batch(st.net, plan.global_batch, seed)
+        inputs = (x.pin_memory(), y.pin_memory())
+    x_h, y_h = inputs
+    st.load(x_h, y_h)
+    if use_graphs and st.graph is None:
+        st.capture()
+    loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+    comm.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    ends = []
+    for _ in range(iterations):
+        st.load(x_h, y_h)
+        st.step()
+        loss_h.copy_(st.loss_buf[:1], non_blocking=True)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        ends.append(e)
+    torch.cuda.synchronize()
+    trace = SimTrace()
+    for rec in tl.fg_ops:
+        trace.op_isolated[rec.op_id] = rec.isolated_duration_us
+        trace.op_durations.setdefault(rec.op_id, [])
+    prev = 0
+    for it, e in enumerate(ends):
+        t = us_to_ticks(ev0.elapsed_time(e) * 1000.0)
+        t = int(comm.max_scalar(float(t), st.device))        # max over ranks
+        trace.iteration_ticks.append(t)
+        for gpu in range(n_gpus):
+            trace.busy.setdefault(gpu, []).append((prev, t))
+        trace.events.append((t, comm.rank, FG_TASK, f"iteration#{it}", "end"))
+        prev = t
+    trace.stop_tick = prev
+    trace.loss = float(loss_h.item())
+    base = baseline_fg_iteration_us or tl.predicted_fg_iteration_us
+    metrics = metrics_from_trace(trace, n_gpus, tl.global_batch, tl.bg_batch, config,
+                                 iterations, base)
+    return trace, metrics
+
+
+def run_two_phase(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
+                  bg_graph: Optional[CompGraph] = None,
+                  config: Optional[SimConfig] = None, iterations: int = 4,
+                  feedback_rounds: int = 1,
+                  baseline_fg_iteration_us: Optional[float] = None, **kw):
+    """run -> feedback_update -> run with flagged ops gating collocation
+    (reference run_two_phase, simulator.py:959-977)."""
+    config = config or SimConfig()
+    flags: frozenset = frozenset()
+    trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
+                         baseline_fg_iteration_us, **kw)
+    for _ in range(feedback_rounds):
+        new = feedback_update(trace, config, flags)
+        if new == flags:
+            break
+        flags = new
+        trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
+                             baseline_fg_iteration_us, **kw)
+    return trace, metrics, flags

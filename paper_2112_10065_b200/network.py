@@ -1,0 +1,159 @@
+"""Executable networks behind the planner's synthetic graphs.
+
+The reference's graphs carry only costs (`synth.py:86-123` for VGG-16);
+the executor needs the real layers.  ``NetSpec`` binds each graph layer
+name to a concrete op with shapes, in the same order, so a plan's
+``(layer_id, g)`` list maps 1:1 onto executable layers.
+
+VGG-16 here is the real network (conv bias, fc1 25088->4096, 138,357,544
+parameters) without dropout.  Layouts: activations NHWC,
+conv weights OHWI ([Cout][3][3][Cin]), dense weights [out][in] with fc1's
+input in NHWC-flatten order (h, w, c).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from .errors import GraphFormatError
+from .graph import CompGraph
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    name: str
+    kind: str            # conv | pool | dense
+    cin: int             # channels (conv/pool) or input features (dense)
+    cout: int
+    hw: int              # input spatial size (conv/pool); 0 for dense
+    relu: bool           # output passes through ReLU
+    in_relu: bool        # input is a ReLU output (dgrad fuses its mask)
+
+    @property
+    def out_hw(self) -> int:
+        return self.hw // 2 if self.kind == "pool" else self.hw
+
+    def in_elems(self) -> int:
+        """Input floats per sample."""
+        return self.hw * self.hw * self.cin if self.kind != "dense" else self.cin
+
+    def out_elems(self) -> int:
+        if self.kind == "dense":
+            return self.cout
+        return self.out_hw * self.out_hw * self.cout
+
+    def in_shape(self, b: int) -> tuple[int, ...]:
+        return (b, self.hw, self.hw, self.cin) if self.kind != "dense" else (b, self.cin)
+
+    def out_shape(self, b: int) -> tuple[int, ...]:
+        if self.kind == "dense":
+            return (b, self.cout)
+        return (b, self.out_hw, self.out_hw, self.cout)
+
+    def param_shapes(self) -> Optional[tuple[tuple[int, ...], tuple[int, ...]]]:
+        if self.kind == "conv":
+            return (self.cout, 3, 3, self.cin), (self.cout,)
+        if self.kind == "dense":
+            return (self.cout, self.cin), (self.cout,)
+        return None
+
+    def n_params(self) -> int:
+        ps = self.param_shapes()
+        return 0 if ps is None else math.prod(ps[0]) + math.prod(ps[1])
+
+    def fwd_flops(self) -> int:
+        """Algorithmic fwd FLOPs per sample (2 per MAC; bias/ReLU excluded)."""
+        if self.kind == "conv":
+            return 2 * 9 * self.cin * self.cout * self.hw * self.hw
+        if self.kind == "dense":
+            return 2 * self.cin * self.cout
+        return 0
+
+
+@dataclass(frozen=True)
+class NetSpec:
+    name: str
+    input_hw: int
+    input_c: int
+    classes: int
+    layers: tuple[LayerSpec, ...]
+
+    def by_name(self) -> dict[str, LayerSpec]:
+        return {l.name: l for l in self.layers}
+
+    def n_params(self) -> int:
+        return sum(l.n_params() for l in self.layers)
+
+    def train_flops_per_sample(self) -> int:
+        """fwd + dgrad + wgrad, minus the first layer's dgrad (its input is
+        the image): the roofline's algorithmic work."""
+        f = sum(l.fwd_flops() for l in self.layers)
+        return 3 * f - self.layers[0].fwd_flops()
+
+
+def vgg16() -> NetSpec:
+    layers = []
+    hw, cin = 224, 3
+    first = True
+    for stage, (cout, n) in enumerate(((64, 2), (128, 2), (256, 3), (512, 3), (512, 3)),
+                                      start=1):
+        for j in range(1, n + 1):
+            layers.append(LayerSpec(f"conv{stage}_{j}", "conv", cin, cout, hw, True,
+                                    not first))
+            first = False
+            cin = cout
+        layers.append(LayerSpec(f"pool{stage}", "pool", cout, cout, hw, False, True))
+        hw //= 2
+    feats = hw * hw * cin
+    for k, (fout, relu) in enumerate(((4096, True), (4096, True), (1000, False)), start=1):
+        layers.append(LayerSpec(f"fc{k}", "dense", feats, fout, 0, relu, True))
+        feats = fout
+    return NetSpec("vgg16", 224, 3, 1000, tuple(layers))
+
+
+_REGISTRY = {"vgg_like": vgg16}
+
+
+def net_for_graph(graph: CompGraph) -> NetSpec:
+    """The executable network behind a planner graph; layer names must
+    match the graph's non-virtual layers one for one, in order."""
+    fn = _REGISTRY.get(graph.name)
+    if fn is None:
+        raise GraphFormatError(f"no executable network registered for graph {graph.name!r}")
+    net = fn()
+    names = [l.name for l in graph.layers if not l.is_virtual]
+    if names != [l.name for l in net.layers]:
+        raise GraphFormatError(f"graph {graph.name!r} layers do not match {net.name}")
+    return net
+
+
+def init_params(net: NetSpec, seed: int = 0) -> dict[str, tuple[torch.Tensor, torch.Tensor]]:
+    """torchvision-style init on CPU (kaiming_normal fan_out/relu for convs,
+    N(0, 0.01) for dense, zero bias), deterministic in ``seed``."""
+    gen = torch.Generator().manual_seed(seed)
+    out = {}
+    for l in net.layers:
+        ps = l.param_shapes()
+        if ps is None:
+            continue
+        if l.kind == "conv":
+            std = math.sqrt(2.0 / (l.cout * 9))
+        else:
+            std = 0.01
+        w = torch.randn(ps[0], generator=gen, dtype=torch.float32) * std
+        b = torch.zeros(ps[1], dtype=torch.float32)
+        out[l.name] = (w, b)
+    return out
+
+
+def synthetic_batch(net: NetSpec, batch: int, seed: int = 0):
+    """x ~ N(0, 1) NHWC and uniform labels, on CPU."""
+    gen = torch.Generator().manual_seed(seed)
+    x = torch.randn((batch, net.input_hw, net.input_hw, net.input_c), generator=gen,
+                    dtype=torch.float32)
+    y = torch.randint(0, net.classes, (batch,), generator=gen, dtype=torch.int64)
+    return x, y.to(torch.int32)

@@ -1,0 +1,344 @@
+"""ctypes binding of libbpx (include/bpx.h) for torch CUDA tensors.
+
+Each wrapper checks dtype / device / contiguity, passes raw device pointers
+and the *current* torch CUDA stream, and turns a nonzero bpx_status_t into
+``KernelError``.  There is deliberately no CPU or PyTorch fallback: if the
+library is missing the first call raises ``ExtensionMissingError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+from .errors import ExtensionMissingError, KernelError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbpx.so")
+
+_lib = None
+
+_c_float_p = ctypes.c_void_p
+_SIGS = {
+    # name: (restype, argtypes)
+    "bpx_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "bpx_abi_version": (ctypes.c_int, []),
+    "bpx_device_supported": (ctypes.c_int, []),
+    "bpx_launch_count": (ctypes.c_longlong, []),
+    "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
+                        + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
+    "bpx_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
+                          + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_conv3x3_dgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
+    "bpx_conv3x3_wgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
+                          + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_conv3x3_wgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
+    "bpx_linear_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 4
+                       + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_linear_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 3),
+    "bpx_linear_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 3
+                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_linear_dgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 3),
+    "bpx_linear_wgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 3
+                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_linear_wgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 3),
+    "bpx_maxpool2x2_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
+                           + [ctypes.c_void_p]),
+    "bpx_maxpool2x2_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
+                           + [ctypes.c_void_p]),
+    "bpx_softmax_xent": (ctypes.c_int, [_c_float_p, ctypes.c_void_p]
+                         + [ctypes.c_int] * 3 + [_c_float_p, _c_float_p, ctypes.c_void_p]),
+    "bpx_sgd_update": (ctypes.c_int, [_c_float_p, _c_float_p, ctypes.c_size_t,
+                                      ctypes.c_float, ctypes.c_void_p]),
+    "bpx_reshard_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_void_p]),
+    "bpx_allreduce_sum_prefix": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                                ctypes.c_void_p, ctypes.c_size_t,
+                                                ctypes.c_void_p]),
+    "bpx_signal_barrier": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_uint32,
+                                          ctypes.c_void_p]),
+    "bpx_simt_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
+                             + [ctypes.c_void_p]),
+    "bpx_simt_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
+                               + [ctypes.c_void_p]),
+    "bpx_simt_conv3x3_wgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
+                               + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load_library(path: str = LIB_PATH):
+    """Load (once) and type the C-ABI; raises ExtensionMissingError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ExtensionMissingError(
+            f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError as exc:
+        raise ExtensionMissingError(f"cannot load {path}: {exc}") from exc
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def launch_count() -> int:
+    """Kernel launches issued through libbpx by this process so far."""
+    return int(load_library().bpx_launch_count())
+
+
+def _check(status: int, what: str) -> None:
+    if status != 0:
+        name = _lib.bpx_status_string(status).decode()
+        raise KernelError(f"{what} failed: {name}", status)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise KernelError("libbpx takes CUDA tensors only (no CPU fallback)")
+    if not t.is_contiguous():
+        raise KernelError("libbpx takes contiguous tensors")
+    return t.data_ptr()
+
+
+def _f32(*ts):
+    for t in ts:
+        if t is not None and t.dtype != torch.float32:
+            raise KernelError(f"expected float32, got {t.dtype}")
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """Grow-only scratch buffer shared by consecutive calls on one stream."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes: int) -> tuple[int, int]:
+        if nbytes > self.buf.numel():
+            self.buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        return (self.buf.data_ptr() if self.buf.numel() else None), self.buf.numel()
+
+    def reserve(self, nbytes: int) -> None:
+        self.get(nbytes)
+
+
+def _ws(ws: Optional[Workspace], nbytes: int, device):
+    if nbytes == 0:
+        return None, 0
+    if ws is None:
+        ws = Workspace(device)
+    return ws.get(nbytes)
+
+
+# ---------------------------------------------------------------- layers
+
+def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(x, w, bias, y)
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    need = lib.bpx_conv3x3_fwd_workspace(n, h, wd, cin, cout)
+    wp, wb = _ws(ws, need, x.device)
+    _check(lib.bpx_conv3x3_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), n, h, wd,
+                               cin, cout, int(relu), wp, wb, _stream()),
+           "bpx_conv3x3_fwd")
+    return y
+
+
+def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(dz, w, mask_src, dx)
+    n, h, wd, cout = dz.shape
+    cin = w.shape[3]
+    need = lib.bpx_conv3x3_dgrad_workspace(n, h, wd, cin, cout)
+    wp, wb = _ws(ws, need, dz.device)
+    _check(lib.bpx_conv3x3_dgrad(_ptr(dz), _ptr(w), _ptr(mask_src), _ptr(dx), n,
+                                 h, wd, cin, cout, wp, wb, _stream()),
+           "bpx_conv3x3_dgrad")
+    return dx
+
+
+def conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(x, dz, dw, dbias)
+    n, h, wd, cin = x.shape
+    cout = dz.shape[3]
+    need = lib.bpx_conv3x3_wgrad_workspace(n, h, wd, cin, cout)
+    wp, wb = _ws(ws, need, x.device)
+    _check(lib.bpx_conv3x3_wgrad(_ptr(x), _ptr(dz), _ptr(dw), _ptr(dbias), n, h,
+                                 wd, cin, cout, wp, wb, _stream()),
+           "bpx_conv3x3_wgrad")
+    return dw
+
+
+def conv_workspace_bytes(n, h, w, cin, cout) -> int:
+    lib = load_library()
+    return max(lib.bpx_conv3x3_fwd_workspace(n, h, w, cin, cout),
+               lib.bpx_conv3x3_dgrad_workspace(n, h, w, cin, cout),
+               lib.bpx_conv3x3_wgrad_workspace(n, h, w, cin, cout))
+
+
+def linear_fwd(x, w, bias, y, relu, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(x, w, bias, y)
+    b, fin = x.shape
+    fout = w.shape[0]
+    need = lib.bpx_linear_fwd_workspace(b, fin, fout)
+    wp, wb = _ws(ws, need, x.device)
+    _check(lib.bpx_linear_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), b, fin, fout,
+                              int(relu), wp, wb, _stream()), "bpx_linear_fwd")
+    return y
+
+
+def linear_dgrad(dy, w, mask_src, dx, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(dy, w, mask_src, dx)
+    b, fout = dy.shape
+    fin = w.shape[1]
+    need = lib.bpx_linear_dgrad_workspace(b, fin, fout)
+    wp, wb = _ws(ws, need, dy.device)
+    _check(lib.bpx_linear_dgrad(_ptr(dy), _ptr(w), _ptr(mask_src), _ptr(dx), b,
+                                fin, fout, wp, wb, _stream()), "bpx_linear_dgrad")
+    return dx
+
+
+def linear_wgrad(x, dy, dw, dbias, ws: Optional[Workspace] = None):
+    lib = load_library()
+    _f32(x, dy, dw, dbias)
+    b, fin = x.shape
+    fout = dy.shape[1]
+    need = lib.bpx_linear_wgrad_workspace(b, fin, fout)
+    wp, wb = _ws(ws, need, x.device)
+    _check(lib.bpx_linear_wgrad(_ptr(x), _ptr(dy), _ptr(dw), _ptr(dbias), b, fin,
+                                fout, wp, wb, _stream()), "bpx_linear_wgrad")
+    return dw
+
+
+def linear_workspace_bytes(b, fin, fout) -> int:
+    lib = load_library()
+    return max(lib.bpx_linear_fwd_workspace(b, fin, fout),
+               lib.bpx_linear_dgrad_workspace(b, fin, fout),
+               lib.bpx_linear_wgrad_workspace(b, fin, fout))
+
+
+def maxpool2x2_fwd(x, y):
+    lib = load_library()
+    _f32(x, y)
+    n, h, w, c = x.shape
+    _check(lib.bpx_maxpool2x2_fwd(_ptr(x), _ptr(y), n, h, w, c, _stream()),
+           "bpx_maxpool2x2_fwd")
+    return y
+
+
+def maxpool2x2_bwd(x, dy, dx):
+    lib = load_library()
+    _f32(x, dy, dx)
+    n, h, w, c = x.shape
+    _check(lib.bpx_maxpool2x2_bwd(_ptr(x), _ptr(dy), _ptr(dx), n, h, w, c,
+                                  _stream()), "bpx_maxpool2x2_bwd")
+    return dx
+
+
+def softmax_xent(logits, labels, b_global, loss_out, dlogits):
+    lib = load_library()
+    _f32(logits, loss_out, dlogits)
+    if labels.dtype != torch.int32:
+        raise KernelError("labels must be int32")
+    b, classes = logits.shape
+    if loss_out.numel() < b + 1:
+        raise KernelError("loss_out needs b_local + 1 floats")
+    _check(lib.bpx_softmax_xent(_ptr(logits), _ptr(labels), b, b_global, classes,
+                                _ptr(loss_out), _ptr(dlogits), _stream()),
+           "bpx_softmax_xent")
+    return loss_out
+
+
+def sgd_update(w, g, lr):
+    lib = load_library()
+    _f32(w, g)
+    _check(lib.bpx_sgd_update(_ptr(w), _ptr(g), w.numel(), float(lr), _stream()),
+           "bpx_sgd_update")
+
+
+# ---------------------------------------------------------------- comm
+
+def reshard_pull(srcs: Sequence[int], src_offsets: Sequence[int], dst: torch.Tensor,
+                 dst_offsets: Sequence[int], nbytes: Sequence[int]):
+    """Copy n_seg byte runs from (peer) device addresses into ``dst``."""
+    lib = load_library()
+    n = len(nbytes)
+    arr = lambda T, v: (T * max(n, 1))(*v)
+    _check(lib.bpx_reshard_pull(ctypes.cast(arr(ctypes.c_void_p, srcs), ctypes.c_void_p),
+                                ctypes.cast(arr(ctypes.c_size_t, src_offsets), ctypes.c_void_p),
+                                _ptr(dst),
+                                ctypes.cast(arr(ctypes.c_size_t, dst_offsets), ctypes.c_void_p),
+                                ctypes.cast(arr(ctypes.c_size_t, nbytes), ctypes.c_void_p),
+                                n, _stream()), "bpx_reshard_pull")
+
+
+def allreduce_sum_prefix(peer_ptrs: Sequence[int], out: torch.Tensor, n: int):
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(peer_ptrs))(*peer_ptrs)
+    _check(lib.bpx_allreduce_sum_prefix(ctypes.cast(arr, ctypes.c_void_p),
+                                        len(peer_ptrs), _ptr(out), int(n), _stream()),
+           "bpx_allreduce_sum_prefix")
+
+
+def signal_barrier(pad_ptrs: Sequence[int], rank: int, epoch: int):
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(pad_ptrs))(*pad_ptrs)
+    _check(lib.bpx_signal_barrier(ctypes.cast(arr, ctypes.c_void_p), rank,
+                                  len(pad_ptrs), epoch & 0xFFFFFFFF, _stream()),
+           "bpx_signal_barrier")
+
+
+# ---------------------------------------------------------------- pinned engine
+
+def simt_conv3x3_fwd(x, w, bias, y, relu=True):
+    lib = load_library()
+    n, h, wd, cin = x.shape
+    _check(lib.bpx_simt_conv3x3_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), n, h, wd,
+                                    cin, w.shape[0], int(relu), _stream()),
+           "bpx_simt_conv3x3_fwd")
+    return y
+
+
+def simt_conv3x3_dgrad(dz, w, mask_src, dx):
+    lib = load_library()
+    n, h, wd, cout = dz.shape
+    _check(lib.bpx_simt_conv3x3_dgrad(_ptr(dz), _ptr(w), _ptr(mask_src), _ptr(dx), n,
+                                      h, wd, w.shape[3], cout, _stream()),
+           "bpx_simt_conv3x3_dgrad")
+    return dx
+
+
+def simt_conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):
+    lib = load_library()
+    n, h, wd, cin = x.shape
+    cout = dz.shape[3]
+    need = lib.bpx_conv3x3_wgrad_workspace(n, h, wd, cin, cout)
+    wp, wb = _ws(ws, need, x.device)
+    _check(lib.bpx_simt_conv3x3_wgrad(_ptr(x), _ptr(dz), _ptr(dw), _ptr(dbias), n, h,
+                                      wd, cin, cout, wp, wb, _stream()),
+           "bpx_simt_conv3x3_wgrad")
+    return dw

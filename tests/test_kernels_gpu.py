@@ -1,0 +1,231 @@
+"""Per-kernel parity of libbpx against the CPU fp64 oracle (oracle/vgg_ref.py).
+
+Tolerances are normwise relative errors against fp64: fp32-accurate
+kernels (FFMA or 3xTF32) land near 1e-6; the gate is 1e-5 (TF32 alone
+would be ~1e-3 and fail)."""
+
+import math
+
+import pytest
+import torch
+
+from paper_2112_10065_b200 import ops
+from paper_2112_10065_b200.network import LayerSpec
+from oracle import vgg_ref
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+DEV = "cuda"
+
+
+def rnd(*shape, seed=0, scale=1.0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randn(shape, generator=g, dtype=torch.float32) * scale
+
+
+def relu_input(*shape, seed=0):
+    return torch.relu(rnd(*shape, seed=seed))
+
+
+# (n, h, cin, cout): every VGG-16 conv channel pair at small spatial sizes,
+# plus ragged pixel counts (M not a multiple of the 128-row tile) and n=1.
+CONV_SHAPES = [
+    (2, 16, 3, 64), (2, 16, 64, 64), (2, 12, 64, 128), (1, 10, 128, 128),
+    (2, 8, 128, 256), (3, 7, 256, 256), (2, 6, 256, 512), (2, 4, 512, 512),
+    (1, 14, 512, 512), (5, 9, 64, 64),
+]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES, ids=str)
+def test_conv_fwd(shape):
+    n, h, cin, cout = shape
+    x = rnd(n, h, h, cin, seed=1)
+    w = rnd(cout, 3, 3, cin, seed=2, scale=math.sqrt(2 / (9 * cin)))
+    b = rnd(cout, seed=3, scale=0.1)
+    spec = LayerSpec("c", "conv", cin, cout, h, True, False)
+    ref = vgg_ref.layer_fwd(spec, x, w, b)
+    y = torch.empty(n, h, h, cout, device=DEV)
+    ops.conv3x3_fwd(x.to(DEV), w.to(DEV), b.to(DEV), y, relu=True)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(y, ref) < TOL
+
+
+@pytest.mark.parametrize("shape", [s for s in CONV_SHAPES if s[2] % 4 == 0], ids=str)
+def test_conv_dgrad_masked(shape):
+    n, h, cin, cout = shape
+    x = relu_input(n, h, h, cin, seed=4)            # layer input = a ReLU output
+    w = rnd(cout, 3, 3, cin, seed=5, scale=math.sqrt(2 / (9 * cin)))
+    dz = rnd(n, h, h, cout, seed=6)
+    dx_ref, _, _ = vgg_ref.conv_grads(x, w, dz)
+    dx_ref = dx_ref * (x > 0)
+    dx = torch.empty(n, h, h, cin, device=DEV)
+    ops.conv3x3_dgrad(dz.to(DEV), w.to(DEV), x.to(DEV), dx)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(dx, dx_ref) < TOL
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES, ids=str)
+def test_conv_wgrad(shape):
+    n, h, cin, cout = shape
+    x = relu_input(n, h, h, cin, seed=7)
+    w = rnd(cout, 3, 3, cin, seed=8)
+    dz = rnd(n, h, h, cout, seed=9)
+    _, dw_ref, db_ref = vgg_ref.conv_grads(x, w, dz)
+    dw = torch.empty(cout, 3, 3, cin, device=DEV)
+    db = torch.empty(cout, device=DEV)
+    ops.conv3x3_wgrad(x.to(DEV), dz.to(DEV), dw, db)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(dw, dw_ref) < TOL
+    assert vgg_ref.normwise_rel(db, db_ref) < TOL
+
+
+def test_conv_wgrad_large_k_split():
+    # conv1_2-like reduction depth (split-K path), deterministic run to run
+    n, h, cin, cout = 4, 56, 64, 64
+    x = relu_input(n, h, h, cin, seed=10).to(DEV)
+    dz = rnd(n, h, h, cout, seed=11).to(DEV)
+    outs = []
+    for _ in range(2):
+        dw = torch.empty(cout, 3, 3, cin, device=DEV)
+        db = torch.empty(cout, device=DEV)
+        ops.conv3x3_wgrad(x, dz, dw, db)
+        outs.append((dw.clone(), db.clone()))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    _, dw_ref, db_ref = vgg_ref.conv_grads(x.cpu(), torch.zeros(cout, 3, 3, cin), dz.cpu())
+    assert vgg_ref.normwise_rel(outs[0][0], dw_ref) < TOL
+
+
+def test_conv_matches_ffma_engine():
+    # tensor-core engine vs the independent FFMA engine at a full VGG shape
+    n, h, cin, cout = 2, 56, 256, 256
+    x = relu_input(n, h, h, cin, seed=12).to(DEV)
+    w = rnd(cout, 3, 3, cin, seed=13, scale=0.03).to(DEV)
+    b = rnd(cout, seed=14).to(DEV)
+    y1 = torch.empty(n, h, h, cout, device=DEV)
+    y2 = torch.empty_like(y1)
+    ops.conv3x3_fwd(x, w, b, y1, relu=True)
+    ops.simt_conv3x3_fwd(x, w, b, y2, relu=True)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(y1, y2.double()) < TOL
+
+
+@pytest.mark.parametrize("b,fin,fout,relu", [(4, 25088, 4096, True), (32, 4096, 4096, True),
+                                             (32, 4096, 1000, False), (3, 64, 40, True),
+                                             (1, 128, 1000, False)], ids=str)
+def test_linear_fwd_bwd(b, fin, fout, relu):
+    x = relu_input(b, fin, seed=15)
+    w = rnd(fout, fin, seed=16, scale=0.01)
+    bias = rnd(fout, seed=17, scale=0.1)
+    dy = rnd(b, fout, seed=18)
+    spec = LayerSpec("f", "dense", fin, fout, 0, relu, True)
+    y_ref = vgg_ref.layer_fwd(spec, x, w, bias)
+    xd, wd = x.double(), w.double()
+    dx_ref = (dy.double() @ wd) * (x > 0)
+    dw_ref = dy.double().t() @ xd
+    db_ref = dy.double().sum(0)
+    X, W = x.to(DEV), w.to(DEV)
+    y = torch.empty(b, fout, device=DEV)
+    ops.linear_fwd(X, W, bias.to(DEV), y, relu)
+    dx = torch.empty(b, fin, device=DEV)
+    ops.linear_dgrad(dy.to(DEV), W, X, dx)
+    dw = torch.empty(fout, fin, device=DEV)
+    db = torch.empty(fout, device=DEV)
+    ops.linear_wgrad(X, dy.to(DEV), dw, db)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(y, y_ref) < TOL
+    assert vgg_ref.normwise_rel(dx, dx_ref) < TOL
+    assert vgg_ref.normwise_rel(dw, dw_ref) < TOL
+    assert vgg_ref.normwise_rel(db, db_ref) < TOL
+
+
+@pytest.mark.parametrize("n,h,c", [(2, 8, 64), (3, 14, 512), (1, 224, 64), (2, 2, 4)])
+def test_maxpool_fwd_bwd_exact(n, h, c):
+    x = relu_input(n, h, h, c, seed=19)
+    x[0, 0, 0, :] = 0.0                       # all-zero windows (ReLU ties)
+    dy = rnd(n, h // 2, h // 2, c, seed=20)
+    xr = x.double().permute(0, 3, 1, 2).requires_grad_(True)
+    yr = torch.nn.functional.max_pool2d(xr, 2, 2)
+    yr.backward(dy.double().permute(0, 3, 1, 2))
+    y = torch.empty(n, h // 2, h // 2, c, device=DEV)
+    dx = torch.empty(n, h, h, c, device=DEV)
+    ops.maxpool2x2_fwd(x.to(DEV), y)
+    ops.maxpool2x2_bwd(x.to(DEV), dy.to(DEV), dx)
+    torch.cuda.synchronize()
+    assert torch.equal(y.cpu(), yr.detach().permute(0, 2, 3, 1).float())
+    assert torch.equal(dx.cpu(), xr.grad.permute(0, 2, 3, 1).float())
+
+
+@pytest.mark.parametrize("b,bg", [(32, 32), (4, 32), (1, 8)])
+def test_softmax_xent(b, bg):
+    z = rnd(b, 1000, seed=21, scale=3.0)
+    lab = torch.randint(0, 1000, (b,), generator=torch.Generator().manual_seed(3)).int()
+    zr = z.double().requires_grad_(True)
+    l = torch.nn.functional.cross_entropy(zr, lab.long(), reduction="sum") / bg
+    l.backward()
+    loss = torch.empty(b + 1, device=DEV)
+    dz = torch.empty(b, 1000, device=DEV)
+    ops.softmax_xent(z.to(DEV), lab.to(DEV), bg, loss, dz)
+    torch.cuda.synchronize()
+    assert abs(loss[0].item() - l.item()) / abs(l.item()) < 1e-6
+    assert vgg_ref.normwise_rel(dz, zr.grad) < 1e-6
+
+
+def test_sgd_update():
+    w = rnd(1003, seed=22)
+    g = rnd(1003, seed=23)
+    W = w.to(DEV)
+    ops.sgd_update(W, g.to(DEV), 0.1)
+    torch.cuda.synchronize()
+    assert torch.allclose(W.cpu(), w - 0.1 * g, atol=0, rtol=1e-7)
+
+
+def test_reshard_pull_with_local_peers():
+    # 4 "peers" simulated as 4 buffers on one device: a g=4 -> h=1 gather of
+    # B=10 samples (ceil layout 3,3,3,1) into rank 0, then 1 -> 4 scatter.
+    from paper_2112_10065_b200.comm import reshard_moves
+    from paper_2112_10065_b200.costs import reshard_segments, shard_range
+    B, bps_f = 10, 48
+    full = rnd(B, bps_f, seed=24)
+    src = []
+    for r in range(4):
+        a, b = shard_range(B, 4, r)
+        src.append(full[a:b].clone().to(DEV))
+    dst = torch.empty(B, bps_f, device=DEV)
+    segs = [(p, q, s, n) for p, q, s, n in reshard_segments(B, 4, 1)]
+    ops.reshard_pull([src[p].data_ptr() for p, *_ in segs],
+                     [(s - p * 3) * bps_f * 4 for p, q, s, n in segs], dst,
+                     [s * bps_f * 4 for p, q, s, n in segs],
+                     [n * bps_f * 4 for *_, n in segs])
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), full)
+    # scatter back with the moves this rank-r view computes
+    for r in range(4):
+        a, b = shard_range(B, 4, r)
+        out = torch.empty(b - a, bps_f, device=DEV)
+        segs = [sg for sg in reshard_segments(B, 1, 4) if sg[1] == r]
+        ops.reshard_pull([dst.data_ptr()] * len(segs), [s * bps_f * 4 for _, _, s, _ in segs],
+                         out, [(s - r * 3) * bps_f * 4 for _, _, s, _ in segs],
+                         [n * bps_f * 4 for *_, n in segs])
+        torch.cuda.synchronize()
+        assert torch.equal(out.cpu(), full[a:b])
+
+
+def test_allreduce_prefix_with_local_peers():
+    n = 1 << 20
+    bufs = [rnd(n, seed=30 + r).to(DEV) for r in range(4)]
+    for g in (2, 4):
+        out = torch.empty(n, device=DEV)
+        ops.allreduce_sum_prefix([b.data_ptr() for b in bufs[:g]], out, n)
+        torch.cuda.synchronize()
+        ref = bufs[0].clone()
+        for r in range(1, g):
+            ref += bufs[r]
+        assert torch.equal(out, ref)        # same fixed rank order
+
+
+def test_signal_barrier_single_rank():
+    pad = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ops.signal_barrier([pad.data_ptr()], 0, 7)
+    torch.cuda.synchronize()
+    assert pad.item() == 7
