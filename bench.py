@@ -226,7 +226,12 @@ def bench_ours(args):
         else:
             s = starts.get((key, "start" if what == "end" else "bstart"))
             if s is not None:
-                op_ms[key] = op_ms.get(key, 0.0) + s.elapsed_time(ev)
+                try:
+                    op_ms[key] = op_ms.get(key, 0.0) + s.elapsed_time(ev)
+                except Exception as exc:      # keep the bench line alive
+                    sys.stderr.write(f"event timing unavailable: {exc}\n")
+                    op_ms = {}
+                    break
     gemm_ms = sum(v for (k, i), v in op_ms.items()
                   if k == "compute" and st.layers[i].spec.kind in ("conv", "dense"))
     flops_step = 0

@@ -199,7 +199,8 @@ class BurstStep:
 
     def _mark(self, tag):
         if self.op_events is not None:
-            ev = torch.cuda.Event(enable_timing=True)
+            # external=True: a real event-record node when captured in a graph
+            ev = torch.cuda.Event(enable_timing=True, external=True)
             ev.record()
             self.op_events.append((tag, ev))
 
