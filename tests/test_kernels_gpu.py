@@ -1,8 +1,8 @@
 """Per-kernel parity of libbpx against the CPU fp64 oracle (oracle/vgg_ref.py).
 
-Tolerances are normwise relative errors against fp64: fp32-accurate
-kernels (FFMA or 3xTF32) land near 1e-6; the gate is 1e-5 (TF32 alone
-would be ~1e-3 and fail)."""
+Gate: normwise relative error against fp64 <= max(2e-6, 4 x the error of
+the same op computed in fp32 on the CPU).  fp32-accurate kernels (FFMA or
+the 3xTF32 tensor-core split) pass; plain TF32 (~1e-3) fails by ~100x."""
 
 import math
 
@@ -14,8 +14,13 @@ from paper_2112_10065_b200.network import LayerSpec
 from oracle import vgg_ref
 
 pytestmark = pytest.mark.gpu
-TOL = 1e-5
 DEV = "cuda"
+
+
+def close(got, ref64, ref32):
+    e = vgg_ref.normwise_rel(got, ref64)
+    gate = max(2e-6, 4 * vgg_ref.normwise_rel(ref32, ref64))
+    assert e <= gate, (e, gate)
 
 
 def rnd(*shape, seed=0, scale=1.0):
@@ -44,10 +49,11 @@ def test_conv_fwd(shape):
     b = rnd(cout, seed=3, scale=0.1)
     spec = LayerSpec("c", "conv", cin, cout, h, True, False)
     ref = vgg_ref.layer_fwd(spec, x, w, b)
+    ref32 = vgg_ref.layer_fwd(spec, x, w, b, dtype=torch.float32)
     y = torch.empty(n, h, h, cout, device=DEV)
     ops.conv3x3_fwd(x.to(DEV), w.to(DEV), b.to(DEV), y, relu=True)
     torch.cuda.synchronize()
-    assert vgg_ref.normwise_rel(y, ref) < TOL
+    close(y, ref, ref32)
 
 
 @pytest.mark.parametrize("shape", [s for s in CONV_SHAPES if s[2] % 4 == 0], ids=str)
@@ -58,10 +64,11 @@ def test_conv_dgrad_masked(shape):
     dz = rnd(n, h, h, cout, seed=6)
     dx_ref, _, _ = vgg_ref.conv_grads(x, w, dz)
     dx_ref = dx_ref * (x > 0)
+    dx32 = vgg_ref.conv_grads(x, w, dz, torch.float32)[0] * (x > 0)
     dx = torch.empty(n, h, h, cin, device=DEV)
     ops.conv3x3_dgrad(dz.to(DEV), w.to(DEV), x.to(DEV), dx)
     torch.cuda.synchronize()
-    assert vgg_ref.normwise_rel(dx, dx_ref) < TOL
+    close(dx, dx_ref, dx32)
 
 
 @pytest.mark.parametrize("shape", CONV_SHAPES, ids=str)
@@ -71,12 +78,13 @@ def test_conv_wgrad(shape):
     w = rnd(cout, 3, 3, cin, seed=8)
     dz = rnd(n, h, h, cout, seed=9)
     _, dw_ref, db_ref = vgg_ref.conv_grads(x, w, dz)
+    _, dw32, db32 = vgg_ref.conv_grads(x, w, dz, torch.float32)
     dw = torch.empty(cout, 3, 3, cin, device=DEV)
     db = torch.empty(cout, device=DEV)
     ops.conv3x3_wgrad(x.to(DEV), dz.to(DEV), dw, db)
     torch.cuda.synchronize()
-    assert vgg_ref.normwise_rel(dw, dw_ref) < TOL
-    assert vgg_ref.normwise_rel(db, db_ref) < TOL
+    close(dw, dw_ref, dw32)
+    close(db, db_ref, db32)
 
 
 def test_conv_wgrad_large_k_split():
@@ -93,7 +101,9 @@ def test_conv_wgrad_large_k_split():
     torch.cuda.synchronize()
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     _, dw_ref, db_ref = vgg_ref.conv_grads(x.cpu(), torch.zeros(cout, 3, 3, cin), dz.cpu())
-    assert vgg_ref.normwise_rel(outs[0][0], dw_ref) < TOL
+    _, dw32, _ = vgg_ref.conv_grads(x.cpu(), torch.zeros(cout, 3, 3, cin), dz.cpu(),
+                                    torch.float32)
+    close(outs[0][0], dw_ref, dw32)
 
 
 def test_conv_matches_ffma_engine():
@@ -107,7 +117,11 @@ def test_conv_matches_ffma_engine():
     ops.conv3x3_fwd(x, w, b, y1, relu=True)
     ops.simt_conv3x3_fwd(x, w, b, y2, relu=True)
     torch.cuda.synchronize()
-    assert vgg_ref.normwise_rel(y1, y2.double()) < TOL
+    spec = LayerSpec("c", "conv", cin, cout, h, True, False)
+    ref = vgg_ref.layer_fwd(spec, x.cpu(), w.cpu(), b.cpu())
+    ref32 = vgg_ref.layer_fwd(spec, x.cpu(), w.cpu(), b.cpu(), dtype=torch.float32)
+    close(y1, ref, ref32)
+    close(y2, ref, ref32)
 
 
 @pytest.mark.parametrize("b,fin,fout,relu", [(4, 25088, 4096, True), (32, 4096, 4096, True),
@@ -133,10 +147,12 @@ def test_linear_fwd_bwd(b, fin, fout, relu):
     db = torch.empty(fout, device=DEV)
     ops.linear_wgrad(X, dy.to(DEV), dw, db)
     torch.cuda.synchronize()
-    assert vgg_ref.normwise_rel(y, y_ref) < TOL
-    assert vgg_ref.normwise_rel(dx, dx_ref) < TOL
-    assert vgg_ref.normwise_rel(dw, dw_ref) < TOL
-    assert vgg_ref.normwise_rel(db, db_ref) < TOL
+    y32 = vgg_ref.layer_fwd(spec, x, w, bias, dtype=torch.float32)
+    dx32 = (dy @ w) * (x > 0)
+    close(y, y_ref, y32)
+    close(dx, dx_ref, dx32)
+    close(dw, dw_ref, dy.t() @ x)
+    close(db, db_ref, dy.sum(0))
 
 
 @pytest.mark.parametrize("n,h,c", [(2, 8, 64), (3, 14, 512), (1, 224, 64), (2, 2, 4)])
