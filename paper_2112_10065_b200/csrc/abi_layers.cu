@@ -9,7 +9,8 @@ using namespace bpx;
 extern "C" {
 
 size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
-  return tc_conv_fwd_ws(n, h, w_, cin, cout);
+  size_t a = tc_conv_fwd_ws(n, h, w_, cin, cout), b = ts_conv_ws(cin, cout);
+  return a > b ? a : b;
 }
 
 bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, float* y,
@@ -18,13 +19,16 @@ bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, 
   BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (ts_conv_ok(cin, cout))
+    return ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
   if (tc_conv_fwd_ok(n, h, w_, cin, cout))
     return tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
   return simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
 }
 
 size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
-  return tc_conv_dgrad_ws(n, h, w_, cin, cout);
+  size_t a = tc_conv_dgrad_ws(n, h, w_, cin, cout), b = ts_conv_ws(cin, cout);
+  return a > b ? a : b;
 }
 
 bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mask_src,
@@ -33,6 +37,8 @@ bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mas
   BPX_CHECK_ARG(dz && w && dx && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (ts_conv_ok(cin, cout))
+    return ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_dgrad_ok(n, h, w_, cin, cout))
     return tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
   return simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st);
@@ -41,7 +47,8 @@ bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mas
 size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
   size_t a = simt_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t b = tc_conv_wgrad_ws(n, h, w_, cin, cout);
-  return a > b ? a : b;
+  size_t c = wg_conv_ws(n, h, w_, cin, cout);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
 bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float* dbias,
@@ -50,6 +57,8 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   BPX_CHECK_ARG(x && dz && dw && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(ws || ws_bytes == 0);
   cudaStream_t st = as_stream(stream);
+  if (wg_conv_ok(cin, cout))
+    return wg_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_wgrad_ok(n, h, w_, cin, cout))
     return tc_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   return simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);

@@ -33,3 +33,26 @@ bpx_status_t tc_linear_wgrad(const float* x, const float* dy, float* dw, float* 
                              int b, int in, int out, void* ws, size_t ws_bytes,
                              cudaStream_t st);
 }  // namespace bpx
+
+// TS engine (tc_ts.cu): conv fwd / dgrad with A in TMEM, B as a pre-split
+// weight image loaded by cp.async.bulk.
+namespace bpx {
+bool ts_conv_ok(int cin, int cout);
+size_t ts_conv_ws(int cin, int cout);
+bpx_status_t ts_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
+                         int h, int w_, int cin, int cout, int relu, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+bpx_status_t ts_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
+                           int n, int h, int w_, int cin, int cout, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
+}  // namespace bpx
+
+// Weight-gradient engine (tc_wgrad.cu): A = dz^T in TMEM, B = im2col(x) in
+// the MN-major shared-memory layout, split-K over pixels.
+namespace bpx {
+bool wg_conv_ok(int cin, int cout);
+size_t wg_conv_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t wg_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias, int n,
+                           int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+}  // namespace bpx
