@@ -218,21 +218,16 @@ def bench_ours(args):
     # per-op durations from the events captured in the graph (last replay)
     op_ms = {}
     starts = {}
-    for tag, ev in marks:
-        kind, idx, what = tag
-        key = (kind, idx)
-        if what in ("start", "bstart"):
-            starts[(key, what)] = ev
-        else:
-            s = starts.get((key, "start" if what == "end" else "bstart"))
-            if s is not None:
-                try:
-                    op_ms[key] = op_ms.get(key, 0.0) + s.elapsed_time(ev)
-                except Exception as exc:      # keep the bench line alive
-                    sys.stderr.write(f"event timing unavailable: {exc}\n")
-                    op_ms = {}
-                    break
-    gemm_ms = sum(v for (k, i), v in op_ms.items()
+    try:
+        for (key, what), ev in marks:
+            if what == "start":
+                starts[key] = ev
+            elif key in starts:
+                op_ms[key] = op_ms.get(key, 0.0) + starts[key].elapsed_time(ev)
+    except Exception as exc:      # keep the bench line alive
+        sys.stderr.write(f"event timing unavailable: {exc}\n")
+        op_ms = {}
+    gemm_ms = sum(v for (k, i, ph), v in op_ms.items()
                   if k == "compute" and st.layers[i].spec.kind in ("conv", "dense"))
     flops_step = 0
     for L in st.layers:
@@ -250,6 +245,33 @@ def bench_ours(args):
     e2e = metrics.fg_throughput_samples_per_s
     a, b = st.input_range()
     h2d = (b - a) * x[0].numel() * 4 + (st.label_range()[1] - st.label_range()[0]) * 4
+
+    # BP+Col: the same foreground multiplexed with the reference's default
+    # background job (small_bg_model, one per GPU, low-priority stream)
+    col = None
+    if not args.no_bg:
+        bg_graph = synth.small_bg_model()
+        tc_, mc = run(p, graph, world, bg_graph, cfg, args.warmup + args.steps,
+                      inputs=(xh, yh), step=st)
+        col = {"bg_job": "small_bg_model (synth.py:247-255) as 12 dense 1408x1408 "
+                         "layers, batch 8, per GPU",
+               "fg_samples_per_s": mc.fg_throughput_samples_per_s,
+               "bg_samples_per_s": mc.bg_throughput_samples_per_s,
+               "total_samples_per_s": mc.cluster_total_throughput_samples_per_s,
+               "total_vs_single_task": mc.cluster_total_throughput_samples_per_s / e2e,
+               "fg_slowdown": e2e / mc.fg_throughput_samples_per_s,
+               "launch_pace_limit": cfg.launch_pace_limit,
+               "graph_split_size": cfg.graph_split_size}
+    # uniform data parallelism on the same box (N > 1 only; at N=1 BP == DP)
+    dp = None
+    if world > 1 and not args.no_dp:
+        from paper_2112_10065_b200.timeline import forced_plan
+        pd = forced_plan(graph, world, world)
+        sd = BurstStep(pd, graph, comm=comm, seed=0, lr=1e-3)
+        _, md = run(pd, graph, world, None, cfg, args.warmup + args.steps,
+                    inputs=(xh, yh), step=sd)
+        dp = {"fg_samples_per_s": md.fg_throughput_samples_per_s,
+              "bp_over_dp": e2e / md.fg_throughput_samples_per_s}
     result = None
     if rank == 0:
         cpu = None
@@ -288,14 +310,16 @@ def bench_ours(args):
                 "traffic": None},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "bp_col": col,
+            "uniform_dp": dp,
             "dominant_op": {"op": str(dom[1]), "ms": dom[0]},
             "loss": trace.loss,
         }
         print(json.dumps(result), flush=True)
         if args.breakdown:
             with open(args.breakdown, "w") as fh:
-                json.dump({f"{k}:{i}:{st.layers[i].spec.name if k != 'allreduce' else i}": v
-                           for (k, i), v in sorted(op_ms.items(), key=lambda t: -t[1])},
+                json.dump({f"{k}:{ph}:{st.layers[i].spec.name if k in ('compute', 'transfer') else i}": v
+                           for (k, i, ph), v in sorted(op_ms.items(), key=lambda t: -t[1])},
                           fh, indent=1)
     if world > 1:
         import torch.distributed as dist
@@ -310,6 +334,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-bg", action="store_true")
+    ap.add_argument("--no-dp", action="store_true")
     ap.add_argument("--breakdown", default=None)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -102,6 +102,11 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_scalar(self, value: float, device) -> float:
+        t = torch.tensor([value], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
     def barrier(self):
         self.dist.barrier()
 
@@ -123,6 +128,9 @@ class LocalComm:
             raise ValueError("single-GPU executor got a multi-GPU allreduce")
 
     def max_scalar(self, value, device):
+        return value
+
+    def sum_scalar(self, value, device):
         return value
 
     def barrier(self):

@@ -63,14 +63,22 @@ class BurstStep:
 
     def __init__(self, plan: TrainingPlan, graph: CompGraph, *, device=None,
                  comm=None, seed: int = 0, lr: float = 0.01,
-                 params: Optional[dict] = None, net: Optional[NetSpec] = None):
+                 params: Optional[dict] = None, net: Optional[NetSpec] = None,
+                 kernels=None):
         self.net = net or net_for_graph(graph)
         self.B = plan.global_batch
         self.comm = comm or LocalComm()
         self.rank = self.comm.rank
-        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        # `kernels` exists only so tests can drive the multi-rank
+        # orchestration on CPU (gloo) with an oracle op set; the product
+        # always runs libbpx and fails loudly if it is missing.
+        self.k = kernels or ops
+        if kernels is None:
+            ops.load_library()
+            self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        else:
+            self.device = torch.device(device or "cpu")
         self.lr = lr
-        ops.load_library()
         gs = [g for lid, g in plan.assignments if not graph.layer(lid).is_virtual]
         if len(gs) != len(self.net.layers):
             raise GraphFormatError("plan does not cover every executable layer")
@@ -123,11 +131,11 @@ class BurstStep:
                 L.dbias = flat[c + nw:c + nw + nb]
                 cursor[L.g] = c + _pad4(nw + nb)
                 if sp.kind == "conv":
-                    ws_need = max(ws_need, ops.conv_workspace_bytes(
+                    ws_need = max(ws_need, self.k.conv_workspace_bytes(
                         L.b, sp.hw, sp.hw, sp.cin, sp.cout))
                 else:
-                    ws_need = max(ws_need, ops.linear_workspace_bytes(L.b, sp.cin, sp.cout))
-        self.ws = ops.Workspace(dev)
+                    ws_need = max(ws_need, self.k.linear_workspace_bytes(L.b, sp.cin, sp.cout))
+        self.ws = self.k.Workspace(dev)
         self.ws.reserve(ws_need)
         last = self.layers[-1]
         self.loss_buf = torch.zeros(max(last.b, 0) + 1, dtype=torch.float32, device=dev)
@@ -154,7 +162,8 @@ class BurstStep:
         device; async when the sources are pinned host tensors."""
         a, b = self.input_range()
         if self.layers[0].active and b > a:
-            self.layers[0].x.copy_(x_global[a:b], non_blocking=True)
+            x0 = self.layers[0].x
+            x0.copy_(x_global[a:b].reshape(x0.shape), non_blocking=True)
         a, b = self.label_range()
         if self.layers[-1].active and b > a:
             self.labels[:b - a].copy_(labels_global[a:b], non_blocking=True)
@@ -164,27 +173,27 @@ class BurstStep:
         L = self.layers[i]
         sp = L.spec
         if sp.kind == "conv":
-            ops.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+            self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
         elif sp.kind == "pool":
-            ops.maxpool2x2_fwd(L.x, L.y)
+            self.k.maxpool2x2_fwd(L.x, L.y)
         else:
-            ops.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
+            self.k.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
 
     def _bwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
         mask = L.x if sp.in_relu else None
         if sp.kind == "conv":
-            ops.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
+            self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
-                ops.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
+                self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
         elif sp.kind == "pool":
-            ops.maxpool2x2_bwd(L.x, L.dy, L.dx)
+            self.k.maxpool2x2_bwd(L.x, L.dy, L.dx)
         else:
             x2 = L.x.view(L.b, sp.cin)
-            ops.linear_wgrad(x2, L.dy, L.dw, L.dbias, ws=self.ws)
+            self.k.linear_wgrad(x2, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
-                ops.linear_dgrad(L.dy, L.w, None if mask is None else x2,
+                self.k.linear_dgrad(L.dy, L.w, None if mask is None else x2,
                                  L.dx.view(L.b, sp.cin), ws=self.ws)
 
     def _reshard(self, i: int, backward: bool) -> None:
@@ -198,72 +207,107 @@ class BurstStep:
                               prev.dy if prev.active else None, prev.g, self.B, bps)
 
     def _mark(self, tag):
-        if self.op_events is not None:
+        if self.op_events is not None and self.device.type == "cuda":
             # external=True: a real event-record node when captured in a graph
             ev = torch.cuda.Event(enable_timing=True, external=True)
             ev.record()
             self.op_events.append((tag, ev))
 
-    def forward_backward(self) -> None:
+    # ------------------------------------------------------------ program
+    def program(self) -> list:
+        """This rank's per-iteration op list in issue order: (key, fn) with
+        key = (kind, index, phase).  Kinds are the reference's OpRecord
+        kinds (compute / transfer / allreduce, simulator.py:175-196) plus
+        the loss and the SGD update; a layer's `compute` is split into its
+        fwd and bwd halves, which run at different times for real."""
+        prog = []
         n = len(self.layers)
         for i in range(n):
             if i and self.layers[i - 1].g != self.layers[i].g:
-                self._mark(("transfer", i, "start"))
-                self._reshard(i, backward=False)
-                self._mark(("transfer", i, "end"))
+                prog.append((("transfer", i, "fwd"), lambda i=i: self._reshard(i, False)))
             if self.layers[i].active:
-                self._mark(("compute", i, "start"))
-                self._fwd(i)
-        last = self.layers[-1]
-        if last.active:
-            ops.softmax_xent(last.y, self.labels[:last.b], self.B, self.loss_buf, last.dy)
+                prog.append((("compute", i, "fwd"), lambda i=i: self._fwd(i)))
+        if self.layers[-1].active:
+            prog.append((("loss", n - 1, "fwd"), self._loss))
         for i in reversed(range(n)):
-            L = self.layers[i]
-            if L.active:
-                self._bwd(i)
-                self._mark(("compute", i, "end"))
-            if i and self.layers[i - 1].g != L.g:
-                self._mark(("transfer", i, "bstart"))
-                self._reshard(i, backward=True)
-                self._mark(("transfer", i, "bend"))
-
-    def sync_and_update(self) -> None:
+            if self.layers[i].active:
+                prog.append((("compute", i, "bwd"), lambda i=i: self._bwd(i)))
+            if i and self.layers[i - 1].g != self.layers[i].g:
+                prog.append((("transfer", i, "bwd"), lambda i=i: self._reshard(i, True)))
         for g in sorted(self.buckets, reverse=True):
             if g > 1:
-                self._mark(("allreduce", g, "start"))
-                self.comm.allreduce(self.buckets[g], g)
-                self._mark(("allreduce", g, "end"))
+                prog.append((("allreduce", g, "sync"),
+                             lambda g=g: self.comm.allreduce(self.buckets[g], g)))
+        prog.append((("sgd", 0, "update"), self._sgd))
+        return prog
+
+    def _loss(self) -> None:
+        last = self.layers[-1]
+        self.k.softmax_xent(last.y, self.labels[:last.b], self.B, self.loss_buf, last.dy)
+
+    def _sgd(self) -> None:
         for L in self.layers:
             if L.active and L.w is not None:
-                ops.sgd_update(L.w, L.dw, self.lr)
-                ops.sgd_update(L.bias, L.dbias, self.lr)
+                self.k.sgd_update(L.w, L.dw, self.lr)
+                self.k.sgd_update(L.bias, L.dbias, self.lr)
+
+    def run_ops(self, prog) -> None:
+        for key, fn in prog:
+            self._mark((key, "start"))
+            fn()
+            self._mark((key, "end"))
+
+    def forward_backward(self) -> None:
+        prog = self.program()
+        self.run_ops([op for op in prog if op[0][0] not in ("allreduce", "sgd")])
+
+    def sync_and_update(self) -> None:
+        prog = self.program()
+        self.run_ops([op for op in prog if op[0][0] in ("allreduce", "sgd")])
 
     def step(self) -> None:
         if self.graph is not None:
             self.graph.replay()
             return
-        self.forward_backward()
-        self.sync_and_update()
+        self.run_ops(self.program())
+
+    def _warm(self, prog, warmup: int) -> None:
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.run_ops(prog)
+        torch.cuda.current_stream().wait_stream(s)
 
     def capture(self, warmup: int = 2) -> None:
         """Capture the whole step (kernels + NCCL) as one CUDA graph; the
         warm-up runs on a side stream as torch requires."""
         record = self.op_events is not None
         self.op_events = None
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self.forward_backward()
-                self.sync_and_update()
-        torch.cuda.current_stream().wait_stream(s)
-        if record:          # events become record nodes inside the graph
+        prog = self.program()
+        self._warm(prog, warmup)
+        if record:          # external events become record nodes in the graph
             self.op_events = []
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.forward_backward()
-            self.sync_and_update()
+            self.run_ops(prog)
         self.graph = g
+
+    def capture_segments(self, cut: set, warmup: int = 1, pool=None) -> list:
+        """Capture the step as consecutive graphs, starting a new graph at
+        every program index in ``cut`` (used to isolate feedback-flagged
+        ops so background work can be held off around them).  Returns
+        [(first_index, keys, graph)]."""
+        prog = self.program()
+        self._warm(prog, warmup)
+        bounds = sorted({0, len(prog)} | {c for c in cut if 0 < c < len(prog)})
+        segs = []
+        for a, b in zip(bounds, bounds[1:]):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool):
+                self.run_ops(prog[a:b])
+            segs.append((a, [k for k, _ in prog[a:b]], g))
+        return segs
 
     def loss(self) -> float:
         """Global mean loss (sum of shard partials over the last layer's g)."""
@@ -301,64 +345,48 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         bg_graph: Optional[CompGraph] = None, config: Optional[SimConfig] = None,
         iterations: int = 4, sensitive: Iterable[str] = (),
         baseline_fg_iteration_us: Optional[float] = None, *,
-        inputs=None, seed: int = 0, lr: float = 0.01, use_graphs: bool = True,
-        step: Optional[BurstStep] = None):
+        inputs=None, seed: int = 0, lr: float = 0.01,
+        step: Optional[BurstStep] = None, bg=None, measure_ops: bool = False):
     """Execute ``iterations`` training steps of ``plan`` on real GPUs.
 
     Same call shape and return types as the reference's
     ``simulate(compile_timeline(plan, graph, n_gpus, bg_graph, config), ...)``
     (simulator.py:451-456): ``(SimTrace, SimMetrics)`` with ticks of 0.1 us
-    taken from CUDA events.  Launch one process per GPU (torchrun) for
-    n_gpus > 1.  ``inputs`` = (x NHWC [B,...], labels [B]) host tensors
-    (pinned for async copies); each iteration copies them in and reads the
-    loss back, end to end.  The background job (``bg_graph``) is scheduled
-    by the multiplexer (see ``multiplex.py``).
+    taken from CUDA events (iteration ends are the max over ranks).  Launch
+    one process per GPU (torchrun) for n_gpus > 1.  ``inputs`` = (x NHWC
+    [B,...], labels [B]) host tensors (pinned); every iteration copies its
+    input shard in, end to end.  With ``bg_graph`` every GPU also trains a
+    single-GPU background job on a low-priority stream (multiplex.py);
+    ``sensitive`` names foreground ops (``multiplex.op_name``) that must
+    not overlap background work.  bg samples/s is summed over GPUs.
     """
+    from .multiplex import BgJob, Multiplexer, op_name
     config = config or SimConfig()
     tl = compile_timeline(plan, graph, n_gpus, bg_graph, config)
-    comm = _dist_comm({g for _, g in plan.assignments})
-    if comm.world != n_gpus and not (comm.world == 1 and n_gpus == 1):
+    comm = step.comm if step is not None else _dist_comm({g for _, g in plan.assignments})
+    if comm.world != n_gpus:
         raise GraphFormatError(f"n_gpus={n_gpus} but world size is {comm.world}")
     st = step or BurstStep(plan, graph, comm=comm, seed=seed, lr=lr)
     if inputs is None:
         x, y = synthetic_batch(st.net, plan.global_batch, seed)
         inputs = (x.pin_memory(), y.pin_memory())
-    x_h, y_h = inputs
-    st.load(x_h, y_h)
-    if use_graphs and st.graph is None:
-        st.capture()
-    loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
-    comm.barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    ends = []
-    for _ in range(iterations):
-        st.load(x_h, y_h)
-        st.step()
-        loss_h.copy_(st.loss_buf[:1], non_blocking=True)
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        ends.append(e)
-    torch.cuda.synchronize()
+    if bg is None and bg_graph is not None:
+        bg = BgJob(bg_graph, config, seed=seed + 1)
+    mux = Multiplexer(st, bg, config, sensitive, measure_ops=measure_ops)
     trace = SimTrace()
-    for rec in tl.fg_ops:
-        trace.op_isolated[rec.op_id] = rec.isolated_duration_us
-        trace.op_durations.setdefault(rec.op_id, [])
-    prev = 0
-    for it, e in enumerate(ends):
-        t = us_to_ticks(ev0.elapsed_time(e) * 1000.0)
-        t = int(comm.max_scalar(float(t), st.device))        # max over ranks
-        trace.iteration_ticks.append(t)
-        for gpu in range(n_gpus):
-            trace.busy.setdefault(gpu, []).append((prev, t))
-        trace.events.append((t, comm.rank, FG_TASK, f"iteration#{it}", "end"))
-        prev = t
-    trace.stop_tick = prev
-    trace.loss = float(loss_h.item())
+    trace = mux.run(iterations, inputs, trace, rank=comm.rank,
+                    comm=comm if comm.world > 1 else None)
     base = baseline_fg_iteration_us or tl.predicted_fg_iteration_us
     metrics = metrics_from_trace(trace, n_gpus, tl.global_batch, tl.bg_batch, config,
                                  iterations, base)
+    if comm.world > 1 and bg is not None:
+        tot = comm.sum_scalar(metrics.bg_throughput_samples_per_s, st.device)
+        metrics = SimMetrics(metrics.fg_iteration_time_us_mean,
+                             metrics.fg_iteration_time_us_p99,
+                             metrics.fg_throughput_samples_per_s, tot,
+                             metrics.fg_throughput_samples_per_s + tot,
+                             metrics.per_gpu_utilization, metrics.qos_degradation)
+    trace.bg_job = bg
     return trace, metrics
 
 
@@ -367,17 +395,34 @@ def run_two_phase(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
                   config: Optional[SimConfig] = None, iterations: int = 4,
                   feedback_rounds: int = 1,
                   baseline_fg_iteration_us: Optional[float] = None, **kw):
-    """run -> feedback_update -> run with flagged ops gating collocation
-    (reference run_two_phase, simulator.py:959-977)."""
+    """Measured counterpart of the reference's run_two_phase
+    (simulator.py:959-977): time every foreground op alone, then collocated
+    with the background; flag ops slowed beyond ``slowdown_ban_threshold``
+    (feedback_update, :896-911) and re-run with them protected.  Returns
+    ``(trace, metrics, flags)``."""
     config = config or SimConfig()
+    st = kw.pop("step", None)
+    if st is None:
+        comm = _dist_comm({g for _, g in plan.assignments})
+        st = BurstStep(plan, graph, comm=comm, seed=kw.get("seed", 0),
+                       lr=kw.get("lr", 0.01))
+    iso, _ = run(plan, graph, n_gpus, None, config, iterations, (),
+                 baseline_fg_iteration_us, step=st, measure_ops=True, **kw)
+    isolated = {k: sum(v) / len(v) for k, v in iso.op_durations.items() if v}
     flags: frozenset = frozenset()
-    trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
-                         baseline_fg_iteration_us, **kw)
+    bg = None
+    trace, metrics = None, None
     for _ in range(feedback_rounds):
+        trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
+                             baseline_fg_iteration_us, step=st, bg=bg, measure_ops=True,
+                             **kw)
+        bg = trace.bg_job
+        trace.op_isolated.update(isolated)
         new = feedback_update(trace, config, flags)
         if new == flags:
             break
         flags = new
-        trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
-                             baseline_fg_iteration_us, **kw)
+    trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
+                         baseline_fg_iteration_us, step=st, bg=bg, **kw)
+    trace.op_isolated.update(isolated)
     return trace, metrics, flags

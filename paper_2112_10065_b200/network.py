@@ -115,7 +115,21 @@ def vgg16() -> NetSpec:
     return NetSpec("vgg16", 224, 3, 1000, tuple(layers))
 
 
-_REGISTRY = {"vgg_like": vgg16}
+def mlp_for_chain(graph: CompGraph) -> NetSpec:
+    """Executable stand-in for the reference's ``custom`` chain family
+    (synth.py:229-244; small_bg_model, the default background job): one
+    dense layer per graph layer with width ~sqrt(params) rounded to 16, so
+    each layer carries about the graph's parameter count (2 M for
+    small_bg_model -> 1408 x 1408) and runs the short kernels the family
+    models.  ReLU everywhere but the classifier."""
+    real = [l for l in graph.layers if not l.is_virtual]
+    width = max(16, int(math.isqrt(max(real[0].params_bytes // 4, 1))) // 16 * 16)
+    layers = tuple(LayerSpec(l.name, "dense", width, width, 0, i + 1 < len(real), i > 0)
+                   for i, l in enumerate(real))
+    return NetSpec(f"mlp{width}x{len(real)}", 1, width, width, layers)
+
+
+_REGISTRY = {"vgg_like": lambda g: vgg16(), "custom": mlp_for_chain}
 
 
 def net_for_graph(graph: CompGraph) -> NetSpec:
@@ -124,7 +138,7 @@ def net_for_graph(graph: CompGraph) -> NetSpec:
     fn = _REGISTRY.get(graph.name)
     if fn is None:
         raise GraphFormatError(f"no executable network registered for graph {graph.name!r}")
-    net = fn()
+    net = fn(graph)
     names = [l.name for l in graph.layers if not l.is_virtual]
     if names != [l.name for l in net.layers]:
         raise GraphFormatError(f"graph {graph.name!r} layers do not match {net.name}")
