@@ -13,8 +13,8 @@ Two exchange steps exist:
 ``TorchComm`` implements both with torch.distributed point-to-point and
 prefix sub-groups (NCCL over NVLink on B200; gloo in the CPU tests, where
 the same code path and index map are exercised with world_size 2).
-``PeerComm`` implements them with the libbpx P2P kernels over peer-mapped
-buffers (``bpx_reshard_pull`` / ``bpx_allreduce_sum_prefix``).
+The libbpx P2P kernels (``bpx_reshard_pull`` / ``bpx_allreduce_sum_prefix``)
+are the peer-memory alternative (PeerComm).
 """
 
 from __future__ import annotations
