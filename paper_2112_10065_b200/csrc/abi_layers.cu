@@ -48,7 +48,10 @@ size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
   size_t a = simt_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t b = tc_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t c = wg_conv_ws(n, h, w_, cin, cout);
-  return a > b ? (a > c ? a : c) : (b > c ? b : c);
+  size_t d = wgt_conv_ws(n, h, w_, cin, cout);
+  size_t m = a > b ? a : b;
+  m = m > c ? m : c;
+  return m > d ? m : d;
 }
 
 bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float* dbias,
@@ -57,6 +60,9 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   BPX_CHECK_ARG(x && dz && dw && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(ws || ws_bytes == 0);
   cudaStream_t st = as_stream(stream);
+  if (wgt_conv_ok(cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
+      (!dbias || aligned16(dbias)))
+    return wgt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (wg_conv_ok(cin, cout))
     return wg_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_wgrad_ok(n, h, w_, cin, cout))

@@ -56,3 +56,13 @@ bpx_status_t wg_conv_wgrad(const float* x, const float* dz, float* dw, float* db
                            int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
                            cudaStream_t st);
 }  // namespace bpx
+
+// TMA-fed weight-gradient engine (tc_wgt.cu): A = im2col(x)^T and B = dz as
+// 4-D TMA boxes (MN-major, SWIZZLE_128B_ATOM_32B), A in TMEM, split-K.
+namespace bpx {
+bool wgt_conv_ok(int cin, int cout);
+size_t wgt_conv_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias, int n,
+                            int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
+}  // namespace bpx

@@ -80,6 +80,28 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)1 << 46;
   return d;
 }
+// MN-major tf32 operand descriptor: the only layout the tensor core accepts
+// for 32-bit MN-major operands is SWIZZLE_128B_BASE32B (layout type 1):
+// rows of 128 B (32 MN elements at one k), 32-B granules XOR (k mod 4).
+// LBO = byte stride between 32-element MN atoms, SBO = byte stride between
+// groups of 4 k-rows.  TMA writes exactly this with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B (verified on B200: tools/probes/probe_mn.cu).
+__device__ __forceinline__ uint64_t make_desc_mn32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return make_desc(saddr, lbo, sbo) | ((uint64_t)1 << 61);
+}
+// 4-D tensor-map tile load (coordinates innermost first; may be negative or
+// past the end: TMA zero-fills out-of-bounds elements).
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
 __host__ __device__ constexpr uint32_t make_idesc(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(BM >> 4) << 24);

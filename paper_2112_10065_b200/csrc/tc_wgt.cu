@@ -1,0 +1,391 @@
+// tcgen05 weight-gradient engine for the 3x3/pad-1 convolutions, fed by TMA:
+//
+//   dW^T[r][co] = sum_p im2col(x)[p][r] * dz[p][co],   r = tap*Cin + ci
+//   M = 9*Cin (A = im2col(x)^T), N = Cout (B = dz), K = pixels (split-K)
+//
+// Both operands are natural NHWC tiles once K = pixels is blocked as a
+// bh x bw window of one image: for a 32-channel chunk of one tap the A tile
+// is x[img][oh0+dy : +bh][ow0+dx : +bw][ci0 : +32], the B tile is
+// dz[img][oh0 : +bh][ow0 : +bw][co0 : +32].  Each is ONE 4-D TMA box; the
+// conv's zero padding (and the ragged image edge) is TMA's out-of-bounds
+// zero fill, so there is no im2col index math and no predication anywhere.
+// Channels are contiguous, so both tiles are MN-major: TMA lays them out
+// with SWIZZLE_128B_ATOM_32B, the one MN-major layout kind::tf32 accepts.
+//
+// fp32 accuracy: 3xTF32 (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi).  The raw fp32
+// tile already IS b_hi for the tensor core (it reads the top 19 bits), so
+//   * A converter warps (one TMEM lane = one row r per thread) read their
+//     row of the raw A tile, split hi/lo in registers and tcgen05.st both
+//     into TMEM -> the MMA takes A from TMEM (TS form);
+//   * B converter warps write only b_lo, elementwise in the same swizzled
+//     layout, and (in CTAs of the first M tile) sum dz per channel in a
+//     fixed order: the bias gradient comes out of the same pass over dz.
+// Partial sums live in TMEM in 64-pixel chunks (two ping-pong buffers) and
+// are promoted into round-to-nearest fp32 registers by the drain warps,
+// because the tensor core's own fp32 accumulation truncates.
+//
+// CTA: 18 warps, one CTA per SM.  warp 0 TMA producer, warp 1 MMA issuer +
+// TMEM owner, warps 2-5 A converters, 6-9 B converters (+bias), 10-17 drain.
+#include <cuda.h>
+#include "tc_ptx.cuh"
+#include "tc_api.h"
+
+namespace bpx {
+namespace wgt {
+using namespace tcx;
+
+constexpr int BK = 32;                 // pixels per stage (rows of every box)
+constexpr int BOX = 32 * BK * 4;       // one 32-channel x 32-pixel box, bytes
+constexpr int PCH = 2;                 // stages per TMEM promotion chunk
+constexpr int NTHREADS = 18 * 32;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, CB0 = 6, DR0 = 10;   // warps 2-5: A converters
+
+template <int BN>
+struct Cfg {
+  static_assert(BN == 64 || BN == 128, "BN");
+  static constexpr int S = BN == 128 ? 4 : 6;
+  static constexpr int A_BYTES = 4 * BOX;                 // 128 rows of A
+  static constexpr int B_BYTES = (BN / 32) * BOX;
+  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;     // A raw | B raw | B lo
+  static constexpr int ACC = 2 * BN;                      // two chunk buffers
+  static constexpr int A_COL = ACC;                       // + S stages of (hi|lo)
+  static constexpr int RG = 128 / (BN / 4);               // bias row groups
+  static constexpr int SMEM = 1024 + S * STAGE + 512 + 128 * 16;
+  static_assert(ACC + S * 2 * BK <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024, "smem budget");
+};
+
+struct Geo {
+  int Cin, Cout, H, W, bh, bw, th, tw;
+  int tiles, tps;            // pixel tiles in total / per split
+  long long slab;            // Cout * 9*Cin
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
+           Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
+  using Cf = Cfg<BN>;
+  extern __shared__ char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
+  uint64_t* aready = full + Cf::S;
+  uint64_t* bready = aready + Cf::S;
+  uint64_t* empty = bready + Cf::S;
+  uint64_t* hfull = empty + Cf::S;
+  uint64_t* hfree = hfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
+  float4* bias_scr = reinterpret_cast<float4*>(smem + Cf::S * Cf::STAGE + 512);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nrows = 9 * g.Cin;                  // M extent
+  const int chunks = nrows / 32;                // 32-row chunks (tap-major)
+  const int cpt = g.Cin / 32;                   // chunks per tap
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
+  const int t0 = blockIdx.z * g.tps;
+  const int nst = max(0, min(g.tiles, t0 + g.tps) - t0);
+  const int per_img = g.th * g.tw;
+
+  if (tid == 0) {
+    for (int s = 0; s < Cf::S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&aready[s], 128);
+      mbar_init(&bready[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&hfull[b], 1);
+      mbar_init(&hfree[b], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == TMA_WARP) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tx);
+      tma_prefetch_desc(&tdz);
+      int na = 0;
+      for (int c = 0; c < 4; ++c) na += (m0 / 32 + c) < chunks;
+      const uint32_t bytes = (uint32_t)(na * BOX + Cf::B_BYTES);
+      for (int i = 0; i < nst; ++i) {
+        const int s = i % Cf::S;
+        if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
+        const int t = t0 + i;
+        const int img = t / per_img, rem = t - img * per_img;
+        const int oh0 = (rem / g.tw) * g.bh, ow0 = (rem % g.tw) * g.bw;
+        char* st = smem + s * Cf::STAGE;
+        mbar_expect_tx(&full[s], bytes);
+        for (int c = 0; c < 4; ++c) {
+          const int gc = m0 / 32 + c;
+          if (gc >= chunks) break;
+          const int tap = gc / cpt, ci0 = (gc - tap * cpt) * 32;
+          tma_load_4d(st + c * BOX, &tx, ci0, ow0 + tap % 3 - 1, oh0 + tap / 3 - 1, img,
+                      &full[s]);
+        }
+        for (int j = 0; j < BN / 32; ++j)
+          tma_load_4d(st + Cf::A_BYTES + j * BOX, &tdz, n0 + 32 * j, ow0, oh0, img, &full[s]);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // M=128, N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
+      constexpr uint32_t idesc = make_idesc(BN) | (1u << 16);
+      for (int i = 0; i < nst; ++i) {
+        const int s = i % Cf::S;
+        const uint32_t ph = (i / Cf::S) & 1;
+        const int c = i / PCH, b = c & 1;
+        if (i % PCH == 0 && c >= 2) {
+          mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&aready[s], ph);
+        mbar_wait(&bready[s], ph);
+        tc_fence_after();
+        const uint32_t d = tmem + b * BN;
+        const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
+        const uint32_t bh = smem_u32(smem + s * Cf::STAGE + Cf::A_BYTES);
+        const uint32_t bl = bh + Cf::B_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint64_t dbh = make_desc_mn32(bh + ks * 1024, BOX, 512);
+          const uint64_t dbl = make_desc_mn32(bl + ks * 1024, BOX, 512);
+          const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
+          mma_ts(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts(d, ah + 8 * ks, dbh, idesc, 1u);
+        }
+        tc_commit(&empty[s]);
+        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit(&hfull[b]);
+      }
+    }
+  } else if (warp < CB0) {
+    // ------------------------------------------------------------ A converters
+    // thread = TMEM lane = row r of the M tile = channel `lane` of chunk q
+    const int q = warp & 3;
+    const bool valid = (m0 / 32 + q) < chunks;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
+    const int g8 = lane >> 3, w4 = (lane & 7) * 4;
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % Cf::S;
+      mbar_wait(&full[s], (i / Cf::S) & 1);
+      const char* box = smem + s * Cf::STAGE + q * BOX;
+      float hi[BK], lo[BK];
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        const float v = valid ? *reinterpret_cast<const float*>(
+                                    box + k * 128 + ((g8 ^ (k & 3)) << 5) + w4)
+                              : 0.f;
+        split(v, hi[k], lo[k]);
+      }
+      const uint32_t a = lanebase + s * 2 * BK;
+      tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
+      tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
+      tmem_st16(a + BK, *reinterpret_cast<float(*)[16]>(lo));
+      tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&aready[s]);
+    }
+  } else if (warp < DR0) {
+    // ------------------------------------------------------------ B converters
+    // b_lo = b - tf32(b), elementwise in the swizzled layout; per-channel dz
+    // sums (bias gradient) over this split's pixels in CTAs of M tile 0.
+    const int bt = tid - CB0 * 32;
+    constexpr int NC4 = BN / 4;                // float4 columns of the tile
+    const int c4 = bt % NC4, rg = bt / NC4;    // fixed column, row group
+    const int box = c4 / 8, gl = (c4 & 7) >> 1, half = c4 & 1;
+    const bool do_bias = bias_part != nullptr && blockIdx.x == 0;
+    float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % Cf::S;
+      mbar_wait(&full[s], (i / Cf::S) & 1);
+      const char* raw = smem + s * Cf::STAGE + Cf::A_BYTES;
+      char* lo = const_cast<char*>(raw) + Cf::B_BYTES;
+#pragma unroll
+      for (int k = rg; k < BK; k += Cf::RG) {
+        const int off = box * BOX + k * 128 + ((gl ^ (k & 3)) << 5) + half * 16;
+        const float4 v = *reinterpret_cast<const float4*>(raw + off);
+        float4 h, l;
+        split(v.x, h.x, l.x); split(v.y, h.y, l.y);
+        split(v.z, h.z, l.z); split(v.w, h.w, l.w);
+        *reinterpret_cast<float4*>(lo + off) = l;
+        if (do_bias) { bs.x += v.x; bs.y += v.y; bs.z += v.z; bs.w += v.w; }
+      }
+      fence_proxy_async();
+      mbar_arrive(&bready[s]);
+    }
+    if (do_bias) {
+      bias_scr[bt] = bs;
+      named_sync(1, 128);
+      if (bt < NC4) {
+        float4 t = bias_scr[bt];
+        for (int r = 1; r < Cf::RG; ++r) {
+          const float4 u = bias_scr[r * NC4 + bt];
+          t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+        }
+        *reinterpret_cast<float4*>(bias_part + (long long)blockIdx.z * g.Cout + n0 + 4 * bt) = t;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ drain + epilogue
+    const int q = warp & 3, hf = (warp - DR0) >> 2;
+    constexpr int CW = BN / 2;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + hf * CW;
+    float acc[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) acc[j] = 0.f;
+    const int nch = (nst + PCH - 1) / PCH;
+    for (int c = 0; c < nch; ++c) {
+      const int b = c & 1;
+      mbar_wait(&hfull[b], (c >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < CW; j += 8) {
+        uint32_t r[8];
+        tmem_ld8(lanebase + b * BN + j, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]);
+      }
+      tc_fence_before();
+      mbar_arrive(&hfree[b]);
+    }
+    const int r = m0 + q * 32 + lane;
+    if (r < nrows) {
+      float* o = part + (long long)blockIdx.z * g.slab + r;
+#pragma unroll
+      for (int j = 0; j < CW; ++j) o[(long long)(n0 + hf * CW + j) * nrows] = acc[j];
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_free(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
+
+// bh x bw pixel window (bh*bw = 32) with the least zero-filled overhang.
+inline void window(int H, int W, int& bh, int& bw) {
+  long long best = -1;
+  for (int w = 32; w >= 1; w >>= 1) {
+    const int h = 32 / w;
+    const long long area = (long long)cdiv(H, h) * h * cdiv(W, w) * w;
+    if (best < 0 || area < best) { best = area; bh = h; bw = w; }
+  }
+}
+
+inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
+  g.Cin = cin; g.Cout = cout; g.H = H; g.W = W;
+  window(H, W, g.bh, g.bw);
+  g.th = cdiv(H, g.bh);
+  g.tw = cdiv(W, g.bw);
+  g.tiles = n * g.th * g.tw;
+  g.slab = (long long)cout * 9 * cin;
+  mt = cdiv(9 * cin, 128);
+  nt = cout / bn_for(cout);
+  const int tiles_mn = mt * nt;
+  int want = num_sms() / tiles_mn;
+  if (want < 1) want = 1;
+  if (want > g.tiles) want = g.tiles;
+  g.tps = cdiv(g.tiles, want);
+  splits = cdiv(g.tiles, g.tps);
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline bool encode_nhwc(CUtensorMap* m, const float* p, int n, int H, int W, int C, int bh,
+                        int bw) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4,
+                                 (cuuint64_t)H * W * C * 4};
+  const cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                const_cast<float*>(p), dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g, int mt,
+                    int nt, int splits, float* part, float* bias_part, cudaStream_t st) {
+  using Cf = Cfg<BN>;
+  auto kern = wgt_kernel<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    attr = true;
+  }
+  kern<<<dim3(mt, nt, splits), NTHREADS, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+  return launch_status();
+}
+
+}  // namespace wgt
+
+// ============================================================ entry points
+
+bool wgt_conv_ok(int cin, int cout) { return cin % 32 == 0 && cout % 64 == 0; }
+
+size_t wgt_conv_ws(int n, int h, int w, int cin, int cout) {
+  wgt::Geo g;
+  int mt, nt, splits;
+  wgt::plan(n, h, w, cin, cout, g, mt, nt, splits);
+  if (splits <= 1) return 0;
+  return ((size_t)splits * (size_t)g.slab + (size_t)splits * cout) * sizeof(float);
+}
+
+bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias, int n,
+                            int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
+  if (!wgt_conv_ok(cin, cout) || !aligned16(x) || !aligned16(dz) || !aligned16(dw))
+    return BPX_ERR_INVALID_ARGUMENT;
+  if (dbias && !aligned16(dbias)) return BPX_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < wgt_conv_ws(n, h, w_, cin, cout)) return BPX_ERR_WORKSPACE;
+  const size_t slab = (size_t)cout * 9 * cin;
+  if (n == 0) {
+    cudaMemsetAsync(dw, 0, sizeof(float) * slab, st);
+    if (dbias) cudaMemsetAsync(dbias, 0, sizeof(float) * cout, st);
+    return launch_status(0);
+  }
+  wgt::Geo g;
+  int mt, nt, splits;
+  wgt::plan(n, h, w_, cin, cout, g, mt, nt, splits);
+  CUtensorMap tx, tdz;
+  if (!wgt::encode_nhwc(&tx, x, n, h, w_, cin, g.bh, g.bw) ||
+      !wgt::encode_nhwc(&tdz, dz, n, h, w_, cout, g.bh, g.bw))
+    return BPX_ERR_INVALID_ARGUMENT;
+  float* part = splits == 1 ? dw : static_cast<float*>(ws);
+  float* bpart = !dbias ? nullptr
+                        : (splits == 1 ? dbias : static_cast<float*>(ws) + (size_t)splits * slab);
+  bpx_status_t s = wgt::bn_for(cout) == 128
+      ? wgt::launch<128>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+      : wgt::launch<64>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+  if (s != BPX_OK || splits == 1) return s;
+  s = split_reduce(part, splits, slab, dw, st);
+  if (s != BPX_OK || !dbias) return s;
+  return split_reduce(bpart, splits, (size_t)cout, dbias, st);
+}
+
+}  // namespace bpx
