@@ -19,6 +19,8 @@ bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, 
   BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (small_conv_fwd_ok(cin, cout))
+    return small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
   if (ts_conv_ok(cin, cout))
     return ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
   if (tc_conv_fwd_ok(n, h, w_, cin, cout))
@@ -49,9 +51,11 @@ size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
   size_t b = tc_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t c = wg_conv_ws(n, h, w_, cin, cout);
   size_t d = wgt_conv_ws(n, h, w_, cin, cout);
+  size_t e = small_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t m = a > b ? a : b;
   m = m > c ? m : c;
-  return m > d ? m : d;
+  m = m > d ? m : d;
+  return m > e ? m : e;
 }
 
 bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float* dbias,
@@ -63,6 +67,8 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   if (wgt_conv_ok(cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
       (!dbias || aligned16(dbias)))
     return wgt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+  if (small_conv_wgrad_ok(cin, cout) && aligned16(dz))
+    return small_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (wg_conv_ok(cin, cout))
     return wg_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_wgrad_ok(n, h, w_, cin, cout))

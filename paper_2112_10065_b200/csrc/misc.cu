@@ -66,8 +66,40 @@ __global__ void split_reduce_kernel(const float4* __restrict__ parts, int splits
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 s = parts[i];
-    for (int k = 1; k < splits; ++k) {
+    int k = 1;
+    for (; k + 8 <= splits; k += 8) {       // 8 loads in flight, adds in order
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = parts[(k + j) * n4 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { s.x += v[j].x; s.y += v[j].y; s.z += v[j].z; s.w += v[j].w; }
+    }
+    for (; k < splits; ++k) {
       float4 v = parts[k * n4 + i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    out[i] = s;
+  }
+}
+// Many splits of a short vector: 8 warps per block each sum every 8th split
+// of 32 float4 columns, then fixed-order combine in shared memory.
+__global__ void split_reduce_wide(const float4* __restrict__ parts, int splits, long long n4,
+                                  float4* __restrict__ out) {
+  __shared__ float4 red[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * 32 + lane;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n4) {
+    for (int k = grp; k < splits; k += 8) {
+      float4 v = parts[k * n4 + i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+  }
+  red[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && i < n4) {
+    for (int g = 1; g < 8; ++g) {
+      const float4 v = red[g][lane];
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
     out[i] = s;
@@ -86,7 +118,12 @@ __global__ void split_reduce_scalar(const float* __restrict__ parts, int splits,
 bpx_status_t split_reduce(const float* parts, int splits, size_t n, float* out,
                           cudaStream_t st) {
   int grid = 4 * num_sms();
-  if (n % 4 == 0 && aligned16(parts) && aligned16(out)) {
+  if (n % 4 == 0 && aligned16(parts) && aligned16(out) && splits >= 32 &&
+      (long long)(n / 4) <= 64LL * num_sms()) {
+    const long long n4 = (long long)(n / 4);
+    split_reduce_wide<<<(int)cdivll(n4, 32), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(parts), splits, n4, reinterpret_cast<float4*>(out));
+  } else if (n % 4 == 0 && aligned16(parts) && aligned16(out)) {
     long long n4 = (long long)(n / 4);
     if (cdivll(n4, 256) < grid) grid = (int)cdivll(n4, 256);
     split_reduce_kernel<<<grid, 256, 0, st>>>(

@@ -26,3 +26,15 @@ bpx_status_t simt_linear_wgrad(const float* x, const float* dy, float* dw, float
                                int b, int in, int out, void* ws, size_t ws_bytes,
                                cudaStream_t st);
 }  // namespace bpx
+
+// FFMA weight gradient for tiny input depth (conv_small.cu: conv1_1, Cin = 3).
+namespace bpx {
+bool small_conv_fwd_ok(int cin, int cout);
+bpx_status_t small_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
+                            int h, int w_, int cin, int cout, int relu, cudaStream_t st);
+bool small_conv_wgrad_ok(int cin, int cout);
+size_t small_conv_wgrad_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t small_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias, int n,
+                              int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
+}  // namespace bpx
