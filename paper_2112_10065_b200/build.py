@@ -15,6 +15,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          f"-I{os.path.join(ROOT, 'include')}"]
+# tuning experiments only (e.g. BPX_NVCC_EXTRA="-DWGT_PCH=4"); empty for the product
+FLAGS += os.environ.get("BPX_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -3,14 +3,15 @@
 //   dW^T[r][co] = sum_p im2col(x)[p][r] * dz[p][co],   r = tap*Cin + ci
 //   M = 9*Cin (A = im2col(x)^T), N = Cout (B = dz), K = pixels (split-K)
 //
-// Both operands are natural NHWC tiles once K = pixels is blocked as a
-// bh x bw window of one image: for a 32-channel chunk of one tap the A tile
-// is x[img][oh0+dy : +bh][ow0+dx : +bw][ci0 : +32], the B tile is
-// dz[img][oh0 : +bh][ow0 : +bw][co0 : +32].  Each is ONE 4-D TMA box; the
-// conv's zero padding (and the ragged image edge) is TMA's out-of-bounds
-// zero fill, so there is no im2col index math and no predication anywhere.
-// Channels are contiguous, so both tiles are MN-major: TMA lays them out
-// with SWIZZLE_128B_ATOM_32B, the one MN-major layout kind::tf32 accepts.
+// K = pixels is blocked as 32 consecutive pixels of the flattened NHWC
+// tensor (so no tile overhangs an image edge, whatever H and W are).  For a
+// 32-channel chunk of one tap the A tile is x[p0+s : +32][ci0 : +32] with
+// s = dy*W + dx, the B tile is dz[p0 : +32][co0 : +32]: each is ONE 2-D TMA
+// box.  Rows whose shifted source pixel wraps across an image row/edge are
+// the conv's zero padding: the A converters zero them from a per-tap
+// ballot mask.  Channels are contiguous, so both tiles are MN-major: TMA
+// lays them out with SWIZZLE_128B_ATOM_32B, the one MN-major layout
+// kind::tf32 accepts.
 //
 // fp32 accuracy: 3xTF32 (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi).  The raw fp32
 // tile already IS b_hi for the tensor core (it reads the top 19 bits), so
@@ -56,8 +57,9 @@ struct Cfg {
 };
 
 struct Geo {
-  int Cin, Cout, H, W, bh, bw, th, tw;
-  int tiles, tps;            // pixel tiles in total / per split
+  int Cin, Cout, H, W;
+  long long npix;
+  int tiles, tps;            // 32-pixel tiles in total / per split
   long long slab;            // Cout * 9*Cin
 };
 
@@ -88,7 +90,6 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
   const int t0 = blockIdx.z * g.tps;
   const int nst = max(0, min(g.tiles, t0 + g.tps) - t0);
-  const int per_img = g.th * g.tw;
 
   if (tid == 0) {
     for (int s = 0; s < Cf::S; ++s) {
@@ -120,20 +121,17 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       for (int i = 0; i < nst; ++i) {
         const int s = i % Cf::S;
         if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
-        const int t = t0 + i;
-        const int img = t / per_img, rem = t - img * per_img;
-        const int oh0 = (rem / g.tw) * g.bh, ow0 = (rem % g.tw) * g.bw;
+        const int p0 = (t0 + i) * BK;
         char* st = smem + s * Cf::STAGE;
         mbar_expect_tx(&full[s], bytes);
         for (int c = 0; c < 4; ++c) {
           const int gc = m0 / 32 + c;
           if (gc >= chunks) break;
           const int tap = gc / cpt, ci0 = (gc - tap * cpt) * 32;
-          tma_load_4d(st + c * BOX, &tx, ci0, ow0 + tap % 3 - 1, oh0 + tap / 3 - 1, img,
-                      &full[s]);
+          tma_load_2d(st + c * BOX, &tx, ci0, p0 + (tap / 3 - 1) * g.W + tap % 3 - 1, &full[s]);
         }
         for (int j = 0; j < BN / 32; ++j)
-          tma_load_4d(st + Cf::A_BYTES + j * BOX, &tdz, n0 + 32 * j, ow0, oh0, img, &full[s]);
+          tma_load_2d(st + Cf::A_BYTES + j * BOX, &tdz, n0 + 32 * j, p0, &full[s]);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -176,16 +174,32 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     const bool valid = (m0 / 32 + q) < chunks;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
     const int g8 = lane >> 3, w4 = (lane & 7) * 4;
+    const int gc = m0 / 32 + q, tap = valid ? gc / cpt : 4;
+    const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+    // coordinates of pixel p0 + lane, advanced by 32 pixels per stage
+    long long p = (long long)t0 * BK + lane;
+    int img = (int)(p / ((long long)g.H * g.W));
+    int rem = (int)(p - (long long)img * g.H * g.W);
+    int oh = rem / g.W, ow = rem - (rem / g.W) * g.W;
     for (int i = 0; i < nst; ++i) {
       const int s = i % Cf::S;
+      const bool ok = valid && p < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
+                      (unsigned)(ow + dx) < (unsigned)g.W;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, ok);
+      p += BK;
+      ow += BK;
+      while (ow >= g.W) {
+        ow -= g.W;
+        if (++oh == g.H) { oh = 0; ++img; }
+      }
       mbar_wait(&full[s], (i / Cf::S) & 1);
       const char* box = smem + s * Cf::STAGE + q * BOX;
       float hi[BK], lo[BK];
 #pragma unroll
       for (int k = 0; k < BK; ++k) {
-        const float v = valid ? *reinterpret_cast<const float*>(
-                                    box + k * 128 + ((g8 ^ (k & 3)) << 5) + w4)
-                              : 0.f;
+        const float v = ((vmask >> k) & 1u) ? *reinterpret_cast<const float*>(
+                                                box + k * 128 + ((g8 ^ (k & 3)) << 5) + w4)
+                                          : 0.f;
         split(v, hi[k], lo[k]);
       }
       const uint32_t a = lanebase + s * 2 * BK;
@@ -281,22 +295,10 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
 
 inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
 
-// bh x bw pixel window (bh*bw = 32) with the least zero-filled overhang.
-inline void window(int H, int W, int& bh, int& bw) {
-  long long best = -1;
-  for (int w = 32; w >= 1; w >>= 1) {
-    const int h = 32 / w;
-    const long long area = (long long)cdiv(H, h) * h * cdiv(W, w) * w;
-    if (best < 0 || area < best) { best = area; bh = h; bw = w; }
-  }
-}
-
 inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
   g.Cin = cin; g.Cout = cout; g.H = H; g.W = W;
-  window(H, W, g.bh, g.bw);
-  g.th = cdiv(H, g.bh);
-  g.tw = cdiv(W, g.bw);
-  g.tiles = n * g.th * g.tw;
+  g.npix = (long long)n * H * W;
+  g.tiles = (int)cdivll(g.npix, BK);
   g.slab = (long long)cout * 9 * cin;
   mt = cdiv(9 * cin, 128);
   nt = cout / bn_for(cout);
@@ -308,19 +310,13 @@ inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& n
   splits = cdiv(g.tiles, g.tps);
 }
 
-typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-inline bool encode_nhwc(CUtensorMap* m, const float* p, int n, int H, int W, int C, int bh,
-                        int bw) {
-  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
-  const cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4,
-                                 (cuuint64_t)H * W * C * 4};
-  const cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)bh, 1};
-  const cuuint32_t es[4] = {1, 1, 1, 1};
-  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+// [pixels][C] fp32, box = 32 channels x 32 pixels, MN-major tf32 layout.
+inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C) {
+  const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)npix};
+  const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)BK};
+  const cuuint32_t es[2] = {1, 1};
+  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                 const_cast<float*>(p), dims, strides, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
@@ -373,8 +369,7 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
   int mt, nt, splits;
   wgt::plan(n, h, w_, cin, cout, g, mt, nt, splits);
   CUtensorMap tx, tdz;
-  if (!wgt::encode_nhwc(&tx, x, n, h, w_, cin, g.bh, g.bw) ||
-      !wgt::encode_nhwc(&tdz, dz, n, h, w_, cout, g.bh, g.bw))
+  if (!wgt::encode_rows(&tx, x, g.npix, cin) || !wgt::encode_rows(&tdz, dz, g.npix, cout))
     return BPX_ERR_INVALID_ARGUMENT;
   float* part = splits == 1 ? dw : static_cast<float*>(ws);
   float* bpart = !dbias ? nullptr
