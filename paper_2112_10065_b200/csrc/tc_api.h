@@ -69,9 +69,12 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
 
 // TMA-fed persistent forward / data-gradient engine (tc_fdt.cu).
 namespace bpx {
-bool fdt_conv_ok(int cin, int cout);
+bool fdt_conv_ok(int cin, int cout, int w);
+size_t fdt_conv_ws(int cin, int cout);
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                          int h, int w_, int cin, int cout, int relu, cudaStream_t st);
+                          int h, int w_, int cin, int cout, int relu, void* ws,
+                          size_t ws_bytes, cudaStream_t st);
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
-                            int n, int h, int w_, int cin, int cout, cudaStream_t st);
+                            int n, int h, int w_, int cin, int cout, void* ws,
+                            size_t ws_bytes, cudaStream_t st);
 }  // namespace bpx

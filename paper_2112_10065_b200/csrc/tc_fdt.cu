@@ -5,26 +5,33 @@
 //   dgrad : dx[q][ci] = mask(q) * sum_{tap,co} dz[q - s_tap][co] * w[co][tap][ci]
 //   s_tap = dy*W + dx  (flattened-pixel shift of the tap)
 //
-// M = pixels (128 per tile), N = output channels, K = (tap, 32-channel chunk)
-// stages.  A stage's A tile is ONE 2-D TMA box: 128 consecutive flattened
-// pixels, shifted by the tap, x 32 channels.  Rows whose shifted source
-// pixel falls outside its image (the conv's zero padding) are zeroed by the
-// A converters from a per-thread 9-bit tap mask computed once per tile.
+// M = pixels (128 consecutive flattened pixels per tile), N = output
+// channels, K = (32-channel chunk, tap) stages.  Per channel chunk the CTA
+// loads ONE halo of the activations by TMA -- flattened rows
+// [m0 - W - 1, m0 + 128 + W + 1) x 32 channels -- and all nine taps read
+// their shifted 128-row window out of it, so activation traffic is
+// (128 + 2W + 2)/128 instead of 9x the tile.  Rows whose shifted source
+// pixel falls outside its image (the conv's zero padding, including the
+// row wrap of the flattened layout) are zeroed by the A converters from a
+// per-thread 9-bit tap mask computed once per tile.
 // The B tile is the raw weight tile, straight from w by TMA:
 //   fwd   B(co, k) = w[co][tap][ci]: K-major, 128-B swizzle (one box)
 //   dgrad B(ci, k) = w[co][tap][ci]: MN-major, SWIZZLE_128B_ATOM_32B, one
 //                    box per 32 input channels (w viewed [Cout][9][Cin]).
 //
 // fp32 accuracy by 3xTF32 (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi); the raw tile
-// is b_hi.  A converters split A into TMEM (TS form); B converters write
-// b_lo next to the raw tile.  TMEM chunk promotion into RN fp32 registers
-// as in the other engines.  The kernel is persistent: the stage ring and the
+// is b_hi.  A converters split A into TMEM (TS form).  b_lo = w - tf32(w) is
+// a pre-split copy of the (small) weight tensor made by one elementwise
+// kernel per call, loaded by TMA next to b_hi: shared memory then carries
+// only the MMA's B reads, the TMA fills and one LDS pass over A -- a
+// converter pass over B in shared memory made this kernel smem-bound.
+// TMEM chunk promotion into RN fp32 registers as in the other engines.  The kernel is persistent: the stage ring and the
 // accumulator ping-pong run straight across tiles, so a tile's epilogue
 // (drain warps: bias + ReLU or ReLU mask, stores) overlaps the next tile's
 // main loop.
 //
-// CTA: 18 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters,
-// 6-9 B converters, 10-17 drain + epilogue.
+// CTA: 14 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters,
+// 6-13 drain + epilogue.
 #include <cuda.h>
 #include "tc_ptx.cuh"
 #include "tc_api.h"
@@ -34,28 +41,28 @@ namespace fdt {
 using namespace tcx;
 
 constexpr int BK = 32;                 // K elements per stage (one channel chunk of a tap)
-constexpr int A_BYTES = 128 * BK * 4;  // 128 pixel rows x 128 B
 constexpr int PCH = 2;                 // stages per TMEM promotion chunk
-constexpr int NTHREADS = 18 * 32;
-constexpr int TMA_WARP = 0, MMA_WARP = 1, CB0 = 6, DR0 = 10;   // 2-5: A converters
+constexpr int NTHREADS = 14 * 32;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
 
 template <int BN>
 struct Cfg {
   static_assert(BN == 64 || BN == 128, "BN");
-  static constexpr int S = BN == 128 ? 4 : 6;
+  static constexpr int S = 4;                             // B / TMEM-A stages
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;     // A raw | B raw | B lo
+  static constexpr int STAGE = 2 * B_BYTES;               // B raw | B lo
   static constexpr int A_COL = 2 * BN;
-  static constexpr int SMEM = 1024 + S * STAGE + 512;
   static_assert(A_COL + S * 2 * BK <= 512, "TMEM budget");
-  static_assert(SMEM <= 227 * 1024, "smem budget");
+  // dynamic smem = 1024 (align) + S*STAGE + 2*halo_bytes + 512 (barriers)
+  static int smem(int halo_bytes) { return 1024 + S * STAGE + 2 * halo_bytes + 512; }
 };
 
 struct Geo {
   int H, W, C;               // C = gathered channels (Cin fwd, Cout dgrad)
   int N;                     // output channels
   int npix, mt, nt, tiles;
-  int dgrad;
+  int hrows, hbox, nhbox;    // halo rows used, rows per TMA box, boxes per halo
+  int halo_bytes;            // one halo slot (nhbox * hbox * 128)
 };
 
 struct EBiasAct {
@@ -95,32 +102,36 @@ struct EMask {
 template <int BN, bool DG, class EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           Geo g, EPI epi) {
+           const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
   using Cf = Cfg<BN>;
+  constexpr int S = Cf::S;
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
-  uint64_t* aready = full + Cf::S;
-  uint64_t* bready = aready + Cf::S;
-  uint64_t* empty = bready + Cf::S;
-  uint64_t* hfull = empty + Cf::S;
-  uint64_t* hfree = hfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
+  char* halo = smem + S * Cf::STAGE;                          // 2 slots
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(halo + 2 * g.halo_bytes);
+  uint64_t* aready = bfull + S;
+  uint64_t* empty = aready + S;
+  uint64_t* hfull = empty + S;       // halo slot loaded
+  uint64_t* hempty = hfull + 2;      // halo slot consumed by all nine taps
+  uint64_t* accfull = hempty + 2;
+  uint64_t* accfree = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfree + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cpt = g.C / BK;                   // channel chunks per tap
+  const int cpt = g.C / BK;                   // channel chunks
   const int nk = 9 * cpt;                     // stages per tile
 
   if (tid == 0) {
-    for (int s = 0; s < Cf::S; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&bfull[s], 1);
       mbar_init(&aready[s], 128);
-      mbar_init(&bready[s], 128);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
-      mbar_init(&hfree[b], 256);
+      mbar_init(&hempty[b], 128);
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accfree[b], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -135,22 +146,32 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     if (lane == 0) {
       tma_prefetch_desc(&ta);
       tma_prefetch_desc(&tb);
-      int i = 0;
+      tma_prefetch_desc(&tbl);
+      int i = 0, hc = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
         const int m0 = (t / g.nt) * 128, n0 = (t % g.nt) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++i) {
-          const int s = i % Cf::S;
-          if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
-          const int tap = kb / cpt, c0 = (kb - tap * cpt) * BK;
-          const int shift = (tap / 3 - 1) * g.W + (tap % 3 - 1);
-          char* st = smem + s * Cf::STAGE;
-          mbar_expect_tx(&full[s], A_BYTES + Cf::B_BYTES);
-          tma_load_2d(st, &ta, c0, DG ? m0 - shift : m0 + shift, &full[s]);
-          if (DG) {
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_3d(st + A_BYTES + j * 4096, &tb, n0 + 32 * j, tap, c0, &full[s]);
-          } else {
-            tma_load_2d(st + A_BYTES, &tb, tap * g.C + c0, n0, &full[s]);
+        for (int cc = 0; cc < cpt; ++cc, ++hc) {
+          const int hs = hc & 1;
+          if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
+          mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_bytes);
+          for (int j = 0; j < g.nhbox; ++j)
+            tma_load_2d(halo + hs * g.halo_bytes + j * g.hbox * 128, &ta, cc * BK,
+                        m0 - g.W - 1 + j * g.hbox, &hfull[hs]);
+          for (int tap = 0; tap < 9; ++tap, ++i) {
+            const int s = i % S;
+            if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+            char* st = smem + s * Cf::STAGE;
+            mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
+            if (DG) {
+              for (int j = 0; j < BN / 32; ++j) {
+                tma_load_3d(st + j * 4096, &tb, n0 + 32 * j, tap, cc * BK, &bfull[s]);
+                tma_load_3d(st + Cf::B_BYTES + j * 4096, &tbl, n0 + 32 * j, tap, cc * BK,
+                            &bfull[s]);
+              }
+            } else {
+              tma_load_2d(st, &tb, tap * g.C + cc * BK, n0, &bfull[s]);
+              tma_load_2d(st + Cf::B_BYTES, &tbl, tap * g.C + cc * BK, n0, &bfull[s]);
+            }
           }
         }
       }
@@ -163,19 +184,19 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       int i = 0, c = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++i) {
-          const int s = i % Cf::S;
-          const uint32_t ph = (i / Cf::S) & 1;
+          const int s = i % S;
+          const uint32_t ph = (i / S) & 1;
           const int b = c & 1;
           if (kb % PCH == 0 && c >= 2) {
-            mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
+            mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
             tc_fence_after();
           }
           mbar_wait(&aready[s], ph);
-          mbar_wait(&bready[s], ph);
+          mbar_wait(&bfull[s], ph);
           tc_fence_after();
           const uint32_t d = tmem + b * BN;
           const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
-          const uint32_t bh = smem_u32(smem + s * Cf::STAGE + A_BYTES);
+          const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
           const uint32_t bl = bh + Cf::B_BYTES;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
@@ -194,19 +215,20 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
           tc_commit(&empty[s]);
           if (kb % PCH == PCH - 1 || kb == nk - 1) {
-            tc_commit(&hfull[b]);
+            tc_commit(&accfull[b]);
             ++c;
           }
         }
       }
     }
-  } else if (warp < CB0) {
+  } else if (warp < DR0) {
     // ------------------------------------------------------------ A converters
-    // thread = TMEM lane = pixel row of the tile
+    // thread = TMEM lane = pixel row of the tile; stage (cc, tap) reads halo
+    // row r + W + 1 +/- s_tap
     const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
     const int hw = g.H * g.W;
-    int i = 0;
+    int i = 0, hc = 0;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
       const int p = (t / g.nt) * 128 + r;
       uint32_t tmask = 0;                     // bit tap: source pixel inside the image
@@ -220,51 +242,38 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W) tmask |= 1u << tap;
         }
       }
-      for (int kb = 0; kb < nk; ++kb, ++i) {
-        const int s = i % Cf::S;
-        const bool ok = (tmask >> (kb / cpt)) & 1u;
-        mbar_wait(&full[s], (i / Cf::S) & 1);
-        const char* row = smem + s * Cf::STAGE + r * 128;
-        float hi[BK], lo[BK];
+      for (int cc = 0; cc < cpt; ++cc, ++hc) {
+        const int hs = hc & 1;
+        mbar_wait(&hfull[hs], (hc >> 1) & 1);
+        const char* hbase = halo + hs * g.halo_bytes;
+        for (int tap = 0; tap < 9; ++tap, ++i) {
+          const int s = i % S;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
+          tc_fence_after();
+          const int sh = (tap / 3 - 1) * g.W + (tap % 3 - 1);
+          const int hr = r + g.W + 1 + (DG ? -sh : sh);
+          const bool ok = (tmask >> tap) & 1u;
+          const char* row = hbase + hr * 128;
+          float hi[BK], lo[BK];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (r & 7)) << 4));
-          split(v.x, hi[4 * j + 0], lo[4 * j + 0]);
-          split(v.y, hi[4 * j + 1], lo[4 * j + 1]);
-          split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
-          split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
+          for (int j = 0; j < 8; ++j) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
+            split(v.x, hi[4 * j + 0], lo[4 * j + 0]);
+            split(v.y, hi[4 * j + 1], lo[4 * j + 1]);
+            split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
+            split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
+          }
+          const uint32_t a = lanebase + s * 2 * BK;
+          tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
+          tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
+          tmem_st16(a + BK, *reinterpret_cast<float(*)[16]>(lo));
+          tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&aready[s]);
         }
-        const uint32_t a = lanebase + s * 2 * BK;
-        tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
-        tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
-        tmem_st16(a + BK, *reinterpret_cast<float(*)[16]>(lo));
-        tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        mbar_arrive(&aready[s]);
-      }
-    }
-  } else if (warp < DR0) {
-    // ------------------------------------------------------------ B converters
-    const int bt = tid - CB0 * 32;
-    int i = 0;
-    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++i) {
-        const int s = i % Cf::S;
-        mbar_wait(&full[s], (i / Cf::S) & 1);
-        const float4* raw = reinterpret_cast<const float4*>(smem + s * Cf::STAGE + A_BYTES);
-        float4* lo = reinterpret_cast<float4*>(smem + s * Cf::STAGE + A_BYTES + Cf::B_BYTES);
-#pragma unroll
-        for (int j = bt; j < Cf::B_BYTES / 16; j += 128) {
-          const float4 v = raw[j];
-          float4 h, l;
-          split(v.x, h.x, l.x); split(v.y, h.y, l.y);
-          split(v.z, h.z, l.z); split(v.w, h.w, l.w);
-          lo[j] = l;
-        }
-        fence_proxy_async();
-        mbar_arrive(&bready[s]);
+        mbar_arrive(&hempty[hs]);
       }
     }
   } else {
@@ -280,7 +289,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
       for (int k = 0; k < nch; ++k, ++c) {
         const int b = c & 1;
-        mbar_wait(&hfull[b], (c >> 1) & 1);
+        mbar_wait(&accfull[b], (c >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int j = 0; j < CW; j += 8) {
@@ -291,7 +300,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           for (int u = 0; u < 8; ++u) acc[j + u] += __uint_as_float(rr[u]);
         }
         tc_fence_before();
-        mbar_arrive(&hfree[b]);
+        mbar_arrive(&accfree[b]);
       }
       const long long p = (long long)(t / g.nt) * 128 + q * 32 + lane;
       const int n0 = (t % g.nt) * BN + hf * CW;
@@ -317,6 +326,18 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 
 // ------------------------------------------------------------------ host side
 
+__global__ void split_lo_kernel(const float4* __restrict__ w, float4* __restrict__ lo,
+                                long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = w[i];
+    float4 h, l;
+    split(v.x, h.x, l.x); split(v.y, h.y, l.y);
+    split(v.z, h.z, l.z); split(v.w, h.w, l.w);
+    lo[i] = l;
+  }
+}
+
 inline bool encode(CUtensorMap* m, const float* p, int rank, const cuuint64_t* dims,
                    const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
   const cuuint32_t es[3] = {1, 1, 1};
@@ -328,8 +349,8 @@ inline bool encode(CUtensorMap* m, const float* p, int rank, const cuuint64_t* d
 }
 
 template <int BN, bool DG, class EPI>
-bpx_status_t run(const float* a, const float* w, int n, int H, int W, int Cin, int Cout,
-                 EPI epi, cudaStream_t st) {
+bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W, int Cin,
+                 int Cout, EPI epi, cudaStream_t st) {
   using Cf = Cfg<BN>;
   Geo g;
   g.H = H; g.W = W;
@@ -339,37 +360,52 @@ bpx_status_t run(const float* a, const float* w, int n, int H, int W, int Cin, i
   g.mt = cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;
-  g.dgrad = DG;
+  g.hrows = 128 + 2 * W + 2;
+  g.nhbox = cdiv(g.hrows, 256);
+  g.hbox = cdiv(cdiv(g.hrows, g.nhbox), 8) * 8;
+  g.halo_bytes = g.nhbox * g.hbox * 128;
+  const int smem = Cf::smem(g.halo_bytes);
+  if (smem > 227 * 1024) return BPX_ERR_INVALID_ARGUMENT;
   CUtensorMap ta, tb;
   {
     const cuuint64_t dims[2] = {(cuuint64_t)g.C, (cuuint64_t)g.npix};
     const cuuint64_t strides[1] = {(cuuint64_t)g.C * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)BK, 128};
+    const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)g.hbox};
     if (!encode(&ta, a, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return BPX_ERR_INVALID_ARGUMENT;
   }
-  if (DG) {       // w as [Cout][9][Cin]: box 32 ci x 1 tap x 32 co, MN-major
-    const cuuint64_t dims[3] = {(cuuint64_t)Cin, 9, (cuuint64_t)Cout};
-    const cuuint64_t strides[2] = {(cuuint64_t)Cin * 4, (cuuint64_t)9 * Cin * 4};
-    const cuuint32_t box[3] = {32, 1, (cuuint32_t)BK};
-    if (!encode(&tb, w, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
-      return BPX_ERR_INVALID_ARGUMENT;
-  } else {        // w as [Cout][9*Cin]: box 32 k x BN rows, K-major
-    const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
-    const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BN};
-    if (!encode(&tb, w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return BPX_ERR_INVALID_ARGUMENT;
+  CUtensorMap tbl;
+  for (int v = 0; v < 2; ++v) {
+    const float* src = v ? wlo : w;
+    CUtensorMap* m = v ? &tbl : &tb;
+    if (DG) {       // w as [Cout][9][Cin]: box 32 ci x 1 tap x 32 co, MN-major
+      const cuuint64_t dims[3] = {(cuuint64_t)Cin, 9, (cuuint64_t)Cout};
+      const cuuint64_t strides[2] = {(cuuint64_t)Cin * 4, (cuuint64_t)9 * Cin * 4};
+      const cuuint32_t box[3] = {32, 1, (cuuint32_t)BK};
+      if (!encode(m, src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return BPX_ERR_INVALID_ARGUMENT;
+    } else {        // w as [Cout][9*Cin]: box 32 k x BN rows, K-major
+      const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
+      const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 4};
+      const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BN};
+      if (!encode(m, src, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        return BPX_ERR_INVALID_ARGUMENT;
+    }
   }
+  const long long n4 = (long long)Cout * 9 * Cin / 4;
+  int sgrid = (int)cdivll(n4, 256);
+  if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
+  split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
+                                         reinterpret_cast<float4*>(wlo), n4);
   auto kern = fdt_kernel<BN, DG, EPI>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int grid = g.tiles < num_sms() ? g.tiles : num_sms();
-  kern<<<grid, NTHREADS, Cf::SMEM, st>>>(ta, tb, g, epi);
-  return launch_status();
+  kern<<<grid, NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
+  return launch_status(2);
 }
 
 inline int bn_for(int N) { return N % 128 == 0 ? 128 : 64; }
@@ -378,29 +414,38 @@ inline int bn_for(int N) { return N % 128 == 0 ? 128 : 64; }
 
 // ============================================================ entry points
 
-bool fdt_conv_ok(int cin, int cout) { return cin % 64 == 0 && cout % 64 == 0; }
+// W <= 224 keeps two halo slots + four B stages inside 227 KB of smem.
+bool fdt_conv_ok(int cin, int cout, int w) { return cin % 64 == 0 && cout % 64 == 0 && w <= 224; }
+
+size_t fdt_conv_ws(int cin, int cout) { return (size_t)cout * 9 * cin * sizeof(float); }
 
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                          int h, int w_, int cin, int cout, int relu, cudaStream_t st) {
-  if (!fdt_conv_ok(cin, cout) || !aligned16(x) || !aligned16(w) || !aligned16(y))
+                          int h, int w_, int cin, int cout, int relu, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
+  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
+  if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
+  float* wlo = static_cast<float*>(ws);
   fdt::EBiasAct epi{y, bias, relu};
   if (fdt::bn_for(cout) == 64)
-    return fdt::run<64, false>(x, w, n, h, w_, cin, cout, epi, st);
-  return fdt::run<128, false>(x, w, n, h, w_, cin, cout, epi, st);
+    return fdt::run<64, false>(x, w, wlo, n, h, w_, cin, cout, epi, st);
+  return fdt::run<128, false>(x, w, wlo, n, h, w_, cin, cout, epi, st);
 }
 
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
-                            int n, int h, int w_, int cin, int cout, cudaStream_t st) {
-  if (!fdt_conv_ok(cin, cout) || !aligned16(dz) || !aligned16(w) || !aligned16(dx) ||
+                            int n, int h, int w_, int cin, int cout, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
+  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(dz) || !aligned16(w) || !aligned16(dx) ||
       (mask && !aligned16(mask)))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
+  if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
+  float* wlo = static_cast<float*>(ws);
   fdt::EMask epi{dx, mask};
   if (fdt::bn_for(cin) == 64)
-    return fdt::run<64, true>(dz, w, n, h, w_, cin, cout, epi, st);
-  return fdt::run<128, true>(dz, w, n, h, w_, cin, cout, epi, st);
+    return fdt::run<64, true>(dz, w, wlo, n, h, w_, cin, cout, epi, st);
+  return fdt::run<128, true>(dz, w, wlo, n, h, w_, cin, cout, epi, st);
 }
 
 }  // namespace bpx
