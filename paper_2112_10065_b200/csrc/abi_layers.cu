@@ -84,17 +84,21 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   return simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
 }
 
+static size_t max3(size_t a, size_t b, size_t c) {
+  size_t m = a > b ? a : b;
+  return m > c ? m : c;
+}
 size_t bpx_linear_fwd_workspace(int b, int in, int out) {
-  size_t a = simt_linear_fwd_ws(b, in, out), c = tc_linear_fwd_ws(b, in, out);
-  return a > c ? a : c;
+  return max3(simt_linear_fwd_ws(b, in, out), tc_linear_fwd_ws(b, in, out),
+              dns_linear_ws(b, in, out));
 }
 size_t bpx_linear_dgrad_workspace(int b, int in, int out) {
-  size_t a = simt_linear_dgrad_ws(b, in, out), c = tc_linear_dgrad_ws(b, in, out);
-  return a > c ? a : c;
+  return max3(simt_linear_dgrad_ws(b, in, out), tc_linear_dgrad_ws(b, in, out),
+              dns_linear_ws(b, in, out));
 }
 size_t bpx_linear_wgrad_workspace(int b, int in, int out) {
-  size_t a = simt_linear_wgrad_ws(b, in, out), c = tc_linear_wgrad_ws(b, in, out);
-  return a > c ? a : c;
+  return max3(simt_linear_wgrad_ws(b, in, out), tc_linear_wgrad_ws(b, in, out),
+              dns_linear_ws(b, in, out));
 }
 
 bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, float* y,
@@ -102,6 +106,8 @@ bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, f
                             void* stream) {
   BPX_CHECK_ARG(x && w && y && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (dns_linear_ok(b, in, out))
+    return dns_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out))
     return tc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
   return simt_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
@@ -112,6 +118,8 @@ bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask
                               void* stream) {
   BPX_CHECK_ARG(dy && w && dx && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (dns_linear_ok(b, in, out))
+    return dns_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out))
     return tc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
   return simt_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
@@ -122,6 +130,8 @@ bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float*
                               void* stream) {
   BPX_CHECK_ARG(x && dy && dw && b >= 0 && in > 0 && out > 0 && aligned16(dw));
   cudaStream_t st = as_stream(stream);
+  if (dns_linear_ok(b, in, out))
+    return dns_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out))
     return tc_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
   return simt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);

@@ -38,3 +38,17 @@ bpx_status_t small_conv_wgrad(const float* x, const float* dz, float* dw, float*
                               int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
                               cudaStream_t st);
 }  // namespace bpx
+
+// FFMA dense layers for per-GPU batches <= 32 (dense_ffma.cu).
+namespace bpx {
+bool dns_linear_ok(int b, int in, int out);
+size_t dns_linear_ws(int b, int in, int out);
+bpx_status_t dns_linear_fwd(const float* x, const float* w, const float* bias, float* y, int b,
+                            int in, int out, int relu, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
+bpx_status_t dns_linear_dgrad(const float* dy, const float* w, const float* mask, float* dx,
+                              int b, int in, int out, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
+bpx_status_t dns_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias, int b,
+                              int in, int out, void* ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace bpx
