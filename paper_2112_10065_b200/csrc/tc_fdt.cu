@@ -41,7 +41,7 @@ namespace fdt {
 using namespace tcx;
 
 constexpr int BK = 32;                 // K elements per stage (one channel chunk of a tap)
-constexpr int PCH = 2;                 // stages per TMEM promotion chunk
+constexpr int PCH = 4;                 // stages per TMEM promotion chunk (K = 128)
 constexpr int NTHREADS = 14 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
 
@@ -249,7 +249,6 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
           if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
-          tc_fence_after();
           const int sh = (tap / 3 - 1) * g.W + (tap % 3 - 1);
           const int hr = r + g.W + 1 + (DG ? -sh : sh);
           const bool ok = (tmask >> tap) & 1u;
@@ -264,6 +263,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
             split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
           }
+          tc_fence_after();
           const uint32_t a = lanebase + s * 2 * BK;
           tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
           tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));

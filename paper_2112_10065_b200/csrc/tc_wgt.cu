@@ -37,7 +37,7 @@ using namespace tcx;
 
 constexpr int BK = 32;                 // pixels per stage (rows of every box)
 constexpr int BOX = 32 * BK * 4;       // one 32-channel x 32-pixel box, bytes
-constexpr int PCH = 2;                 // stages per TMEM promotion chunk
+constexpr int PCH = 4;                 // stages per TMEM promotion chunk (K = 128)
 constexpr int NTHREADS = 18 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, CB0 = 6, DR0 = 10;   // warps 2-5: A converters
 
