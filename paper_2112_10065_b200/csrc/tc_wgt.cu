@@ -35,16 +35,19 @@ namespace bpx {
 namespace wgt {
 using namespace tcx;
 
-constexpr int BK = 32;                 // pixels per stage (rows of every box)
-constexpr int BOX = 32 * BK * 4;       // one 32-channel x 32-pixel box, bytes
-constexpr int PCH = 4;                 // stages per TMEM promotion chunk (K = 128)
 constexpr int NTHREADS = 18 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, CB0 = 6, DR0 = 10;   // warps 2-5: A converters
 
+// BN = 128: 32 pixels per stage, 4 stages.  BN = 64 (Cout = 64): 64 pixels
+// per stage, 3 stages -- a stage then carries as many MMA cycles as a
+// BN = 128 stage, so the per-stage handshakes cost the same fraction.
 template <int BN>
 struct Cfg {
   static_assert(BN == 64 || BN == 128, "BN");
-  static constexpr int S = BN == 128 ? 4 : 6;
+  static constexpr int BK = BN == 128 ? 32 : 64;          // pixels per stage
+  static constexpr int BOX = 32 * BK * 4;                 // 32 channels x BK pixels
+  static constexpr int PCH = 128 / BK;                    // stages per promotion chunk (K = 128)
+  static constexpr int S = BN == 128 ? 4 : 3;
   static constexpr int A_BYTES = 4 * BOX;                 // 128 rows of A
   static constexpr int B_BYTES = (BN / 32) * BOX;
   static constexpr int STAGE = A_BYTES + 2 * B_BYTES;     // A raw | B raw | B lo
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
   using Cf = Cfg<BN>;
+  constexpr int BK = Cf::BK, BOX = Cf::BOX, PCH = Cf::PCH;
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
@@ -176,37 +180,49 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     const int g8 = lane >> 3, w4 = (lane & 7) * 4;
     const int gc = m0 / 32 + q, tap = valid ? gc / cpt : 4;
     const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-    // coordinates of pixel p0 + lane, advanced by 32 pixels per stage
+    // coordinates of pixel p0 + lane (+32 per half), advanced by BK pixels per stage
     long long p = (long long)t0 * BK + lane;
     int img = (int)(p / ((long long)g.H * g.W));
     int rem = (int)(p - (long long)img * g.H * g.W);
     int oh = rem / g.W, ow = rem - (rem / g.W) * g.W;
-    for (int i = 0; i < nst; ++i) {
-      const int s = i % Cf::S;
-      const bool ok = valid && p < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
-                      (unsigned)(ow + dx) < (unsigned)g.W;
-      const uint32_t vmask = __ballot_sync(0xffffffffu, ok);
-      p += BK;
-      ow += BK;
+    auto advance = [&](int by) {
+      p += by;
+      ow += by;
       while (ow >= g.W) {
         ow -= g.W;
         if (++oh == g.H) { oh = 0; ++img; }
       }
+    };
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % Cf::S;
+      uint32_t vmask[BK / 32];
+#pragma unroll
+      for (int h = 0; h < BK / 32; ++h) {
+        const bool ok = valid && p < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
+                        (unsigned)(ow + dx) < (unsigned)g.W;
+        vmask[h] = __ballot_sync(0xffffffffu, ok);
+        advance(32);
+      }
       mbar_wait(&full[s], (i / Cf::S) & 1);
       const char* box = smem + s * Cf::STAGE + q * BOX;
-      float hi[BK], lo[BK];
-#pragma unroll
-      for (int k = 0; k < BK; ++k) {
-        const float v = ((vmask >> k) & 1u) ? *reinterpret_cast<const float*>(
-                                                box + k * 128 + ((g8 ^ (k & 3)) << 5) + w4)
-                                          : 0.f;
-        split(v, hi[k], lo[k]);
-      }
       const uint32_t a = lanebase + s * 2 * BK;
-      tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
-      tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
-      tmem_st16(a + BK, *reinterpret_cast<float(*)[16]>(lo));
-      tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+#pragma unroll
+      for (int h = 0; h < BK / 32; ++h) {
+        float hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int kk = 32 * h + k;
+          const float v = ((vmask[h] >> k) & 1u)
+                              ? *reinterpret_cast<const float*>(box + kk * 128 +
+                                                                ((g8 ^ (kk & 3)) << 5) + w4)
+                              : 0.f;
+          split(v, hi[k], lo[k]);
+        }
+        tmem_st16(a + 32 * h, *reinterpret_cast<float(*)[16]>(hi));
+        tmem_st16(a + 32 * h + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
+        tmem_st16(a + BK + 32 * h, *reinterpret_cast<float(*)[16]>(lo));
+        tmem_st16(a + BK + 32 * h + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&aready[s]);
@@ -298,7 +314,7 @@ inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
 inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
   g.Cin = cin; g.Cout = cout; g.H = H; g.W = W;
   g.npix = (long long)n * H * W;
-  g.tiles = (int)cdivll(g.npix, BK);
+  g.tiles = (int)cdivll(g.npix, bn_for(cout) == 128 ? Cfg<128>::BK : Cfg<64>::BK);
   g.slab = (long long)cout * 9 * cin;
   mt = cdiv(9 * cin, 128);
   nt = cout / bn_for(cout);
@@ -310,8 +326,8 @@ inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& n
   splits = cdiv(g.tiles, g.tps);
 }
 
-// [pixels][C] fp32, box = 32 channels x 32 pixels, MN-major tf32 layout.
-inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C) {
+// [pixels][C] fp32, box = 32 channels x BK pixels, MN-major tf32 layout.
+inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C, int BK) {
   const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)npix};
   const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
   const cuuint32_t box[2] = {32, (cuuint32_t)BK};
@@ -369,7 +385,9 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
   int mt, nt, splits;
   wgt::plan(n, h, w_, cin, cout, g, mt, nt, splits);
   CUtensorMap tx, tdz;
-  if (!wgt::encode_rows(&tx, x, g.npix, cin) || !wgt::encode_rows(&tdz, dz, g.npix, cout))
+  const int bk = wgt::bn_for(cout) == 128 ? wgt::Cfg<128>::BK : wgt::Cfg<64>::BK;
+  if (!wgt::encode_rows(&tx, x, g.npix, cin, bk) ||
+      !wgt::encode_rows(&tdz, dz, g.npix, cout, bk))
     return BPX_ERR_INVALID_ARGUMENT;
   float* part = splits == 1 ? dw : static_cast<float*>(ws);
   float* bpart = !dbias ? nullptr
