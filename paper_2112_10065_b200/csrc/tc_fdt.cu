@@ -45,10 +45,10 @@ constexpr int PCH = 4;                 // stages per TMEM promotion chunk (K = 1
 constexpr int NTHREADS = 14 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
 
-template <int BN>
+template <int BN, int NS = 4>
 struct Cfg {
   static_assert(BN == 64 || BN == 128, "BN");
-  static constexpr int S = 4;                             // B / TMEM-A stages
+  static constexpr int S = NS;                            // B / TMEM-A stages
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = 2 * B_BYTES;               // B raw | B lo
   static constexpr int A_COL = 2 * BN;
@@ -99,11 +99,11 @@ struct EMask {
   }
 };
 
-template <int BN, bool DG, class EPI>
+template <int BN, int NS, bool DG, class EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
-  using Cf = Cfg<BN>;
+  using Cf = Cfg<BN, NS>;
   constexpr int S = Cf::S;
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -352,6 +352,9 @@ template <int BN, bool DG, class EPI>
 bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W, int Cin,
                  int Cout, EPI epi, cudaStream_t st) {
   using Cf = Cfg<BN>;
+  // BN = 64 leaves TMEM for 6 A stages (64 + 64 accumulator columns); use
+  // them when the halo ring still fits in shared memory.
+  using Cf6 = Cfg<64, 6>;
   Geo g;
   g.H = H; g.W = W;
   g.C = DG ? Cout : Cin;
@@ -364,7 +367,8 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
   g.nhbox = cdiv(g.hrows, 256);
   g.hbox = cdiv(cdiv(g.hrows, g.nhbox), 8) * 8;
   g.halo_bytes = g.nhbox * g.hbox * 128;
-  const int smem = Cf::smem(g.halo_bytes);
+  const bool deep = BN == 64 && Cf6::smem(g.halo_bytes) <= 227 * 1024;
+  const int smem = deep ? Cf6::smem(g.halo_bytes) : Cf::smem(g.halo_bytes);
   if (smem > 227 * 1024) return BPX_ERR_INVALID_ARGUMENT;
   CUtensorMap ta, tb;
   {
@@ -397,10 +401,14 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
   if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
   split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
                                          reinterpret_cast<float4*>(wlo), n4);
-  auto kern = fdt_kernel<BN, DG, EPI>;
+  constexpr int DEEP = BN == 64 ? 6 : 4;
+  auto kern = deep ? fdt_kernel<BN, DEEP, DG, EPI> : fdt_kernel<BN, 4, DG, EPI>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fdt_kernel<BN, 4, DG, EPI>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fdt_kernel<BN, DEEP, DG, EPI>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int grid = g.tiles < num_sms() ? g.tiles : num_sms();
