@@ -180,9 +180,24 @@ def _time_gemm_ops(st, reps=5):
     return rows
 
 
+def _ncu_traffic(dom):
+    """DRAM bytes per launch of the dominant op from the committed ncu
+    --set full capture (profiles/dominant_traffic.json, written by
+    tools/ncu_traffic.py), or None when no capture of this op exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dominant_traffic.json")) as fh:
+            rec = json.load(fh).get(f"{dom['layer']} {dom['op']}")
+    except Exception:
+        return None, None
+    if not rec:
+        return None, None
+    return rec["traffic"], rec
+
+
 def _roofline(dom, tf32_peak, peak_src, step_ms, flops_step, gemm_ms):
     if dom is None:
         return None
+    traffic, rec = _ncu_traffic(dom)
     achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
     return {
         "bound": "tensor", "unit": "TFLOP/s",
@@ -196,7 +211,10 @@ def _roofline(dom, tf32_peak, peak_src, step_ms, flops_step, gemm_ms):
         "step_gemm": {"flops": flops_step, "ms_sum_of_launches": gemm_ms,
                       "achieved_tflops": flops_step / (gemm_ms / 1e3) / 1e12,
                       "share_of_step": gemm_ms / step_ms},
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": (f"ncu --set full ({rec['source']}): dram read {rec['dram_read']:.3e} "
+                           f"+ write {rec['dram_write']:.3e} B per launch; tensor pipe "
+                           f"{rec['tensor_pipe_pct']:.1f}% active") if rec else None,
     }
 
 

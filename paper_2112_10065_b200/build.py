@@ -55,7 +55,7 @@ def build(force=False, verbose=False):
         if verbose and out:
             sys.stderr.write(out.decode())
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

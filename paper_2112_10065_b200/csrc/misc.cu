@@ -51,8 +51,22 @@ size_t colsum_workspace_floats(long long rows, int cols) {
   return (size_t)colsum_parts(rows) * (size_t)cols;
 }
 
+// Few rows (a dense layer's batch): one thread per column, rows in order.
+__global__ void colsum_rows(const float* __restrict__ in, int rows, int cols,
+                            float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += in[(long long)r * cols + c];
+  out[c] = s;
+}
+
 bpx_status_t colsum(const float* in, long long rows, int cols, float* out,
                     float* ws, size_t ws_floats, cudaStream_t st) {
+  if (rows <= 512) {
+    colsum_rows<<<cdiv(cols, 128), 128, 0, st>>>(in, (int)rows, cols, out);
+    return launch_status();
+  }
   int parts = colsum_parts(rows);
   if (ws_floats < (size_t)parts * cols) return BPX_ERR_WORKSPACE;
   long long chunk = cdivll(rows, parts);

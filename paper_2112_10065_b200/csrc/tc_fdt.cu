@@ -32,7 +32,7 @@
 //
 // CTA: 14 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters,
 // 6-13 drain + epilogue.
-#include <cuda.h>
+#include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "tc_api.h"
 
@@ -341,7 +341,7 @@ __global__ void split_lo_kernel(const float4* __restrict__ w, float4* __restrict
 inline bool encode(CUtensorMap* m, const float* p, int rank, const cuuint64_t* dims,
                    const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
   const cuuint32_t es[3] = {1, 1, 1};
-  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
                                 const_cast<float*>(p), dims, strides, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

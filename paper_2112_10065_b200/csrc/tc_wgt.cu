@@ -27,7 +27,7 @@
 //
 // CTA: 18 warps, one CTA per SM.  warp 0 TMA producer, warp 1 MMA issuer +
 // TMEM owner, warps 2-5 A converters, 6-9 B converters (+bias), 10-17 drain.
-#include <cuda.h>
+#include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "tc_api.h"
 
@@ -332,7 +332,7 @@ inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C, i
   const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
   const cuuint32_t box[2] = {32, (cuuint32_t)BK};
   const cuuint32_t es[2] = {1, 1};
-  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                 const_cast<float*>(p), dims, strides, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,

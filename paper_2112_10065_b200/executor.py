@@ -97,8 +97,12 @@ class BurstStep:
         for L in self.layers:
             if L.active and L.spec.param_shapes():
                 sizes[L.g] = sizes.get(L.g, 0) + _pad4(L.spec.n_params())
+        # parameters live in flat buffers with the same layout as the gradient
+        # buckets, so the SGD update is one launch per bucket
+        self.pbuckets: dict[int, torch.Tensor] = {}
         for g, n in sizes.items():
             self.buckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
+            self.pbuckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
         cursor = {g: 0 for g in sizes}
 
         ws_need = 0
@@ -122,11 +126,13 @@ class BurstStep:
             ps = sp.param_shapes()
             if ps:
                 w, b = params[sp.name]
-                L.w = w.to(dev).contiguous()
-                L.bias = b.to(dev).contiguous()
-                flat = self.buckets[L.g]
+                flat, pflat = self.buckets[L.g], self.pbuckets[L.g]
                 c = cursor[L.g]
                 nw, nb = w.numel(), b.numel()
+                L.w = pflat[c:c + nw].view(ps[0])
+                L.w.copy_(w.reshape(ps[0]))
+                L.bias = pflat[c + nw:c + nw + nb]
+                L.bias.copy_(b.reshape(-1))
                 L.dw = flat[c:c + nw].view(ps[0])
                 L.dbias = flat[c + nw:c + nw + nb]
                 cursor[L.g] = c + _pad4(nw + nb)
@@ -246,10 +252,8 @@ class BurstStep:
         self.k.softmax_xent(last.y, self.labels[:last.b], self.B, self.loss_buf, last.dy)
 
     def _sgd(self) -> None:
-        for L in self.layers:
-            if L.active and L.w is not None:
-                self.k.sgd_update(L.w, L.dw, self.lr)
-                self.k.sgd_update(L.bias, L.dbias, self.lr)
+        for g in sorted(self.buckets):
+            self.k.sgd_update(self.pbuckets[g], self.buckets[g], self.lr)
 
     def run_ops(self, prog) -> None:
         for key, fn in prog:
