@@ -8,9 +8,9 @@
 //     splits into TF32 hi/lo and tcgen05.st's them; the MMA reads A from TMEM.
 //   * B = im2col(x) is produced into shared memory in the UMMA K-major
 //     no-swizzle layout with 4x4 register transposes (4 channels x 4
-//     pixels per thread).  (An MN-major B tile would avoid the transpose,
-//     but kind::tf32 with an MN-major B operand returned all zeros on B200
-//     in both the no-swizzle and 128B-swizzle layouts, so it is not used.)
+//     pixels per thread).  (Fallback engine: tc_wgt.cu reads MN-major tiles
+//     directly -- kind::tf32 takes MN-major operands only in the
+//     SWIZZLE_128B_BASE32B layout, see tools/probes/probe_mn.cu.)
 //   * hi*hi + hi*lo + lo*hi accumulate in 64-K chunks in ping-pong TMEM
 //     buffers, promoted to RN fp32 registers by drain warps (see tc_engine.cu
 //     for why: the tensor core's fp32 accumulate truncates).
