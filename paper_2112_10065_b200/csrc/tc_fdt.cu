@@ -124,14 +124,14 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&bfull[s], 1);
-      mbar_init(&aready[s], 128);
+      mbar_init(&aready[s], 4);          // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
-      mbar_init(&hempty[b], 128);
+      mbar_init(&hempty[b], 4);
       mbar_init(&accfull[b], 1);
-      mbar_init(&accfree[b], 256);
+      mbar_init(&accfree[b], 8);         // one arrival per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -271,9 +271,11 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
-          mbar_arrive(&aready[s]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&aready[s]);
         }
-        mbar_arrive(&hempty[hs]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hempty[hs]);
       }
     }
   } else {
@@ -300,7 +302,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           for (int u = 0; u < 8; ++u) acc[j + u] += __uint_as_float(rr[u]);
         }
         tc_fence_before();
-        mbar_arrive(&accfree[b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accfree[b]);
       }
       const long long p = (long long)(t / g.nt) * 128 + q * 32 + lane;
       const int n0 = (t % g.nt) * BN + hf * CW;

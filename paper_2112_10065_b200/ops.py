@@ -17,7 +17,7 @@ import torch
 from .errors import ExtensionMissingError, KernelError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbpx.so")
+LIB_PATH = os.environ.get("BPX_LIB", os.path.join(_HERE, "libbpx.so"))  # BPX_LIB: A/B timing of builds
 
 _lib = None
 
