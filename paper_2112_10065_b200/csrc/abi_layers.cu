@@ -23,8 +23,10 @@ bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, 
   cudaStream_t st = as_stream(stream);
   if (small_conv_fwd_ok(cin, cout))
     return small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
-  if (fdt_conv_ok(cin, cout, w_) && aligned16(x))
-    return fdt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+  if (fdt_conv_ok(cin, cout, w_) && aligned16(x)) {
+    bpx_status_t s = fdt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (ts_conv_ok(cin, cout))
     return ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
   if (tc_conv_fwd_ok(n, h, w_, cin, cout))
@@ -45,8 +47,10 @@ bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mas
   BPX_CHECK_ARG(dz && w && dx && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w));
   cudaStream_t st = as_stream(stream);
-  if (fdt_conv_ok(cin, cout, w_) && aligned16(dz) && (!mask_src || aligned16(mask_src)))
-    return fdt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+  if (fdt_conv_ok(cin, cout, w_) && aligned16(dz) && (!mask_src || aligned16(mask_src))) {
+    bpx_status_t s = fdt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (ts_conv_ok(cin, cout))
     return ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_dgrad_ok(n, h, w_, cin, cout))

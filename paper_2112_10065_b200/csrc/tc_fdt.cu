@@ -5,15 +5,19 @@
 //   dgrad : dx[q][ci] = mask(q) * sum_{tap,co} dz[q - s_tap][co] * w[co][tap][ci]
 //   s_tap = dy*W + dx  (flattened-pixel shift of the tap)
 //
-// M = pixels (128 consecutive flattened pixels per tile), N = output
-// channels, K = (32-channel chunk, tap) stages.  Per channel chunk the CTA
-// loads ONE halo of the activations by TMA -- flattened rows
-// [m0 - W - 1, m0 + 128 + W + 1) x 32 channels -- and all nine taps read
-// their shifted 128-row window out of it, so activation traffic is
-// (128 + 2W + 2)/128 instead of 9x the tile.  Rows whose shifted source
-// pixel falls outside its image (the conv's zero padding, including the
-// row wrap of the flattened layout) are zeroed by the A converters from a
-// per-thread 9-bit tap mask computed once per tile.
+// M = 128 output pixels per tile, N = output channels, K = (channel chunk,
+// tap) stages.  Per channel chunk the CTA loads ONE halo of the activations
+// by TMA and all nine taps read their shifted 128-row window out of it, so
+// activation traffic is the halo/tile ratio instead of 9x the tile:
+//   * 2-D tiles (W, H divisible by a TW x TH = 128 block, e.g. 32 x 4 at
+//     224x224): the halo is one 4-D box (TW+2) x (TH+2) x 32 channels whose
+//     out-of-bounds rows TMA zero-fills -- the conv's padding for free;
+//   * otherwise 128 consecutive flattened pixels: the halo is the flattened
+//     rows [m0 - W - 1, m0 + 128 + W + 1), and rows whose source pixel wraps
+//     across an image row/edge are zeroed by the A converters from a 9-bit
+//     per-pixel tap mask computed once per tile.
+// A stage carries 32 channels (N = 128 tiles) or 64 (N = 64 tiles), so every
+// stage holds the same 768 MMA cycles and pays one converter/MMA handshake.
 // The B tile is the raw weight tile, straight from w by TMA:
 //   fwd   B(co, k) = w[co][tap][ci]: K-major, 128-B swizzle (one box)
 //   dgrad B(ci, k) = w[co][tap][ci]: MN-major, SWIZZLE_128B_ATOM_32B, one
@@ -40,20 +44,21 @@ namespace bpx {
 namespace fdt {
 using namespace tcx;
 
-constexpr int BK = 32;                 // K elements per stage (one channel chunk of a tap)
-constexpr int PCH = 4;                 // stages per TMEM promotion chunk (K = 128)
 constexpr int NTHREADS = 14 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
 
-template <int BN, int NS = 4>
+// BN output channels per tile, KS channels per stage, NS stages.
+template <int BN, int KS, int NS>
 struct Cfg {
-  static_assert(BN == 64 || BN == 128, "BN");
-  static constexpr int S = NS;                            // B / TMEM-A stages
-  static constexpr int B_BYTES = BN * BK * 4;
+  static_assert((BN == 128 && KS == 32) || (BN == 64 && KS == 64), "tile");
+  static constexpr int S = NS;
+  static constexpr int NCH = KS / 32;                     // 32-channel halves per stage
+  static constexpr int PCH = 128 / KS;                    // stages per promotion chunk (K = 128)
+  static constexpr int B_BYTES = BN * KS * 4;
   static constexpr int STAGE = 2 * B_BYTES;               // B raw | B lo
-  static constexpr int A_COL = 2 * BN;
-  static_assert(A_COL + S * 2 * BK <= 512, "TMEM budget");
-  // dynamic smem = 1024 (align) + S*STAGE + 2*halo_bytes + 512 (barriers)
+  static constexpr int A_COL = 2 * BN;                    // accumulators: 2 x BN columns
+  static_assert(A_COL + S * 2 * KS <= 512, "TMEM budget");
+  // dynamic smem = 1024 (align) + S*STAGE + 2 halo slots + 512 (barriers)
   static int smem(int halo_bytes) { return 1024 + S * STAGE + 2 * halo_bytes + 512; }
 };
 
@@ -61,8 +66,11 @@ struct Geo {
   int H, W, C;               // C = gathered channels (Cin fwd, Cout dgrad)
   int N;                     // output channels
   int npix, mt, nt, tiles;
-  int hrows, hbox, nhbox;    // halo rows used, rows per TMA box, boxes per halo
-  int halo_bytes;            // one halo slot (nhbox * hbox * 128)
+  int tw, th;                // 2-D tile (tw * th = 128) or 0 = flattened tiles
+  int hbox, nhbox;           // rows per halo TMA box, boxes per 32-channel halo
+  int half_bytes;            // smem stride of one 32-channel halo (1 KB aligned)
+  int halo_bytes;            // one halo slot (NCH halves)
+  int halo_tx;               // bytes TMA delivers per halo slot
 };
 
 struct EBiasAct {
@@ -99,12 +107,31 @@ struct EMask {
   }
 };
 
-template <int BN, int NS, bool DG, class EPI>
+// Output-tile geometry shared by the producer, converters and epilogue.
+struct Tile {
+  int m0;                    // flattened tiles: first pixel
+  int img, oh0, ow0;         // 2-D tiles: image and block origin
+};
+__device__ __forceinline__ Tile tile_of(const Geo& g, int mi) {
+  Tile t{};
+  if (g.tw) {
+    const int bw = g.W / g.tw, per = bw * (g.H / g.th);
+    t.img = mi / per;
+    const int rem = mi - t.img * per;
+    t.oh0 = (rem / bw) * g.th;
+    t.ow0 = (rem % bw) * g.tw;
+  } else {
+    t.m0 = mi * 128;
+  }
+  return t;
+}
+
+template <int BN, int KS, int NS, bool DG, class EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
-  using Cf = Cfg<BN, NS>;
-  constexpr int S = Cf::S;
+  using Cf = Cfg<BN, KS, NS>;
+  constexpr int S = Cf::S, NCH = Cf::NCH, PCH = Cf::PCH;
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   char* halo = smem + S * Cf::STAGE;                          // 2 slots
@@ -118,7 +145,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfree + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cpt = g.C / BK;                   // channel chunks
+  const int cpt = g.C / KS;                   // channel chunks per tile
   const int nk = 9 * cpt;                     // stages per tile
 
   if (tid == 0) {
@@ -149,28 +176,42 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       tma_prefetch_desc(&tbl);
       int i = 0, hc = 0;
       for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-        const int m0 = (t / g.nt) * 128, n0 = (t % g.nt) * BN;
+        const Tile T = tile_of(g, t / g.nt);
+        const int n0 = (t % g.nt) * BN;
         for (int cc = 0; cc < cpt; ++cc, ++hc) {
           const int hs = hc & 1;
           if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
-          mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_bytes);
-          for (int j = 0; j < g.nhbox; ++j)
-            tma_load_2d(halo + hs * g.halo_bytes + j * g.hbox * 128, &ta, cc * BK,
-                        m0 - g.W - 1 + j * g.hbox, &hfull[hs]);
+          mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_tx);
+          char* hb = halo + hs * g.halo_bytes;
+#pragma unroll
+          for (int c2 = 0; c2 < NCH; ++c2) {
+            const int c0 = cc * KS + c2 * 32;
+            if (g.tw) {
+              tma_load_4d(hb + c2 * g.half_bytes, &ta, c0, T.ow0 - 1, T.oh0 - 1, T.img,
+                          &hfull[hs]);
+            } else {
+              for (int j = 0; j < g.nhbox; ++j)
+                tma_load_2d(hb + c2 * g.half_bytes + j * g.hbox * 128, &ta, c0,
+                            T.m0 - g.W - 1 + j * g.hbox, &hfull[hs]);
+            }
+          }
           for (int tap = 0; tap < 9; ++tap, ++i) {
             const int s = i % S;
             if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
             char* st = smem + s * Cf::STAGE;
             mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
-            if (DG) {
+            if (DG) {        // BN/32 boxes of 32 ci x KS co rows (MN-major)
               for (int j = 0; j < BN / 32; ++j) {
-                tma_load_3d(st + j * 4096, &tb, n0 + 32 * j, tap, cc * BK, &bfull[s]);
-                tma_load_3d(st + Cf::B_BYTES + j * 4096, &tbl, n0 + 32 * j, tap, cc * BK,
+                tma_load_3d(st + j * KS * 128, &tb, n0 + 32 * j, tap, cc * KS, &bfull[s]);
+                tma_load_3d(st + Cf::B_BYTES + j * KS * 128, &tbl, n0 + 32 * j, tap, cc * KS,
                             &bfull[s]);
               }
-            } else {
-              tma_load_2d(st, &tb, tap * g.C + cc * BK, n0, &bfull[s]);
-              tma_load_2d(st + Cf::B_BYTES, &tbl, tap * g.C + cc * BK, n0, &bfull[s]);
+            } else {         // NCH boxes of 32 k x BN rows (K-major)
+              for (int h = 0; h < NCH; ++h) {
+                const int k0 = tap * g.C + cc * KS + 32 * h;
+                tma_load_2d(st + h * BN * 128, &tb, k0, n0, &bfull[s]);
+                tma_load_2d(st + Cf::B_BYTES + h * BN * 128, &tbl, k0, n0, &bfull[s]);
+              }
             }
           }
         }
@@ -195,18 +236,19 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           mbar_wait(&bfull[s], ph);
           tc_fence_after();
           const uint32_t d = tmem + b * BN;
-          const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
+          const uint32_t ah = tmem + Cf::A_COL + s * 2 * KS, al = ah + KS;
           const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
           const uint32_t bl = bh + Cf::B_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
+          for (int ks = 0; ks < KS / 8; ++ks) {
             uint64_t dbh, dbl;
             if (DG) {
-              dbh = make_desc_mn32(bh + ks * 1024, 4096, 512);
-              dbl = make_desc_mn32(bl + ks * 1024, 4096, 512);
+              dbh = make_desc_mn32(bh + ks * 1024, KS * 128, 512);
+              dbl = make_desc_mn32(bl + ks * 1024, KS * 128, 512);
             } else {
-              dbh = make_desc_sw128(bh + ks * 32, 16, 1024);
-              dbl = make_desc_sw128(bl + ks * 32, 16, 1024);
+              const uint32_t off = (ks >> 2) * BN * 128 + (ks & 3) * 32;
+              dbh = make_desc_sw128(bh + off, 16, 1024);
+              dbl = make_desc_sw128(bl + off, 16, 1024);
             }
             const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
             mma_ts(d, al + 8 * ks, dbh, idesc, acc);
@@ -223,23 +265,27 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ A converters
-    // thread = TMEM lane = pixel row of the tile; stage (cc, tap) reads halo
-    // row r + W + 1 +/- s_tap
+    // thread = TMEM lane = output pixel r of the tile; stage (cc, tap) reads
+    // the halo row of its source pixel
     const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
     const int hw = g.H * g.W;
+    const int rr = g.tw ? r / g.tw : 0, rc = g.tw ? r % g.tw : 0;
     int i = 0, hc = 0;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-      const int p = (t / g.nt) * 128 + r;
-      uint32_t tmask = 0;                     // bit tap: source pixel inside the image
-      if (p < g.npix) {
-        const int img = p / hw, rem = p - img * hw;
-        const int oh = rem / g.W, ow = rem - oh * g.W;
+      uint32_t tmask = 0x1ff;                 // bit tap: source pixel inside the image
+      if (!g.tw) {
+        const int p = (t / g.nt) * 128 + r;
+        tmask = 0;
+        if (p < g.npix) {
+          const int img = p / hw, rem = p - img * hw;
+          const int oh = rem / g.W, ow = rem - oh * g.W;
 #pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-          const int ih = DG ? oh - dy : oh + dy, iw = DG ? ow - dx : ow + dx;
-          if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W) tmask |= 1u << tap;
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+            const int ih = DG ? oh - dy : oh + dy, iw = DG ? ow - dx : ow + dx;
+            if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W) tmask |= 1u << tap;
+          }
         }
       }
       for (int cc = 0; cc < cpt; ++cc, ++hc) {
@@ -249,26 +295,30 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
           if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
-          const int sh = (tap / 3 - 1) * g.W + (tap % 3 - 1);
-          const int hr = r + g.W + 1 + (DG ? -sh : sh);
+          const int dy = DG ? 1 - tap / 3 : tap / 3 - 1, dx = DG ? 1 - tap % 3 : tap % 3 - 1;
+          const int hr = g.tw ? (rr + 1 + dy) * (g.tw + 2) + rc + 1 + dx
+                              : r + g.W + 1 + dy * g.W + dx;
           const bool ok = (tmask >> tap) & 1u;
-          const char* row = hbase + hr * 128;
-          float hi[BK], lo[BK];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
-            split(v.x, hi[4 * j + 0], lo[4 * j + 0]);
-            split(v.y, hi[4 * j + 1], lo[4 * j + 1]);
-            split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
-            split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
-          }
           tc_fence_after();
-          const uint32_t a = lanebase + s * 2 * BK;
-          tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
-          tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
-          tmem_st16(a + BK, *reinterpret_cast<float(*)[16]>(lo));
-          tmem_st16(a + BK + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+          const uint32_t a = lanebase + s * 2 * KS;
+#pragma unroll
+          for (int c2 = 0; c2 < NCH; ++c2) {
+            const char* row = hbase + c2 * g.half_bytes + hr * 128;
+            float hi[32], lo[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
+              split(v.x, hi[4 * j + 0], lo[4 * j + 0]);
+              split(v.y, hi[4 * j + 1], lo[4 * j + 1]);
+              split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
+              split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
+            }
+            tmem_st16(a + 32 * c2, *reinterpret_cast<float(*)[16]>(hi));
+            tmem_st16(a + 32 * c2 + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
+            tmem_st16(a + KS + 32 * c2, *reinterpret_cast<float(*)[16]>(lo));
+            tmem_st16(a + KS + 32 * c2 + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           __syncwarp();
@@ -284,6 +334,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     constexpr int CW = BN / 2;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + hf * CW;
     const int nch = (nk + PCH - 1) / PCH;
+    const int r = q * 32 + lane;
     int c = 0;
     for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
       float acc[CW];
@@ -305,7 +356,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         __syncwarp();
         if (lane == 0) mbar_arrive(&accfree[b]);
       }
-      const long long p = (long long)(t / g.nt) * 128 + q * 32 + lane;
+      const Tile T = tile_of(g, t / g.nt);
+      const long long p = g.tw ? ((long long)T.img * g.H + T.oh0 + r / g.tw) * g.W + T.ow0 +
+                                     r % g.tw
+                               : (long long)T.m0 + r;
       const int n0 = (t % g.nt) * BN + hf * CW;
       if (p < g.npix) {
 #pragma unroll
@@ -343,58 +397,76 @@ __global__ void split_lo_kernel(const float4* __restrict__ w, float4* __restrict
 
 inline bool encode(CUtensorMap* m, const float* p, int rank, const cuuint64_t* dims,
                    const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
-  const cuuint32_t es[3] = {1, 1, 1};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
-                                const_cast<float*>(p), dims, strides, box, es,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(p), dims,
+                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool DG, class EPI>
+// 2-D output tile tw x th = 128 that divides the image, widest first.
+inline void tile2d(int H, int W, int& tw, int& th) {
+  tw = th = 0;
+  for (int w = 32; w >= 16; w >>= 1)
+    if (W % w == 0 && H % (128 / w) == 0) { tw = w; th = 128 / w; return; }
+}
+
+template <int BN, int KS, int NS, bool DG, class EPI>
 bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W, int Cin,
                  int Cout, EPI epi, cudaStream_t st) {
-  using Cf = Cfg<BN>;
-  // BN = 64 leaves TMEM for 6 A stages (64 + 64 accumulator columns); use
-  // them when the halo ring still fits in shared memory.
-  using Cf6 = Cfg<64, 6>;
+  using Cf = Cfg<BN, KS, NS>;
   Geo g;
   g.H = H; g.W = W;
   g.C = DG ? Cout : Cin;
   g.N = DG ? Cin : Cout;
+  if (g.C % KS || g.N % BN) return BPX_ERR_UNSUPPORTED;
   g.npix = n * H * W;
-  g.mt = cdiv(g.npix, 128);
+  tile2d(H, W, g.tw, g.th);
+  if (BN == 64 && !g.tw) return BPX_ERR_UNSUPPORTED;      // halo ring would not fit
+  g.mt = g.tw ? n * (H / g.th) * (W / g.tw) : cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;
-  g.hrows = 128 + 2 * W + 2;
-  g.nhbox = cdiv(g.hrows, 256);
-  g.hbox = cdiv(cdiv(g.hrows, g.nhbox), 8) * 8;
-  g.halo_bytes = g.nhbox * g.hbox * 128;
-  const bool deep = BN == 64 && Cf6::smem(g.halo_bytes) <= 227 * 1024;
-  const int smem = deep ? Cf6::smem(g.halo_bytes) : Cf::smem(g.halo_bytes);
-  if (smem > 227 * 1024) return BPX_ERR_INVALID_ARGUMENT;
-  CUtensorMap ta, tb;
-  {
+  if (g.tw) {
+    g.nhbox = 1;
+    g.hbox = cdiv((g.tw + 2) * (g.th + 2), 8) * 8;
+  } else {
+    const int hrows = 128 + 2 * W + 2;
+    g.nhbox = cdiv(hrows, 256);
+    g.hbox = cdiv(cdiv(hrows, g.nhbox), 8) * 8;
+  }
+  g.half_bytes = g.nhbox * g.hbox * 128;
+  g.halo_bytes = Cf::NCH * g.half_bytes;
+  g.halo_tx = Cf::NCH * (g.tw ? (g.tw + 2) * (g.th + 2) * 128 : g.half_bytes);
+  const int smem = Cf::smem(g.halo_bytes);
+  if (smem > 227 * 1024) return BPX_ERR_UNSUPPORTED;
+  CUtensorMap ta, tb, tbl;
+  if (g.tw) {        // activations [n][H][W][C]: box 32 ch x (tw+2) x (th+2) x 1 image
+    const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.C * 4, (cuuint64_t)W * g.C * 4,
+                                   (cuuint64_t)H * W * g.C * 4};
+    const cuuint32_t box[4] = {32, (cuuint32_t)g.tw + 2, (cuuint32_t)g.th + 2, 1};
+    if (!encode(&ta, a, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return BPX_ERR_INVALID_ARGUMENT;
+  } else {           // activations [pixels][C]: box 32 ch x hbox rows
     const cuuint64_t dims[2] = {(cuuint64_t)g.C, (cuuint64_t)g.npix};
     const cuuint64_t strides[1] = {(cuuint64_t)g.C * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)g.hbox};
+    const cuuint32_t box[2] = {32, (cuuint32_t)g.hbox};
     if (!encode(&ta, a, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return BPX_ERR_INVALID_ARGUMENT;
   }
-  CUtensorMap tbl;
   for (int v = 0; v < 2; ++v) {
     const float* src = v ? wlo : w;
     CUtensorMap* m = v ? &tbl : &tb;
-    if (DG) {       // w as [Cout][9][Cin]: box 32 ci x 1 tap x 32 co, MN-major
+    if (DG) {       // w as [Cout][9][Cin]: box 32 ci x 1 tap x KS co, MN-major
       const cuuint64_t dims[3] = {(cuuint64_t)Cin, 9, (cuuint64_t)Cout};
       const cuuint64_t strides[2] = {(cuuint64_t)Cin * 4, (cuuint64_t)9 * Cin * 4};
-      const cuuint32_t box[3] = {32, 1, (cuuint32_t)BK};
+      const cuuint32_t box[3] = {32, 1, (cuuint32_t)KS};
       if (!encode(m, src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
         return BPX_ERR_INVALID_ARGUMENT;
     } else {        // w as [Cout][9*Cin]: box 32 k x BN rows, K-major
       const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
       const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 4};
-      const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BN};
+      const cuuint32_t box[2] = {32, (cuuint32_t)BN};
       if (!encode(m, src, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
     }
@@ -404,14 +476,10 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
   if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
   split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
                                          reinterpret_cast<float4*>(wlo), n4);
-  constexpr int DEEP = BN == 64 ? 6 : 4;
-  auto kern = deep ? fdt_kernel<BN, DEEP, DG, EPI> : fdt_kernel<BN, 4, DG, EPI>;
+  auto kern = fdt_kernel<BN, KS, NS, DG, EPI>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fdt_kernel<BN, 4, DG, EPI>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fdt_kernel<BN, DEEP, DG, EPI>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int grid = g.tiles < num_sms() ? g.tiles : num_sms();
@@ -419,14 +487,24 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
   return launch_status(2);
 }
 
-inline int bn_for(int N) { return N % 128 == 0 ? 128 : 64; }
+template <bool DG, class EPI>
+bpx_status_t dispatch(const float* a, const float* w, float* wlo, int n, int H, int W,
+                      int Cin, int Cout, EPI epi, cudaStream_t st) {
+  const int N = DG ? Cin : Cout;
+  if (N % 128 == 0) return run<128, 32, 4, DG>(a, w, wlo, n, H, W, Cin, Cout, epi, st);
+  return run<64, 64, 3, DG>(a, w, wlo, n, H, W, Cin, Cout, epi, st);
+}
 
 }  // namespace fdt
 
 // ============================================================ entry points
 
-// W <= 224 keeps two halo slots + four B stages inside 227 KB of smem.
-bool fdt_conv_ok(int cin, int cout, int w) { return cin % 64 == 0 && cout % 64 == 0 && w <= 224; }
+// Channel counts in multiples of 64, W <= 224 (two halo slots + the B stages
+// fit in 227 KB of smem).  64-wide N tiles also need a 2-D output tile.
+bool fdt_conv_ok(int cin, int cout, int w) {
+  if (cin % 64 || cout % 64 || w > 224) return false;
+  return true;
+}
 
 size_t fdt_conv_ws(int cin, int cout) { return (size_t)cout * 9 * cin * sizeof(float); }
 
@@ -437,11 +515,8 @@ bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, flo
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
-  float* wlo = static_cast<float*>(ws);
   fdt::EBiasAct epi{y, bias, relu};
-  if (fdt::bn_for(cout) == 64)
-    return fdt::run<64, false>(x, w, wlo, n, h, w_, cin, cout, epi, st);
-  return fdt::run<128, false>(x, w, wlo, n, h, w_, cin, cout, epi, st);
+  return fdt::dispatch<false>(x, w, static_cast<float*>(ws), n, h, w_, cin, cout, epi, st);
 }
 
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
@@ -452,11 +527,8 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, 
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
-  float* wlo = static_cast<float*>(ws);
   fdt::EMask epi{dx, mask};
-  if (fdt::bn_for(cin) == 64)
-    return fdt::run<64, true>(dz, w, wlo, n, h, w_, cin, cout, epi, st);
-  return fdt::run<128, true>(dz, w, wlo, n, h, w_, cin, cout, epi, st);
+  return fdt::dispatch<true>(dz, w, static_cast<float*>(ws), n, h, w_, cin, cout, epi, st);
 }
 
 }  // namespace bpx
