@@ -10,7 +10,7 @@ extern "C" {
 
 size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
   size_t a = tc_conv_fwd_ws(n, h, w_, cin, cout), b = ts_conv_ws(cin, cout);
-  size_t c = fdt_conv_ws(cin, cout);
+  size_t c = fdt_conv_ws(n, h, w_, cin, cout);
   a = a > b ? a : b;
   return a > c ? a : c;
 }
@@ -36,7 +36,7 @@ bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, 
 
 size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
   size_t a = tc_conv_dgrad_ws(n, h, w_, cin, cout), b = ts_conv_ws(cin, cout);
-  size_t c = fdt_conv_ws(cin, cout);
+  size_t c = fdt_conv_ws(n, h, w_, cin, cout);
   a = a > b ? a : b;
   return a > c ? a : c;
 }

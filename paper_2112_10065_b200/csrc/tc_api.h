@@ -70,7 +70,7 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
 // TMA-fed persistent forward / data-gradient engine (tc_fdt.cu).
 namespace bpx {
 bool fdt_conv_ok(int cin, int cout, int w);
-size_t fdt_conv_ws(int cin, int cout);
+size_t fdt_conv_ws(int n, int h, int w, int cin, int cout);
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
                           int h, int w_, int cin, int cout, int relu, void* ws,
                           size_t ws_bytes, cudaStream_t st);

@@ -71,6 +71,8 @@ struct Geo {
   int half_bytes;            // smem stride of one 32-channel halo (1 KB aligned)
   int halo_bytes;            // one halo slot (NCH halves)
   int halo_tx;               // bytes TMA delivers per halo slot
+  int ksplit, units;         // K halves per tile (1 or 2) and work units = tiles * ksplit
+  float* part;               // ksplit > 1: raw partial sums [ksplit][npix][N]
 };
 
 struct EBiasAct {
@@ -145,8 +147,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfree + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cpt = g.C / KS;                   // channel chunks per tile
-  const int nk = 9 * cpt;                     // stages per tile
+  const int cpu = g.C / KS / g.ksplit;        // channel chunks per work unit
+  const int nk = 9 * cpu;                     // stages per work unit
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -175,10 +177,11 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       tma_prefetch_desc(&tb);
       tma_prefetch_desc(&tbl);
       int i = 0, hc = 0;
-      for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+        const int t = u / g.ksplit, kh = u % g.ksplit;
         const Tile T = tile_of(g, t / g.nt);
         const int n0 = (t % g.nt) * BN;
-        for (int cc = 0; cc < cpt; ++cc, ++hc) {
+        for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           const int hs = hc & 1;
           if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
           mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_tx);
@@ -223,7 +226,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       // M=128, N=BN, tf32 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
       constexpr uint32_t idesc = make_idesc(BN) | (DG ? (1u << 16) : 0u);
       int i = 0, c = 0;
-      for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++i) {
           const int s = i % S;
           const uint32_t ph = (i / S) & 1;
@@ -272,7 +275,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int hw = g.H * g.W;
     const int rr = g.tw ? r / g.tw : 0, rc = g.tw ? r % g.tw : 0;
     int i = 0, hc = 0;
-    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+      const int t = u / g.ksplit;
       uint32_t tmask = 0x1ff;                 // bit tap: source pixel inside the image
       if (!g.tw) {
         const int p = (t / g.nt) * 128 + r;
@@ -288,7 +292,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
         }
       }
-      for (int cc = 0; cc < cpt; ++cc, ++hc) {
+      for (int cc = 0; cc < cpu; ++cc, ++hc) {
         const int hs = hc & 1;
         mbar_wait(&hfull[hs], (hc >> 1) & 1);
         const char* hbase = halo + hs * g.halo_bytes;
@@ -336,7 +340,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int nch = (nk + PCH - 1) / PCH;
     const int r = q * 32 + lane;
     int c = 0;
-    for (int t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+      const int t = u / g.ksplit, kh = u % g.ksplit;
       float acc[CW];
 #pragma unroll
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
@@ -362,12 +367,20 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                                : (long long)T.m0 + r;
       const int n0 = (t % g.nt) * BN + hf * CW;
       if (p < g.npix) {
+        if (g.ksplit > 1) {               // raw partial; fdt_finish applies the epilogue
+          float* o = g.part + ((long long)kh * g.npix + p) * g.N + n0;
 #pragma unroll
-        for (int j = 0; j < CW; j += 8) {
-          float v[8];
+          for (int j = 0; j < CW; j += 4)
+            *reinterpret_cast<float4*>(o + j) =
+                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = acc[j + u];
-          epi(p, n0 + j, g.N, v);
+          for (int j = 0; j < CW; j += 8) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = acc[j + e];
+            epi(p, n0 + j, g.N, v);
+          }
         }
       }
     }
@@ -382,6 +395,36 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 }
 
 // ------------------------------------------------------------------ host side
+
+// Split-K finish: out = epilogue(part[0] + part[1] + ...), fixed order.
+template <class EPI>
+__global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long npix, int N,
+                           EPI epi) {
+  const long long groups = npix * (N / 8);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < groups;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / (N / 8);
+    const int n0 = (int)(e % (N / 8)) * 8;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < ksplit; ++k) {
+      const float4* src = reinterpret_cast<const float4*>(part + ((long long)k * npix + p) * N + n0);
+      const float4 a = src[0], b = src[1];
+      v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+      v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    }
+    epi(p, n0, N, v);
+  }
+}
+
+// Work units: output tiles, split along K (2, 4 or 8 ways) while the tiles
+// alone would leave the persistent grid under two waves -- conv5 at 14x14
+// (196 tiles on 148 SMs), or any layer at the small per-GPU batches of a
+// wide burst plan; the parts' raw sums meet in fdt_finish.
+inline int ksplit_for(long long tiles, int chunks) {
+  int k = 1;
+  while (k < 8 && tiles * k < 2LL * num_sms() && chunks % (2 * k) == 0) k *= 2;
+  return k;
+}
 
 __global__ void split_lo_kernel(const float4* __restrict__ w, float4* __restrict__ lo,
                                 long long n4) {
@@ -412,8 +455,8 @@ inline void tile2d(int H, int W, int& tw, int& th) {
 }
 
 template <int BN, int KS, int NS, bool DG, class EPI>
-bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W, int Cin,
-                 int Cout, EPI epi, cudaStream_t st) {
+bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n, int H, int W,
+                 int Cin, int Cout, EPI epi, cudaStream_t st) {
   using Cf = Cfg<BN, KS, NS>;
   Geo g;
   g.H = H; g.W = W;
@@ -426,6 +469,9 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
   g.mt = g.tw ? n * (H / g.th) * (W / g.tw) : cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;
+  g.ksplit = ksplit_for(g.tiles, g.C / KS);
+  g.units = g.tiles * g.ksplit;
+  g.part = part;
   if (g.tw) {
     g.nhbox = 1;
     g.hbox = cdiv((g.tw + 2) * (g.th + 2), 8) * 8;
@@ -482,17 +528,22 @@ bpx_status_t run(const float* a, const float* w, float* wlo, int n, int H, int W
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const int grid = g.tiles < num_sms() ? g.tiles : num_sms();
+  const int grid = g.units < num_sms() ? g.units : num_sms();
   kern<<<grid, NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
-  return launch_status(2);
+  if (g.ksplit == 1) return launch_status(2);
+  const long long groups = (long long)g.npix * (g.N / 8);
+  int fg = (int)cdivll(groups, 256);
+  if (fg > 8 * num_sms()) fg = 8 * num_sms();
+  fdt_finish<<<fg, 256, 0, st>>>(part, g.ksplit, g.npix, g.N, epi);
+  return launch_status(3);
 }
 
 template <bool DG, class EPI>
-bpx_status_t dispatch(const float* a, const float* w, float* wlo, int n, int H, int W,
-                      int Cin, int Cout, EPI epi, cudaStream_t st) {
+bpx_status_t dispatch(const float* a, const float* w, float* wlo, float* part, int n, int H,
+                      int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
   const int N = DG ? Cin : Cout;
-  if (N % 128 == 0) return run<128, 32, 4, DG>(a, w, wlo, n, H, W, Cin, Cout, epi, st);
-  return run<64, 64, 3, DG>(a, w, wlo, n, H, W, Cin, Cout, epi, st);
+  if (N % 128 == 0) return run<128, 32, 4, DG>(a, w, wlo, part, n, H, W, Cin, Cout, epi, st);
+  return run<64, 64, 3, DG>(a, w, wlo, part, n, H, W, Cin, Cout, epi, st);
 }
 
 }  // namespace fdt
@@ -506,7 +557,23 @@ bool fdt_conv_ok(int cin, int cout, int w) {
   return true;
 }
 
-size_t fdt_conv_ws(int cin, int cout) { return (size_t)cout * 9 * cin * sizeof(float); }
+// workspace: the weights' lo split, then (split-K) raw partials [ksplit][pixels][N]
+size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
+  const size_t wlo = (size_t)cout * 9 * cin;
+  const long long npix = (long long)n * h * w;
+  size_t part = 0;
+  for (int dg = 0; dg < 2; ++dg) {        // fwd (N = cout) and dgrad (N = cin)
+    const int N = dg ? cin : cout, C = dg ? cout : cin;
+    const int ks = N % 128 == 0 ? 32 : 64;
+    const long long tiles = cdivll(npix, 128) * (N / (N % 128 == 0 ? 128 : 64));
+    const int k = C % ks == 0 ? fdt::ksplit_for(tiles, C / ks) : 1;
+    if (k > 1) {
+      const size_t need = (size_t)k * npix * N;
+      part = part > need ? part : need;
+    }
+  }
+  return (wlo + part) * sizeof(float);
+}
 
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
                           int h, int w_, int cin, int cout, int relu, void* ws,
@@ -514,9 +581,11 @@ bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, flo
   if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
-  if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
+  if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EBiasAct epi{y, bias, relu};
-  return fdt::dispatch<false>(x, w, static_cast<float*>(ws), n, h, w_, cin, cout, epi, st);
+  float* wlo = static_cast<float*>(ws);
+  return fdt::dispatch<false>(x, w, wlo, wlo + (size_t)cout * 9 * cin, n, h, w_, cin, cout, epi,
+                              st);
 }
 
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
@@ -526,9 +595,11 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, 
       (mask && !aligned16(mask)))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
-  if (ws_bytes < fdt_conv_ws(cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
+  if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EMask epi{dx, mask};
-  return fdt::dispatch<true>(dz, w, static_cast<float*>(ws), n, h, w_, cin, cout, epi, st);
+  float* wlo = static_cast<float*>(ws);
+  return fdt::dispatch<true>(dz, w, wlo, wlo + (size_t)cout * 9 * cin, n, h, w_, cin, cout, epi,
+                             st);
 }
 
 }  // namespace bpx
