@@ -93,12 +93,16 @@ static size_t max3(size_t a, size_t b, size_t c) {
   return m > c ? m : c;
 }
 size_t bpx_linear_fwd_workspace(int b, int in, int out) {
-  return max3(simt_linear_fwd_ws(b, in, out), tc_linear_fwd_ws(b, in, out),
-              dns_linear_ws(b, in, out));
+  size_t m = max3(simt_linear_fwd_ws(b, in, out), tc_linear_fwd_ws(b, in, out),
+                  dns_linear_ws(b, in, out));
+  size_t d = dtc_linear_ws(b, in, out);
+  return m > d ? m : d;
 }
 size_t bpx_linear_dgrad_workspace(int b, int in, int out) {
-  return max3(simt_linear_dgrad_ws(b, in, out), tc_linear_dgrad_ws(b, in, out),
-              dns_linear_ws(b, in, out));
+  size_t m = max3(simt_linear_dgrad_ws(b, in, out), tc_linear_dgrad_ws(b, in, out),
+                  dns_linear_ws(b, in, out));
+  size_t d = dtc_linear_ws(b, in, out);
+  return m > d ? m : d;
 }
 size_t bpx_linear_wgrad_workspace(int b, int in, int out) {
   return max3(simt_linear_wgrad_ws(b, in, out), tc_linear_wgrad_ws(b, in, out),
@@ -110,6 +114,10 @@ bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, f
                             void* stream) {
   BPX_CHECK_ARG(x && w && y && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (dtc_linear_ok(b, in, out)) {
+    bpx_status_t s = dtc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (dns_linear_ok(b, in, out))
     return dns_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out))
@@ -122,6 +130,10 @@ bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask
                               void* stream) {
   BPX_CHECK_ARG(dy && w && dx && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (dtc_linear_ok(b, in, out)) {
+    bpx_status_t s = dtc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (dns_linear_ok(b, in, out))
     return dns_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out))

@@ -78,3 +78,15 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, 
                             int n, int h, int w_, int cin, int cout, void* ws,
                             size_t ws_bytes, cudaStream_t st);
 }  // namespace bpx
+
+// TMA-fed tcgen05 dense fwd / dgrad for batches <= 32 (tc_dense.cu).
+namespace bpx {
+bool dtc_linear_ok(int b, int in, int out);
+size_t dtc_linear_ws(int b, int in, int out);
+bpx_status_t dtc_linear_fwd(const float* x, const float* w, const float* bias, float* y, int b,
+                            int in, int out, int relu, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
+bpx_status_t dtc_linear_dgrad(const float* dy, const float* w, const float* mask, float* dx,
+                              int b, int in, int out, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
+}  // namespace bpx
