@@ -38,6 +38,9 @@ CONV_SHAPES = [
     (2, 16, 3, 64), (2, 16, 64, 64), (2, 12, 64, 128), (1, 10, 128, 128),
     (2, 8, 128, 256), (3, 7, 256, 256), (2, 6, 256, 512), (2, 4, 512, 512),
     (1, 14, 512, 512), (5, 9, 64, 64),
+    # full-size images: 2-D output tiles with 4-D TMA halos (32x4 at 224,
+    # 16x8 at 112) and the 64-channel stages of 64-wide N tiles
+    (1, 224, 64, 64), (1, 112, 64, 128),
 ]
 
 
@@ -126,7 +129,8 @@ def test_conv_matches_ffma_engine():
 
 @pytest.mark.parametrize("b,fin,fout,relu", [(4, 25088, 4096, True), (32, 4096, 4096, True),
                                              (32, 4096, 1000, False), (3, 64, 40, True),
-                                             (1, 128, 1000, False)], ids=str)
+                                             (1, 128, 1000, False), (17, 256, 384, True),
+                                             (2, 512, 128, False)], ids=str)
 def test_linear_fwd_bwd(b, fin, fout, relu):
     x = relu_input(b, fin, seed=15)
     w = rnd(fout, fin, seed=16, scale=0.01)
