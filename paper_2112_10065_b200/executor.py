@@ -163,16 +163,24 @@ class BurstStep:
         L = self.layers[-1]
         return L.s0, L.s0 + L.b
 
-    def load(self, x_global: torch.Tensor, labels_global: torch.Tensor) -> None:
-        """Copy this rank's shards (x: NHWC [B,...], labels [B]) to the
-        device; async when the sources are pinned host tensors."""
+    def input_pairs(self, x_global: torch.Tensor, labels_global: torch.Tensor) -> list:
+        """[(device destination, host source)] of this rank's input shards
+        (x: NHWC [B,...], labels [B])."""
+        pairs = []
         a, b = self.input_range()
         if self.layers[0].active and b > a:
             x0 = self.layers[0].x
-            x0.copy_(x_global[a:b].reshape(x0.shape), non_blocking=True)
+            pairs.append((x0, x_global[a:b].reshape(x0.shape)))
         a, b = self.label_range()
         if self.layers[-1].active and b > a:
-            self.labels[:b - a].copy_(labels_global[a:b], non_blocking=True)
+            pairs.append((self.labels[:b - a], labels_global[a:b]))
+        return pairs
+
+    def load(self, x_global: torch.Tensor, labels_global: torch.Tensor) -> None:
+        """Copy this rank's shards to the device; async when the sources
+        are pinned host tensors."""
+        for dst, src in self.input_pairs(x_global, labels_global):
+            dst.copy_(src, non_blocking=True)
 
     # ------------------------------------------------------------ step
     def _fwd(self, i: int) -> None:

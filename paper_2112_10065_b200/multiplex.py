@@ -132,6 +132,30 @@ class Multiplexer:
         qi = 0
         ends = []
         op_acc: dict[str, list] = {}
+        # Inputs arrive end to end every iteration, pipelined: the H2D copy of
+        # iteration it+1 runs on a copy stream into a staging buffer while
+        # iteration it computes; the step then takes it with one D2D copy.
+        # Each iteration's loss is read back to pinned host memory.
+        pairs = fg.input_pairs(*inputs) if inputs is not None else []
+        staging = [torch.empty_like(d) for d, _ in pairs]
+        copy_stream = torch.cuda.Stream()
+        h2d_done: dict[int, torch.cuda.Event] = {}
+        d2d_done: dict[int, torch.cuda.Event] = {}
+        loss_host = torch.empty(2, dtype=torch.float32).pin_memory()
+
+        def prefetch(it):
+            if not pairs or it >= iterations:
+                return
+            with torch.cuda.stream(copy_stream):
+                if it - 1 in d2d_done:
+                    copy_stream.wait_event(d2d_done[it - 1])
+                for buf, (_, src) in zip(staging, pairs):
+                    buf.copy_(src, non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(copy_stream)
+                h2d_done[it] = e
+
+        prefetch(0)
 
         def retire_bg():
             nonlocal bg_iter
@@ -163,14 +187,22 @@ class Multiplexer:
                 it, j = seg_queue[qi]
                 if fg_pending and fg_pending[0][1] < it - (0 if self.measure else 1):
                     break
-                if inputs is not None and j == 0:
+                if pairs and j == 0:
                     with torch.cuda.stream(self.fg_stream):
-                        fg.load(*inputs)
+                        self.fg_stream.wait_event(h2d_done[it])
+                        for (dst, _), buf in zip(pairs, staging):
+                            dst.copy_(buf, non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(self.fg_stream)
+                        d2d_done[it] = e
+                    prefetch(it + 1)
                 with torch.cuda.stream(self.fg_stream):
                     if self.flagged[j]:
                         for e, _ in outstanding:         # let queued bg drain first
                             self.fg_stream.wait_event(e)
                     self.segments[j][2].replay()
+                    if j == len(self.segments) - 1:     # the step's result to the host
+                        loss_host[it % 2].copy_(fg.loss_buf[0], non_blocking=True)
                     e = torch.cuda.Event(enable_timing=True)
                     e.record(self.fg_stream)
                 if self.flagged[j]:
