@@ -43,6 +43,9 @@
 namespace bpx {
 namespace fdt {
 using namespace tcx;
+#ifdef FDT_PROF
+void* fdt_prof_ptr = nullptr;
+#endif
 
 constexpr int NTHREADS = 14 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
@@ -73,6 +76,7 @@ struct Geo {
   int halo_tx;               // bytes TMA delivers per halo slot
   int ksplit, units;         // K halves per tile (1 or 2) and work units = tiles * ksplit
   float* part;               // ksplit > 1: raw partial sums [ksplit][npix][N]
+  void* prof;                // FDT_PROF builds: MMA-issuer cycle counters
 };
 
 struct EBiasAct {
@@ -226,45 +230,71 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       // M=128, N=BN, tf32 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
       constexpr uint32_t idesc = make_idesc(BN) | (DG ? (1u << 16) : 0u);
       int i = 0, c = 0;
+#ifdef FDT_PROF
+      long long t_acc = 0, t_a = 0, t_issue = 0, t0 = clock64();
+#endif
       for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++i) {
           const int s = i % S;
           const uint32_t ph = (i / S) & 1;
           const int b = c & 1;
           if (kb % PCH == 0 && c >= 2) {
+#ifdef FDT_PROF
+            long long q0 = clock64();
+#endif
             mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
             tc_fence_after();
+#ifdef FDT_PROF
+            t_acc += clock64() - q0;
+#endif
           }
+#ifdef FDT_PROF
+          long long q1 = clock64();
+#endif
+          // aready[s] also covers the stage's B tiles: the converters wait for
+          // them before arriving, so the issuer makes one barrier check per
+          // stage (its checks come straight out of MMA issue time: the tensor
+          // pipe's queue is only a few instructions deep)
           mbar_wait(&aready[s], ph);
-          mbar_wait(&bfull[s], ph);
           tc_fence_after();
+#ifdef FDT_PROF
+          long long q3 = clock64();
+          t_a += q3 - q1;
+#endif
           const uint32_t d = tmem + b * BN;
           const uint32_t ah = tmem + Cf::A_COL + s * 2 * KS, al = ah + KS;
           const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
-          const uint32_t bl = bh + Cf::B_BYTES;
+          const uint64_t dbh0 = DG ? make_desc_mn32(bh, KS * 128, 512) : make_desc_sw128(bh, 16, 1024);
+          const uint64_t dbl0 = dbh0 + (Cf::B_BYTES >> 4);
 #pragma unroll
           for (int ks = 0; ks < KS / 8; ++ks) {
-            uint64_t dbh, dbl;
-            if (DG) {
-              dbh = make_desc_mn32(bh + ks * 1024, KS * 128, 512);
-              dbl = make_desc_mn32(bl + ks * 1024, KS * 128, 512);
-            } else {
-              const uint32_t off = (ks >> 2) * BN * 128 + (ks & 3) * 32;
-              dbh = make_desc_sw128(bh + off, 16, 1024);
-              dbl = make_desc_sw128(bl + off, 16, 1024);
-            }
+            // descriptor start address is (addr >> 4) in bits [0,14)
+            const uint32_t off = DG ? ks * 1024 : (ks >> 2) * BN * 128 + (ks & 3) * 32;
+            const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
             const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
             mma_ts(d, al + 8 * ks, dbh, idesc, acc);
             mma_ts(d, ah + 8 * ks, dbl, idesc, 1u);
             mma_ts(d, ah + 8 * ks, dbh, idesc, 1u);
           }
           tc_commit(&empty[s]);
+#ifdef FDT_PROF
+          t_issue += clock64() - q3;
+#endif
           if (kb % PCH == PCH - 1 || kb == nk - 1) {
             tc_commit(&accfull[b]);
             ++c;
           }
         }
       }
+#ifdef FDT_PROF
+      unsigned long long* pst = reinterpret_cast<unsigned long long*>(g.prof);
+      atomicAdd(pst + 0, (unsigned long long)(clock64() - t0));
+      atomicAdd(pst + 1, (unsigned long long)t_acc);
+      atomicAdd(pst + 2, (unsigned long long)t_a);
+      atomicAdd(pst + 3, 0ull);
+      atomicAdd(pst + 4, (unsigned long long)t_issue);
+      atomicAdd(pst + 5, (unsigned long long)i);
+#endif
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ A converters
@@ -325,8 +355,11 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
+          if (lane == 0) {
+            mbar_wait(&bfull[s], (i / S) & 1);     // aready[s] implies the B tiles
+            mbar_arrive(&aready[s]);
+          }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&aready[s]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&hempty[hs]);
@@ -472,6 +505,15 @@ bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n,
   g.ksplit = ksplit_for(g.tiles, g.C / KS);
   g.units = g.tiles * g.ksplit;
   g.part = part;
+#ifdef FDT_PROF
+  static void* prof = nullptr;
+  if (!prof) cudaMalloc(&prof, 64);
+  cudaMemsetAsync(prof, 0, 64, st);
+  g.prof = prof;
+  fdt_prof_ptr = prof;
+#else
+  g.prof = nullptr;
+#endif
   if (g.tw) {
     g.nhbox = 1;
     g.hbox = cdiv((g.tw + 2) * (g.th + 2), 8) * 8;
@@ -603,3 +645,13 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, 
 }
 
 }  // namespace bpx
+
+#ifdef FDT_PROF
+// Profiling builds only (BPX_NVCC_EXTRA=-DFDT_PROF): MMA-issuer cycles of the
+// last fdt launch -- {total, wait accfree, wait aready, 0, issue, stages}
+// summed over CTAs (tools/fdt_prof.py).
+extern "C" __attribute__((visibility("default"))) void bpx_fdt_prof(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  if (bpx::fdt::fdt_prof_ptr) cudaMemcpy(out, bpx::fdt::fdt_prof_ptr, 48, cudaMemcpyDeviceToHost);
+}
+#endif
