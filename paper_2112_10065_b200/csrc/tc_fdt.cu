@@ -226,7 +226,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     }
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (the whole warp runs the loop; elect.sync picks the issuing lane)
+    {
       // M=128, N=BN, tf32 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
       constexpr uint32_t idesc = make_idesc(BN) | (DG ? (1u << 16) : 0u);
       int i = 0, c = 0;
@@ -272,28 +273,30 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             const uint32_t off = DG ? ks * 1024 : (ks >> 2) * BN * 128 + (ks & 3) * 32;
             const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
             const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
-            mma_ts(d, al + 8 * ks, dbh, idesc, acc);
-            mma_ts(d, ah + 8 * ks, dbl, idesc, 1u);
-            mma_ts(d, ah + 8 * ks, dbh, idesc, 1u);
+            mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
+            mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+            mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
           }
-          tc_commit(&empty[s]);
+          tc_commit_elect(&empty[s]);
 #ifdef FDT_PROF
           t_issue += clock64() - q3;
 #endif
           if (kb % PCH == PCH - 1 || kb == nk - 1) {
-            tc_commit(&accfull[b]);
+            tc_commit_elect(&accfull[b]);
             ++c;
           }
         }
       }
 #ifdef FDT_PROF
       unsigned long long* pst = reinterpret_cast<unsigned long long*>(g.prof);
+      if (lane == 0) {
       atomicAdd(pst + 0, (unsigned long long)(clock64() - t0));
       atomicAdd(pst + 1, (unsigned long long)t_acc);
       atomicAdd(pst + 2, (unsigned long long)t_a);
       atomicAdd(pst + 3, 0ull);
       atomicAdd(pst + 4, (unsigned long long)t_issue);
       atomicAdd(pst + 5, (unsigned long long)i);
+      }
 #endif
     }
   } else if (warp < DR0) {

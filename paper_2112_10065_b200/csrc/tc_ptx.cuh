@@ -54,6 +54,27 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b_desc, 
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d), "r"(a), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// Warp-converged issue: the whole warp runs the issuer loop and one lane,
+// picked by elect.sync inside the same asm block, issues.  Issuing from a
+// `lane == 0` branch instead makes the compiler wrap every tcgen05
+// instruction in a uniform-datapath waterfall loop (~70 cycles per MMA
+// measured, more than a 128x64x8 MMA takes to execute).
+__device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d), "r"(a), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
