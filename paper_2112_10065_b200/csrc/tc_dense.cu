@@ -106,7 +106,7 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       }
     }
   } else if (warp == MMA_WARP) {
-    if (lane == 0) {
+    {                                   // whole warp; elect.sync issues
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
                                  ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       for (int i = 0; i < nst; ++i) {
@@ -129,12 +129,12 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           const uint64_t dbh = make_desc_sw128(bh + ks * 32, 16, 1024);
           const uint64_t dbl = make_desc_sw128(bl + ks * 32, 16, 1024);
           const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
-          mma_ts(d, al + 8 * ks, dbh, idesc, acc);
-          mma_ts(d, ah + 8 * ks, dbl, idesc, 1u);
-          mma_ts(d, ah + 8 * ks, dbh, idesc, 1u);
+          mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
         }
-        tc_commit(&empty[s]);
-        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit(&hfull[b]);
+        tc_commit_elect(&empty[s]);
+        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
       }
     }
   } else if (warp < DR0) {
