@@ -47,8 +47,10 @@ using namespace tcx;
 void* fdt_prof_ptr = nullptr;
 #endif
 
-constexpr int NTHREADS = 14 * 32;
-constexpr int TMA_WARP = 0, MMA_WARP = 1, DR0 = 6;   // warps 2-5: A converters
+constexpr int TMA_WARP = 0, MMA_WARP = 1, CV0 = 2;   // A converters from warp 2
+#ifndef FDT_NCONV
+#define FDT_NCONV 8
+#endif
 
 // BN output channels per tile, KS channels per stage, NS stages.
 template <int BN, int KS, int NS>
@@ -57,6 +59,12 @@ struct Cfg {
   static constexpr int S = NS;
   static constexpr int NCH = KS / 32;                     // 32-channel halves per stage
   static constexpr int PCH = 128 / KS;                    // stages per promotion chunk (K = 128)
+  // A converter warps (two per TMEM lane quadrant split the channels) and
+  // drain warps (64 accumulator columns per thread)
+  static constexpr int NCONV = FDT_NCONV;
+  static constexpr int NDRAIN = BN / 16;
+  static constexpr int DR0 = CV0 + NCONV;
+  static constexpr int NTHREADS = 32 * (2 + NCONV + NDRAIN);
   static constexpr int B_BYTES = BN * KS * 4;
   static constexpr int STAGE = 2 * B_BYTES;               // B raw | B lo
   static constexpr int A_COL = 2 * BN;                    // accumulators: 2 x BN columns
@@ -133,11 +141,12 @@ __device__ __forceinline__ Tile tile_of(const Geo& g, int mi) {
 }
 
 template <int BN, int KS, int NS, bool DG, class EPI>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<BN, KS, NS>::NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
   using Cf = Cfg<BN, KS, NS>;
   constexpr int S = Cf::S, NCH = Cf::NCH, PCH = Cf::PCH;
+  constexpr int NCONV = Cf::NCONV, NDRAIN = Cf::NDRAIN, DR0 = Cf::DR0;
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   char* halo = smem + S * Cf::STAGE;                          // 2 slots
@@ -157,14 +166,14 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&bfull[s], 1);
-      mbar_init(&aready[s], 4);          // one arrival per converter warp
+      mbar_init(&aready[s], NCONV);      // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
-      mbar_init(&hempty[b], 4);
+      mbar_init(&hempty[b], NCONV);
       mbar_init(&accfull[b], 1);
-      mbar_init(&accfree[b], 8);         // one arrival per drain warp
+      mbar_init(&accfree[b], NDRAIN);    // one arrival per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -339,22 +348,25 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           tc_fence_after();
           const uint32_t a = lanebase + s * 2 * KS;
 #pragma unroll
-          for (int c2 = 0; c2 < NCH; ++c2) {
-            const char* row = hbase + c2 * g.half_bytes + hr * 128;
-            float hi[32], lo[32];
+          // this warp's 16-channel units: part, part + NCONV/4, ...
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+          for (int k = 0; k < KS / 16 / (NCONV / 4); ++k) {
+            const int u16 = ((warp - CV0) >> 2) + k * (NCONV / 4);
+            const int c2 = u16 >> 1, j0 = (u16 & 1) * 4;
+            const char* row = hbase + c2 * g.half_bytes + hr * 128;
+            float hi[16], lo[16];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = j0 + jj;
               float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
               if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
-              split(v.x, hi[4 * j + 0], lo[4 * j + 0]);
-              split(v.y, hi[4 * j + 1], lo[4 * j + 1]);
-              split(v.z, hi[4 * j + 2], lo[4 * j + 2]);
-              split(v.w, hi[4 * j + 3], lo[4 * j + 3]);
+              split(v.x, hi[4 * jj + 0], lo[4 * jj + 0]);
+              split(v.y, hi[4 * jj + 1], lo[4 * jj + 1]);
+              split(v.z, hi[4 * jj + 2], lo[4 * jj + 2]);
+              split(v.w, hi[4 * jj + 3], lo[4 * jj + 3]);
             }
-            tmem_st16(a + 32 * c2, *reinterpret_cast<float(*)[16]>(hi));
-            tmem_st16(a + 32 * c2 + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
-            tmem_st16(a + KS + 32 * c2, *reinterpret_cast<float(*)[16]>(lo));
-            tmem_st16(a + KS + 32 * c2 + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+            tmem_st16(a + 16 * u16, hi);
+            tmem_st16(a + KS + 16 * u16, lo);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
@@ -371,7 +383,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   } else {
     // ------------------------------------------------------------ drain + epilogue
     const int q = warp & 3, hf = (warp - DR0) >> 2;
-    constexpr int CW = BN / 2;
+    constexpr int CW = BN * 4 / NDRAIN;                 // 64 columns per drain thread
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + hf * CW;
     const int nch = (nk + PCH - 1) / PCH;
     const int r = q * 32 + lane;
@@ -574,7 +586,7 @@ bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n,
     attr = true;
   }
   const int grid = g.units < num_sms() ? g.units : num_sms();
-  kern<<<grid, NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
+  kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
   if (g.ksplit == 1) return launch_status(2);
   const long long groups = (long long)g.npix * (g.N / 8);
   int fg = (int)cdivll(groups, 256);
