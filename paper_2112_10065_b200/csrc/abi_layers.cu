@@ -21,6 +21,10 @@ bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, 
   BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
   cudaStream_t st = as_stream(stream);
+  if (c1_conv_fwd_ok(cin, cout)) {
+    bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (small_conv_fwd_ok(cin, cout))
     return small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(x)) {

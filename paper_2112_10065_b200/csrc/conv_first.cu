@@ -1,0 +1,191 @@
+// Forward of the first conv (Cin = 3, Cout = 64) on tcgen05: K = 27 taps x
+// channels, padded to 32, is ONE MMA stage, so the layer is a stream of
+// 128-pixel tiles bounded by writing y (411 MB at B = 32):
+//
+//   y[p][co] = relu(b[co] + sum_{r<27} col[p][r] * w[co][r])
+//
+// Persistent CTAs, two TMEM buffers (A hi|lo 64 columns + D 64 columns each)
+// so tile t+1 is gathered and multiplied while tile t drains:
+//   * gather warps (thread = pixel = TMEM lane) load the 27 im2col values
+//     straight from x (19 MB, L2-resident), split them into TF32 hi/lo and
+//     tcgen05.st them;
+//   * one warp issues the 3xTF32 MMAs (B = the 64 x 32 weight tile, hi and
+//     lo, built once per CTA in shared memory, K-major 128-B swizzle);
+//   * drain warps add the bias, apply the ReLU and store 256-byte rows.
+// One 32-K MMA chain per tile needs no chunk promotion.
+#include "tc_ptx.cuh"
+#include "simt_api.h"
+
+namespace bpx {
+namespace c1 {
+using namespace tcx;
+
+constexpr int COUT = 64, R = 27, KP = 32;
+constexpr int NTHREADS = 9 * 32;       // warp 0 MMA, 1-4 gather, 5-8 drain
+constexpr int SMEM = 1024 + 2 * COUT * KP * 4 + 128;
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
+              const float* __restrict__ bias, float* __restrict__ y, int H, int W,
+              long long npix, int relu) {
+  extern __shared__ char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* bh = smem;                        // 64 rows x 128 B, 128-B swizzle
+  char* bl = smem + COUT * KP * 4;
+  uint64_t* aready = reinterpret_cast<uint64_t*>(bl + COUT * KP * 4);
+  uint64_t* dfull = aready + 2;
+  uint64_t* tfree = dfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long tiles = (npix + 127) / 128;
+
+  // weights, K-major with the 128-B swizzle: row co, 16-B granule j at j ^ (co & 7)
+  for (int e = tid; e < COUT * KP; e += NTHREADS) {
+    const int co = e / KP, k = e % KP;
+    const float v = k < R ? __ldg(w + co * R + k) : 0.f;
+    float h, l;
+    split(v, h, l);
+    const int off = co * 128 + (((k >> 2) ^ (co & 7)) << 4) + (k & 3) * 4;
+    *reinterpret_cast<float*>(bh + off) = v;
+    *reinterpret_cast<float*>(bl + off) = l;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&aready[b], 4);
+      mbar_init(&dfull[b], 1);
+      mbar_init(&tfree[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;       // buffer b: A at 128*b, D at 128*b + 64
+
+  if (warp == 0) {
+    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                               ((uint32_t)(COUT >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t dbh0 = make_desc_sw128(smem_u32(bh), 16, 1024);
+    const uint64_t dbl0 = make_desc_sw128(smem_u32(bl), 16, 1024);
+    int it = 0;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      mbar_wait(&aready[b], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ah = tmem + 128 * b, al = ah + KP, d = ah + 64;
+#pragma unroll
+      for (int ks = 0; ks < KP / 8; ++ks) {
+        const uint64_t dbh = dbh0 + ks * 2, dbl = dbl0 + ks * 2;     // +32 B
+        mma_ts_elect(d, al + 8 * ks, dbh, idesc, ks > 0 ? 1u : 0u);
+        mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+        mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+      }
+      tc_commit_elect(&dfull[b]);
+    }
+  } else if (warp < 5) {
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16);
+    const int hw = H * W;
+    int it = 0;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      const long long p = t * 128 + r;
+      float v[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) v[k] = 0.f;
+      if (p < npix) {
+        const int img = (int)(p / hw), rem = (int)(p - (long long)img * hw);
+        const int oh = rem / W, ow = rem - oh * W;
+        const float* xi = x + (long long)img * hw * 3;
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) {
+          const int ih = oh + tap / 3 - 1, iw = ow + tap % 3 - 1;
+          if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W) {
+            const float* s = xi + ((long long)ih * W + iw) * 3;
+            v[3 * tap] = __ldg(s);
+            v[3 * tap + 1] = __ldg(s + 1);
+            v[3 * tap + 2] = __ldg(s + 2);
+          }
+        }
+      }
+      float hi[KP], lo[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) split(v[k], hi[k], lo[k]);
+      if (it >= 2) mbar_wait(&tfree[b], ((it >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t a = lanebase + 128 * b;
+      tmem_st16(a, *reinterpret_cast<float(*)[16]>(hi));
+      tmem_st16(a + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
+      tmem_st16(a + KP, *reinterpret_cast<float(*)[16]>(lo));
+      tmem_st16(a + KP + 16, *reinterpret_cast<float(*)[16]>(lo + 16));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aready[b]);
+    }
+  } else {
+    const int q = warp & 3, r = q * 32 + lane;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16);
+    float bv[COUT];
+#pragma unroll
+    for (int j = 0; j < COUT; ++j) bv[j] = bias ? __ldg(bias + j) : 0.f;
+    int it = 0;
+    for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      mbar_wait(&dfull[b], (it >> 1) & 1);
+      tc_fence_after();
+      const long long p = t * 128 + r;
+      float* dst = y + p * COUT;
+#pragma unroll
+      for (int j = 0; j < COUT; j += 8) {
+        uint32_t rr[8];
+        tmem_ld8(lanebase + 128 * b + 64 + j, rr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float s = __uint_as_float(rr[u]) + bv[j + u];
+          o[u] = relu ? fmaxf(s, 0.f) : s;
+        }
+        if (p < npix) {
+          *reinterpret_cast<float4*>(dst + j) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4*>(dst + j + 4) = make_float4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfree[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free(tmem, 256);
+  }
+}
+
+}  // namespace c1
+
+bool c1_conv_fwd_ok(int cin, int cout) { return cin == 3 && cout == c1::COUT; }
+
+bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
+                         int h, int w_, int relu, cudaStream_t st) {
+  const long long npix = (long long)n * h * w_;
+  if (npix == 0) return launch_status(0);
+  if (!aligned16(y)) return BPX_ERR_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(c1::c1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         c1::SMEM);
+    attr = true;
+  }
+  const long long tiles = (npix + 127) / 128;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, y, h, w_, npix, relu);
+  return launch_status();
+}
+
+}  // namespace bpx

@@ -52,3 +52,10 @@ bpx_status_t dns_linear_dgrad(const float* dy, const float* w, const float* mask
 bpx_status_t dns_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias, int b,
                               int in, int out, void* ws, size_t ws_bytes, cudaStream_t st);
 }  // namespace bpx
+
+// tcgen05 forward of the first conv (Cin = 3, Cout = 64; conv_first.cu).
+namespace bpx {
+bool c1_conv_fwd_ok(int cin, int cout);
+bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
+                         int h, int w_, int relu, cudaStream_t st);
+}  // namespace bpx
