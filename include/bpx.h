@@ -104,6 +104,13 @@ BPX_API bpx_status_t bpx_maxpool2x2_fwd(const float* x, float* y, int n, int h, 
                                 int c, void* stream);
 BPX_API bpx_status_t bpx_maxpool2x2_bwd(const float* x, const float* dy, float* dx,
                                 int n, int h, int w_, int c, void* stream);
+/* Same pool, keeping each window's first-max position (idx: one byte per
+ * output element, values 0..3 in (row, col) order) for a backward that
+ * reads idx + dy instead of x + dy.                                        */
+BPX_API bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* idx, int n,
+                                    int h, int w_, int c, void* stream);
+BPX_API bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* dx,
+                                    int n, int h, int w_, int c, void* stream);
 
 /* Mean softmax cross-entropy over the GLOBAL batch: loss_out[0] =
  * sum_{local rows} CE / b_global (fixed order); loss_out must hold

@@ -207,6 +207,66 @@ __global__ void maxpool_bwd_kernel(const float4* __restrict__ x, const float4* _
   }
 }
 
+// Index variants: the forward also stores each window's first-max position
+// (one byte per output channel, PyTorch's tie order), so the backward reads
+// 1 byte per output instead of re-reading the 4x larger input.
+__device__ __forceinline__ unsigned char argmax4(float a, float b, float c, float d, float& m) {
+  unsigned char k = 0; m = a;
+  if (b > m) { m = b; k = 1; }
+  if (c > m) { m = c; k = 2; }
+  if (d > m) { m = d; k = 3; }
+  return k;
+}
+
+__global__ void maxpool_fwd_idx_kernel(const float4* __restrict__ x, float4* __restrict__ y,
+                                       uchar4* __restrict__ idx, int n, int h, int w, int c4) {
+  const int oh = h / 2, ow = w / 2;
+  const long long total = (long long)n * oh * ow * c4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i % c4); long long p = i / c4;
+    int xo = (int)(p % ow); p /= ow;
+    int yo = (int)(p % oh); int b = (int)(p / oh);
+    const float4* base = x + (((long long)b * h + 2 * yo) * w + 2 * xo) * c4 + c;
+    const long long rs = (long long)w * c4;
+    const float4 a = base[0], bb = base[c4], cc = base[rs], d = base[rs + c4];
+    float4 r;
+    uchar4 k;
+    k.x = argmax4(a.x, bb.x, cc.x, d.x, r.x);
+    k.y = argmax4(a.y, bb.y, cc.y, d.y, r.y);
+    k.z = argmax4(a.z, bb.z, cc.z, d.z, r.z);
+    k.w = argmax4(a.w, bb.w, cc.w, d.w, r.w);
+    y[i] = r;
+    idx[i] = k;
+  }
+}
+
+__global__ void maxpool_bwd_idx_kernel(const uchar4* __restrict__ idx,
+                                       const float4* __restrict__ dy, float4* __restrict__ dx,
+                                       int n, int h, int w, int c4) {
+  const int oh = h / 2, ow = w / 2;
+  const long long total = (long long)n * oh * ow * c4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i % c4); long long p = i / c4;
+    int xo = (int)(p % ow); p /= ow;
+    int yo = (int)(p % oh); int b = (int)(p / oh);
+    const long long o = (((long long)b * h + 2 * yo) * w + 2 * xo) * c4 + c;
+    const long long rs = (long long)w * c4;
+    const uchar4 k = idx[i];
+    const float4 g = dy[i];
+    float4 r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      r[j].x = k.x == j ? g.x : 0.f;
+      r[j].y = k.y == j ? g.y : 0.f;
+      r[j].z = k.z == j ? g.z : 0.f;
+      r[j].w = k.w == j ? g.w : 0.f;
+    }
+    dx[o] = r[0]; dx[o + c4] = r[1]; dx[o + rs] = r[2]; dx[o + rs + c4] = r[3];
+  }
+}
+
 static int ew_grid(long long work) {
   long long g = cdivll(work, 256);
   long long cap = 8LL * num_sms();
@@ -337,6 +397,30 @@ bpx_status_t bpx_maxpool2x2_bwd(const float* x, const float* dy, float* dx, int 
   if (total == 0) return BPX_OK;
   maxpool_bwd_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
+      reinterpret_cast<float4*>(dx), n, h, w_, c / 4);
+  return launch_status();
+}
+
+bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* idx, int n, int h,
+                                    int w_, int c, void* stream) {
+  BPX_CHECK_ARG(x && y && idx && n >= 0 && h % 2 == 0 && w_ % 2 == 0 && c % 4 == 0);
+  BPX_CHECK_ARG(aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
+  long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
+  if (total == 0) return BPX_OK;
+  maxpool_fwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+      reinterpret_cast<uchar4*>(idx), n, h, w_, c / 4);
+  return launch_status();
+}
+
+bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* dx, int n,
+                                    int h, int w_, int c, void* stream) {
+  BPX_CHECK_ARG(idx && dy && dx && n >= 0 && h % 2 == 0 && w_ % 2 == 0 && c % 4 == 0);
+  BPX_CHECK_ARG(aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
+  long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
+  if (total == 0) return BPX_OK;
+  maxpool_bwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uchar4*>(idx), reinterpret_cast<const float4*>(dy),
       reinterpret_cast<float4*>(dx), n, h, w_, c / 4);
   return launch_status();
 }

@@ -55,6 +55,7 @@ class _Layer:
     bias: Optional[torch.Tensor] = None
     dw: Optional[torch.Tensor] = None
     dbias: Optional[torch.Tensor] = None
+    idx: Optional[torch.Tensor] = None     # pool: first-max position per output
     reshard_in: bool = False               # input arrives through a reshard
 
 
@@ -117,6 +118,8 @@ class BurstStep:
             else:
                 L.x = prev.y.view(sp.in_shape(L.b))
             L.y = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+            if sp.kind == "pool" and hasattr(self.k, "maxpool2x2_fwd_idx"):
+                L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
             L.dy = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
             if i > 0:
                 if L.reshard_in:
@@ -189,7 +192,10 @@ class BurstStep:
         if sp.kind == "conv":
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
         elif sp.kind == "pool":
-            self.k.maxpool2x2_fwd(L.x, L.y)
+            if L.idx is not None:
+                self.k.maxpool2x2_fwd_idx(L.x, L.y, L.idx)
+            else:
+                self.k.maxpool2x2_fwd(L.x, L.y)
         else:
             self.k.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
 
@@ -202,7 +208,10 @@ class BurstStep:
             if i > 0:
                 self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
         elif sp.kind == "pool":
-            self.k.maxpool2x2_bwd(L.x, L.dy, L.dx)
+            if L.idx is not None:
+                self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx)
+            else:
+                self.k.maxpool2x2_bwd(L.x, L.dy, L.dx)
         else:
             x2 = L.x.view(L.b, sp.cin)
             self.k.linear_wgrad(x2, L.dy, L.dw, L.dbias, ws=self.ws)

@@ -50,6 +50,10 @@ _SIGS = {
                            + [ctypes.c_void_p]),
     "bpx_maxpool2x2_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
                            + [ctypes.c_void_p]),
+    "bpx_maxpool2x2_fwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
+                               + [ctypes.c_void_p]),
+    "bpx_maxpool2x2_bwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
+                               + [ctypes.c_void_p]),
     "bpx_softmax_xent": (ctypes.c_int, [_c_float_p, ctypes.c_void_p]
                          + [ctypes.c_int] * 3 + [_c_float_p, _c_float_p, ctypes.c_void_p]),
     "bpx_sgd_update": (ctypes.c_int, [_c_float_p, _c_float_p, ctypes.c_size_t,
@@ -256,6 +260,26 @@ def maxpool2x2_bwd(x, dy, dx):
     n, h, w, c = x.shape
     _check(lib.bpx_maxpool2x2_bwd(_ptr(x), _ptr(dy), _ptr(dx), n, h, w, c,
                                   _stream()), "bpx_maxpool2x2_bwd")
+    return dx
+
+
+def maxpool2x2_fwd_idx(x, y, idx):
+    """Pool forward that also records each window's first-max position
+    (``idx``: uint8, same shape as ``y``)."""
+    lib = load_library()
+    _f32(x, y)
+    n, h, w, c = x.shape
+    _check(lib.bpx_maxpool2x2_fwd_idx(_ptr(x), _ptr(y), _ptr(idx), n, h, w, c, _stream()),
+           "bpx_maxpool2x2_fwd_idx")
+    return y
+
+
+def maxpool2x2_bwd_idx(idx, dy, dx):
+    lib = load_library()
+    _f32(dy, dx)
+    n, h, w, c = dx.shape
+    _check(lib.bpx_maxpool2x2_bwd_idx(_ptr(idx), _ptr(dy), _ptr(dx), n, h, w, c, _stream()),
+           "bpx_maxpool2x2_bwd_idx")
     return dx
 
 

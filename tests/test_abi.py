@@ -30,7 +30,8 @@ def test_header_declares_the_surface():
     names = declared()
     for must in ("bpx_conv3x3_fwd", "bpx_conv3x3_dgrad", "bpx_conv3x3_wgrad",
                  "bpx_linear_fwd", "bpx_linear_dgrad", "bpx_linear_wgrad",
-                 "bpx_maxpool2x2_fwd", "bpx_maxpool2x2_bwd", "bpx_softmax_xent",
+                 "bpx_maxpool2x2_fwd", "bpx_maxpool2x2_bwd", "bpx_maxpool2x2_fwd_idx",
+                 "bpx_maxpool2x2_bwd_idx", "bpx_softmax_xent",
                  "bpx_sgd_update", "bpx_reshard_pull", "bpx_allreduce_sum_prefix",
                  "bpx_signal_barrier", "bpx_status_string"):
         assert must in names

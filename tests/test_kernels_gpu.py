@@ -171,9 +171,16 @@ def test_maxpool_fwd_bwd_exact(n, h, c):
     dx = torch.empty(n, h, h, c, device=DEV)
     ops.maxpool2x2_fwd(x.to(DEV), y)
     ops.maxpool2x2_bwd(x.to(DEV), dy.to(DEV), dx)
+    # index variants: first-max positions recorded by the forward
+    y2 = torch.empty_like(y)
+    dx2 = torch.empty_like(dx)
+    idx = torch.empty(y.shape, dtype=torch.uint8, device=DEV)
+    ops.maxpool2x2_fwd_idx(x.to(DEV), y2, idx)
+    ops.maxpool2x2_bwd_idx(idx, dy.to(DEV), dx2)
     torch.cuda.synchronize()
     assert torch.equal(y.cpu(), yr.detach().permute(0, 2, 3, 1).float())
     assert torch.equal(dx.cpu(), xr.grad.permute(0, 2, 3, 1).float())
+    assert torch.equal(y2, y) and torch.equal(dx2, dx)
 
 
 @pytest.mark.parametrize("b,bg", [(32, 32), (4, 32), (1, 8)])
