@@ -29,7 +29,8 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
               const float* __restrict__ bias, float* __restrict__ y, int H, int W,
               long long npix, int relu) {
   extern __shared__ char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
+  char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   char* bh = smem;                        // 64 rows x 128 B, 128-B swizzle
   char* bl = smem + COUT * KP * 4;
   uint64_t* aready = reinterpret_cast<uint64_t*>(bl + COUT * KP * 4);

@@ -54,7 +54,8 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
            const __grid_constant__ CUtensorMap tbl, Geo g) {
   using Cf = Cfg<NB>;
   extern __shared__ char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
+  char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cf::STAGE);
   uint64_t* aready = full + S;
   uint64_t* empty = aready + S;

@@ -148,7 +148,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   constexpr int S = Cf::S, NCH = Cf::NCH, PCH = Cf::PCH;
   constexpr int NCONV = Cf::NCONV, NDRAIN = Cf::NDRAIN, DR0 = Cf::DR0;
   extern __shared__ char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
+  char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   char* halo = smem + S * Cf::STAGE;                          // 2 slots
   uint64_t* bfull = reinterpret_cast<uint64_t*>(halo + 2 * g.halo_bytes);
   uint64_t* aready = bfull + S;

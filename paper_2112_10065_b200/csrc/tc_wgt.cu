@@ -77,7 +77,8 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   using Cf = Cfg<BN>;
   constexpr int BK = Cf::BK, BOX = Cf::BOX, PCH = Cf::PCH;
   extern __shared__ char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
+  char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
   uint64_t* aready = full + Cf::S;
   uint64_t* bready = aready + Cf::S;
