@@ -80,9 +80,8 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
-  uint64_t* aready = full + Cf::S;
-  uint64_t* bready = aready + Cf::S;
-  uint64_t* empty = bready + Cf::S;
+  uint64_t* ready = full + Cf::S;            // A and B converters done
+  uint64_t* empty = ready + 2 * Cf::S;
   uint64_t* hfull = empty + Cf::S;
   uint64_t* hfree = hfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
@@ -99,8 +98,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   if (tid == 0) {
     for (int s = 0; s < Cf::S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&aready[s], 128);
-      mbar_init(&bready[s], 128);
+      mbar_init(&ready[s], 256);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -141,7 +139,9 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     }
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (the whole warp runs the loop, elect.sync picks the issuing lane; one
+    // barrier check per stage: A and B converters both arrive on ready[s])
+    {
       // M=128, N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
       constexpr uint32_t idesc = make_idesc(BN) | (1u << 16);
       for (int i = 0; i < nst; ++i) {
@@ -152,8 +152,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
           tc_fence_after();
         }
-        mbar_wait(&aready[s], ph);
-        mbar_wait(&bready[s], ph);
+        mbar_wait(&ready[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
@@ -164,12 +163,12 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const uint64_t dbh = make_desc_mn32(bh + ks * 1024, BOX, 512);
           const uint64_t dbl = make_desc_mn32(bl + ks * 1024, BOX, 512);
           const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
-          mma_ts(d, al + 8 * ks, dbh, idesc, acc);
-          mma_ts(d, ah + 8 * ks, dbl, idesc, 1u);
-          mma_ts(d, ah + 8 * ks, dbh, idesc, 1u);
+          mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
         }
-        tc_commit(&empty[s]);
-        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit(&hfull[b]);
+        tc_commit_elect(&empty[s]);
+        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
       }
     }
   } else if (warp < CB0) {
@@ -226,7 +225,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(&aready[s]);
+      mbar_arrive(&ready[s]);
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ B converters
@@ -254,7 +253,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         if (do_bias) { bs.x += v.x; bs.y += v.y; bs.z += v.z; bs.w += v.w; }
       }
       fence_proxy_async();
-      mbar_arrive(&bready[s]);
+      mbar_arrive(&ready[s]);
     }
     if (do_bias) {
       bias_scr[bt] = bs;
