@@ -68,6 +68,13 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t b_
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d), "r"(a), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// true in exactly one (elected) lane of a converged warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}"
+               : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -35,12 +35,22 @@ namespace bpx {
 namespace wgt {
 using namespace tcx;
 
-constexpr int NTHREADS = 18 * 32;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, CB0 = 6, DR0 = 10;   // warps 2-5: A converters
+constexpr int TMB_WARP = 18;                    // B (dz) TMA producer (decoupled rings only)
 
 // BN = 128: 32 pixels per stage, 4 stages.  BN = 64 (Cout = 64): 64 pixels
 // per stage, 3 stages -- a stage then carries as many MMA cycles as a
 // BN = 128 stage, so the per-stage handshakes cost the same fraction.
+//
+// Two rings.  The B ring (raw dz | dz lo) and the TMEM A slots have S
+// stages and are released by the MMA commit.  The raw A tiles have their own
+// ring of SA stages, released by the A converters as soon as they hold the
+// tile in registers, so the x loads run up to SA stages ahead instead of
+// waiting for the MMA: with one shared ring the converters waited on TMA
+// ~40% of the time and the MMA on the converters ~44% (ncu, conv3_2).
+// BN = 64 (conv1_2) keeps one joint ring (A slot s = stage s, one producer,
+// 18 warps): the smem budget leaves no extra A slot there (SA = S = 3), and
+// decoupled measured 0.88 vs 0.83 ms.
 template <int BN>
 struct Cfg {
   static_assert(BN == 64 || BN == 128, "BN");
@@ -48,13 +58,24 @@ struct Cfg {
   static constexpr int BOX = 32 * BK * 4;                 // 32 channels x BK pixels
   static constexpr int PCH = 128 / BK;                    // stages per promotion chunk (K = 128)
   static constexpr int S = BN == 128 ? 4 : 3;
+  static constexpr bool DEC = BN == 128;                  // decoupled A ring
+  static constexpr int SA = DEC ? 5 : S;
+  static constexpr int NT = DEC ? 19 * 32 : 18 * 32;
   static constexpr int A_BYTES = 4 * BOX;                 // 128 rows of A
   static constexpr int B_BYTES = (BN / 32) * BOX;
-  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;     // A raw | B raw | B lo
+  // [A0 | B0 raw | B0 lo] [A1 | B1 ...] ... then the extra A slots (SA > S).
+  // Interleaving the A and B tiles measured 3-13% faster than separate A and
+  // B regions (conv1_2 0.83 vs 0.95 ms, conv5_x 0.14 vs 0.16 ms).
+  static constexpr int STAGE = A_BYTES + 2 * B_BYTES;
+  static constexpr int RINGS = S * STAGE + (SA - S) * A_BYTES;
+  __device__ static char* a_tile(char* smem, int s) {
+    return s < S ? smem + s * STAGE : smem + S * STAGE + (s - S) * A_BYTES;
+  }
+  __device__ static char* b_tile(char* smem, int s) { return smem + s * STAGE + A_BYTES; }
   static constexpr int ACC = 2 * BN;                      // two chunk buffers
   static constexpr int A_COL = ACC;                       // + S stages of (hi|lo)
   static constexpr int RG = 128 / (BN / 4);               // bias row groups
-  static constexpr int SMEM = 1024 + S * STAGE + 512 + 128 * 16;
+  static constexpr int SMEM = 1024 + RINGS + 512 + 128 * 16;
   static_assert(ACC + S * 2 * BK <= 512, "TMEM budget");
   static_assert(SMEM <= 227 * 1024, "smem budget");
 };
@@ -71,7 +92,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 }
 
 template <int BN>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<BN>::NT, 1)
 wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
   using Cf = Cfg<BN>;
@@ -79,13 +100,16 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::S * Cf::STAGE);
-  uint64_t* ready = full + Cf::S;            // A and B converters done
-  uint64_t* empty = ready + 2 * Cf::S;
-  uint64_t* hfull = empty + Cf::S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::RINGS);   // B stage landed
+  uint64_t* ready = full + 8;                // A and B converters done
+  uint64_t* empty = ready + 8;               // MMA done: B stage + TMEM A slot free
+  uint64_t* afull = empty + 8;               // A tile landed
+  uint64_t* afree = afull + 8;               // A tile read by the converters
+  uint64_t* hfull = afree + 8;
   uint64_t* hfree = hfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + 2);
-  float4* bias_scr = reinterpret_cast<float4*>(smem + Cf::S * Cf::STAGE + 512);
+  float4* bias_scr = reinterpret_cast<float4*>(smem + Cf::RINGS + 512);
+  static_assert(Cf::S <= 8 && Cf::SA <= 8, "barrier slots");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nrows = 9 * g.Cin;                  // M extent
@@ -101,6 +125,10 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       mbar_init(&ready[s], 256);
       mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < Cf::SA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&afree[s], 128);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
       mbar_init(&hfree[b], 256);
@@ -114,33 +142,51 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   const uint32_t tmem = *tmem_slot;
 
   if (warp == TMA_WARP) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA: x (A)
     if (lane == 0) {
       tma_prefetch_desc(&tx);
-      tma_prefetch_desc(&tdz);
+      if (!Cf::DEC) tma_prefetch_desc(&tdz);
       int na = 0;
       for (int c = 0; c < 4; ++c) na += (m0 / 32 + c) < chunks;
-      const uint32_t bytes = (uint32_t)(na * BOX + Cf::B_BYTES);
+      const uint32_t bytes = (uint32_t)(na * BOX) + (Cf::DEC ? 0u : (uint32_t)Cf::B_BYTES);
       for (int i = 0; i < nst; ++i) {
-        const int s = i % Cf::S;
-        if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
+        const int s = i % Cf::SA;
+        uint64_t* bar = Cf::DEC ? &afull[s] : &full[s];
+        if (i >= Cf::SA) mbar_wait(Cf::DEC ? &afree[s] : &empty[s], ((i / Cf::SA) - 1) & 1);
         const int p0 = (t0 + i) * BK;
-        char* st = smem + s * Cf::STAGE;
-        mbar_expect_tx(&full[s], bytes);
+        char* st = Cf::a_tile(smem, s);
+        mbar_expect_tx(bar, bytes);
         for (int c = 0; c < 4; ++c) {
           const int gc = m0 / 32 + c;
           if (gc >= chunks) break;
           const int tap = gc / cpt, ci0 = (gc - tap * cpt) * 32;
-          tma_load_2d(st + c * BOX, &tx, ci0, p0 + (tap / 3 - 1) * g.W + tap % 3 - 1, &full[s]);
+          tma_load_2d(st + c * BOX, &tx, ci0, p0 + (tap / 3 - 1) * g.W + tap % 3 - 1, bar);
         }
+        if (!Cf::DEC)
+          for (int j = 0; j < BN / 32; ++j)
+            tma_load_2d(Cf::b_tile(smem, s) + j * BOX, &tdz, n0 + 32 * j, p0, bar);
+      }
+    }
+  } else if (Cf::DEC && warp == TMB_WARP) {
+    // ------------------------------------------------------------ TMA: dz (B)
+    if (lane == 0) {
+      tma_prefetch_desc(&tdz);
+      for (int i = 0; i < nst; ++i) {
+        const int s = i % Cf::S;
+        if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
+        const int p0 = (t0 + i) * BK;
+        char* st = Cf::b_tile(smem, s);
+        mbar_expect_tx(&full[s], (uint32_t)Cf::B_BYTES);
         for (int j = 0; j < BN / 32; ++j)
-          tma_load_2d(st + Cf::A_BYTES + j * BOX, &tdz, n0 + 32 * j, p0, &full[s]);
+          tma_load_2d(st + j * BOX, &tdz, n0 + 32 * j, p0, &full[s]);
       }
     }
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     // (the whole warp runs the loop, elect.sync picks the issuing lane; one
-    // barrier check per stage: A and B converters both arrive on ready[s])
+    // barrier check per stage: A and B converters both arrive on ready[s]).
+    // (Issuing the dz loads from this warp as well, after a wait for
+    // MMA(i-1), measured 8% slower than the separate B producer warp.)
     {
       // M=128, N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
       constexpr uint32_t idesc = make_idesc(BN) | (1u << 16);
@@ -156,7 +202,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
-        const uint32_t bh = smem_u32(smem + s * Cf::STAGE + Cf::A_BYTES);
+        const uint32_t bh = smem_u32(Cf::b_tile(smem, s));
         const uint32_t bl = bh + Cf::B_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
@@ -194,7 +240,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       }
     };
     for (int i = 0; i < nst; ++i) {
-      const int s = i % Cf::S;
+      const int s = i % Cf::S, sa = i % Cf::SA;
       uint32_t vmask[BK / 32];
 #pragma unroll
       for (int h = 0; h < BK / 32; ++h) {
@@ -203,8 +249,8 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         vmask[h] = __ballot_sync(0xffffffffu, ok);
         advance(32);
       }
-      mbar_wait(&full[s], (i / Cf::S) & 1);
-      const char* box = smem + s * Cf::STAGE + q * BOX;
+      mbar_wait(Cf::DEC ? &afull[sa] : &full[s], (i / Cf::SA) & 1);
+      const char* box = Cf::a_tile(smem, sa) + q * BOX;
       const uint32_t a = lanebase + s * 2 * BK;
 #pragma unroll
       for (int h = 0; h < BK / 32; ++h) {
@@ -217,6 +263,11 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
                                                                 ((g8 ^ (kk & 3)) << 5) + w4)
                               : 0.f;
           split(v, hi[k], lo[k]);
+        }
+        if (Cf::DEC && h == BK / 32 - 1) mbar_arrive(&afree[sa]);   // A tile in registers
+        if (Cf::DEC && h == 0 && i >= Cf::S) {              // TMEM slot s: MMA(i - S) done
+          mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
+          tc_fence_after();
         }
         tmem_st16(a + 32 * h, *reinterpret_cast<float(*)[16]>(hi));
         tmem_st16(a + 32 * h + 16, *reinterpret_cast<float(*)[16]>(hi + 16));
@@ -240,7 +291,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     for (int i = 0; i < nst; ++i) {
       const int s = i % Cf::S;
       mbar_wait(&full[s], (i / Cf::S) & 1);
-      const char* raw = smem + s * Cf::STAGE + Cf::A_BYTES;
+      const char* raw = Cf::b_tile(smem, s);
       char* lo = const_cast<char*>(raw) + Cf::B_BYTES;
 #pragma unroll
       for (int k = rg; k < BK; k += Cf::RG) {
@@ -350,7 +401,7 @@ bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g,
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     attr = true;
   }
-  kern<<<dim3(mt, nt, splits), NTHREADS, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+  kern<<<dim3(mt, nt, splits), Cf::NT, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
   return launch_status();
 }
 
