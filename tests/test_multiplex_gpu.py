@@ -48,3 +48,29 @@ def test_two_phase_feedback_and_gated_rerun(fg):
     assert all(f.split(":")[0] in ("compute", "transfer", "allreduce", "loss", "sgd")
                for f in flags)
     assert m.fg_throughput_samples_per_s > 0 and len(tr.iteration_ticks) == 3
+
+
+@pytest.mark.timeout(900)
+def test_pareto_sweep_rows_match_reference_schema():
+    """Measured pareto_sweep (simulator.py:984-1044 semantics) on VGG-16 at
+    B=8: bp+col rows per (amp, config), partition rows for k <= total,
+    cluster = fg + bg, rows sorted by label, reference table format."""
+    import math
+    from paper_2112_10065_b200.sweep import PARETO_HEADER, pareto_sweep, pareto_to_table
+    g = synth.vgg_like(seed=0, global_batch=8)
+    cfgs = [SimConfig(warmup_iterations=1, bg_batch_size=8)]
+    rows = pareto_sweep(g, 1, [2.0], cfgs, bg_graph=synth.small_bg_model(), iterations=3,
+                        partition_sizes=(1, 2))
+    assert [r["label"] for r in rows] == sorted(r["label"] for r in rows)
+    assert [r["scenario"] for r in rows] == ["bp+col", "partition"]
+    for r in rows:
+        assert tuple(r) == PARETO_HEADER
+        assert r["fg_iteration_us"] > 0 and r["fg_speedup"] > 0
+    bp, part = rows
+    assert bp["bg_throughput"] > 0
+    assert bp["cluster_throughput"] >= bp["bg_throughput"]
+    assert part["bg_throughput"] == 0.0 and math.isnan(part["amp_limit"])
+    # on one GPU the partition k=1 foreground is the one-GPU plan itself
+    assert abs(part["fg_speedup"] - 1.0) < 0.25
+    tab = pareto_to_table(rows).splitlines()
+    assert tab[0].split("\t") == list(PARETO_HEADER) and len(tab) == 3
