@@ -112,6 +112,33 @@ BPX_API bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* i
 BPX_API bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* dx,
                                     int n, int h, int w_, int c, void* stream);
 
+/* ---- branch/join elements of the residual net behind `wideresnet_like`
+ * (synth.py:126-169; the `add` layers of its residual diamonds, the stage
+ * transitions where hw halves, and the pool before the classifier).
+ * Residual join (post-activation basic block, ResNet "option A" shortcut):
+ *   y = relu?(a + P(s)),  a, y: [n][h][w][c],  s: [n][h*f][w*f][cs], cs <= c,
+ *   P = stride-f subsample (f = 2 if down) + zero channel padding cs -> c.  */
+BPX_API bpx_status_t bpx_residual_add_fwd(const float* a, const float* s, float* y, int n,
+                                  int h, int w_, int c, int cs, int down, int relu,
+                                  void* stream);
+/* Gradient into the skip source h ([n][h*f][w*f][cs], grad wrt h's
+ * pre-activation; mask = h's ReLU output):
+ *   dh = (accumulate ? dh : 0) + [sampled pixel] * (dmain + (mask > 0) * dz[.., :cs])
+ * dmain (nullable, [n][h][w][cs]) = the already-masked data gradient of a
+ * first conv that read the subsampled h; accumulate and dmain are exclusive. */
+BPX_API bpx_status_t bpx_residual_skip_bwd(const float* dz, const float* dmain,
+                                   const float* mask, float* dh, int n, int h, int w_,
+                                   int c, int cs, int down, int accumulate, void* stream);
+/* y[n][h][w][c] = x[n][2h][2w][c] (stride-2 subsample of the stage input) */
+BPX_API bpx_status_t bpx_subsample2_fwd(const float* x, float* y, int n, int h, int w_,
+                                int c, void* stream);
+/* Global average pool [n][h][w][c] -> [n][c]; bwd: dx = dy / (h*w), masked
+ * by (mask > 0) when mask (the pooled ReLU output) is given.               */
+BPX_API bpx_status_t bpx_global_avgpool_fwd(const float* x, float* y, int n, int h, int w_,
+                                    int c, void* stream);
+BPX_API bpx_status_t bpx_global_avgpool_bwd(const float* dy, const float* mask, float* dx,
+                                    int n, int h, int w_, int c, void* stream);
+
 /* Mean softmax cross-entropy over the GLOBAL batch: loss_out[0] =
  * sum_{local rows} CE / b_global (fixed order); loss_out must hold
  * b_local + 1 floats ([1..b_local] = per-row terms);

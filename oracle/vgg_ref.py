@@ -6,7 +6,10 @@ bench.py's cpu_baseline / --impl reference legs, never by the product.
 The reference toolkit has no forward/backward at all (it prices a
 `compute` op per layer: /root/reference/pkg/src/burstplan/simulator.py:254-261,
 synth.py:86-123), so this is a restatement of the *paper's* step
- for the network `paper_2112_10065_b200.network.vgg16`:
+ for the networks of `paper_2112_10065_b200.network`
+(VGG-16, and the residual net behind `wideresnet_like`: conv with an
+optional stride-2 input subsample, residual `add` with a ResNet option-A
+shortcut, global average pool):
 forward layer by layer, mean softmax cross-entropy over the global batch,
 backward, per-layer weight gradients.  Numerics parity is therefore
 "unpinned" against the reference (no golden vectors exist there); it is
@@ -38,14 +41,29 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
                         b.detach().to(dtype).clone().requires_grad_(True))
     h = x_nhwc.to(dtype).permute(0, 3, 1, 2).contiguous()       # NCHW
     flat = False
+    outs = {}
     for l in net.layers:
         if l.kind == "conv":
             w, b = leaves[l.name]
+            if getattr(l, "down", False):
+                h = h[:, :, ::2, ::2]
             h = F.conv2d(h, w.permute(0, 3, 1, 2), b, padding=1)
             if l.relu:
                 h = F.relu(h)
         elif l.kind == "pool":
             h = F.max_pool2d(h, 2, 2)
+        elif l.kind == "add":            # residual join, ResNet option-A shortcut
+            s = outs[l.skip]
+            if l.skip_down:
+                s = s[:, :, ::2, ::2]
+            if s.shape[1] < h.shape[1]:
+                s = F.pad(s, (0, 0, 0, 0, 0, h.shape[1] - s.shape[1]))
+            h = h + s
+            if l.relu:
+                h = F.relu(h)
+        elif l.kind == "gap":
+            h = h.mean(dim=(2, 3))
+            flat = True
         else:
             if not flat:
                 h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)   # NHWC flatten
@@ -54,6 +72,7 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
             h = F.linear(h, w, b)
             if l.relu:
                 h = F.relu(h)
+        outs[l.name] = h
     loss = F.cross_entropy(h, labels.to(torch.int64))
     loss.backward()
     grads = {n: (w.grad.detach(), b.grad.detach()) for n, (w, b) in leaves.items()}

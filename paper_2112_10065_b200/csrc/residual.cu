@@ -1,0 +1,207 @@
+// Branch/join element kernels for the residual (WRN-style) executable net
+// behind the reference's `wideresnet_like` family (synth.py:126-169): the
+// `add` join of each residual diamond, the stride-2 subsample at stage
+// transitions, and the global average pool before the classifier.  All are
+// HBM-bound elementwise passes: float4 over NHWC channels, grid-stride,
+// fixed-order arithmetic (deterministic).
+//
+// Residual join (post-activation basic block):
+//   y = relu(a + P(s)),  a, y: [n][h][w][c],  s: [n][h*f][w*f][cs], cs <= c
+//   P = stride-f subsample (f = 2 at a stage transition, else 1) followed by
+//       zero channel padding cs -> c (ResNet "option A" shortcut: no params)
+// Its backward to the skip source h (grad wrt h's pre-activation, the
+// executor's `dy` convention: the consumer applies the producer's ReLU mask):
+//   dh[n][H][W][cs] = (acc ? dh : 0)
+//                     + [H%f==0 && W%f==0] * (dmain[n][H/f][W/f][cs]     (if given)
+//                                             + (mask > 0) * dz[n][H/f][W/f][c < cs])
+// `dmain` is the low-resolution data gradient of the block's first conv
+// (already masked by its dgrad) when that conv reads a subsampled copy of h,
+// so one pass writes all of dh at a transition; otherwise the first conv's
+// dgrad has written dh in place and the skip term is accumulated (acc = 1).
+#include "common.cuh"
+#include "simt_api.h"
+
+namespace bpx {
+namespace {
+
+int grid_for(long long work) {
+  long long g = cdivll(work, 256);
+  long long cap = 8LL * num_sms();
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+__device__ __forceinline__ float4 relu4(float4 v) {
+  return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+}
+
+__global__ void resadd_fwd_kernel(const float4* __restrict__ a, const float4* __restrict__ s,
+                                  float4* __restrict__ y, long long total, int h, int w, int c4,
+                                  int cs4, int f, int relu) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % c4);
+    const long long pix = e / c4;
+    const int ow = (int)(pix % w);
+    const long long r = pix / w;
+    const int oh = (int)(r % h);
+    const long long img = r / h;
+    float4 v = a[e];
+    if (ci < cs4) {
+      const float4 t = s[((img * (h * f) + (long long)oh * f) * (w * f) + (long long)ow * f) * cs4 + ci];
+      v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+    }
+    y[e] = relu ? relu4(v) : v;
+  }
+}
+
+__global__ void skip_bwd_kernel(const float4* __restrict__ dz, const float4* __restrict__ dmain,
+                                const float4* __restrict__ mask, float4* __restrict__ dh,
+                                long long total, int H, int W, int c4, int cs4, int f, int acc) {
+  const int h = H / f, w = W / f;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % cs4);
+    const long long pix = e / cs4;
+    const int iw = (int)(pix % W);
+    const long long r = pix / W;
+    const int ih = (int)(r % H);
+    const long long img = r / H;
+    float4 v = acc ? dh[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ih % f == 0 && iw % f == 0) {
+      const long long lp = (img * h + ih / f) * w + iw / f;      // low-res pixel
+      if (dmain) {
+        const float4 d = dmain[lp * cs4 + ci];
+        v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+      }
+      const float4 g = dz[lp * c4 + ci];
+      const float4 m = mask[e];
+      v.x += m.x > 0.f ? g.x : 0.f; v.y += m.y > 0.f ? g.y : 0.f;
+      v.z += m.z > 0.f ? g.z : 0.f; v.w += m.w > 0.f ? g.w : 0.f;
+    }
+    dh[e] = v;
+  }
+}
+
+__global__ void subsample2_kernel(const float4* __restrict__ x, float4* __restrict__ y,
+                                  long long total, int h, int w, int c4) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % c4);
+    const long long pix = e / c4;
+    const int ow = (int)(pix % w);
+    const long long r = pix / w;
+    const int oh = (int)(r % h);
+    const long long img = r / h;
+    y[e] = x[((img * (2 * h) + 2LL * oh) * (2 * w) + 2LL * ow) * c4 + ci];
+  }
+}
+
+// one thread per (image, 4 channels): fixed-order sum over the hw pixels
+__global__ void gap_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y, int n,
+                               int hw, int c4, float scale) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * c4;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long img = e / c4;
+    const int ci = (int)(e % c4);
+    const float4* p = x + img * hw * c4 + ci;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < hw; ++q) {
+      const float4 v = p[(long long)q * c4];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    y[e] = make_float4(s.x * scale, s.y * scale, s.z * scale, s.w * scale);
+  }
+}
+
+__global__ void gap_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ mask,
+                               float4* __restrict__ dx, long long total, int hw, int c4,
+                               float scale) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % c4);
+    const long long img = e / ((long long)hw * c4);
+    const float4 g = dy[img * c4 + ci];
+    float4 v = make_float4(g.x * scale, g.y * scale, g.z * scale, g.w * scale);
+    if (mask) {
+      const float4 m = mask[e];
+      v.x = m.x > 0.f ? v.x : 0.f; v.y = m.y > 0.f ? v.y : 0.f;
+      v.z = m.z > 0.f ? v.z : 0.f; v.w = m.w > 0.f ? v.w : 0.f;
+    }
+    dx[e] = v;
+  }
+}
+
+}  // namespace
+}  // namespace bpx
+
+using namespace bpx;
+
+extern "C" {
+
+bpx_status_t bpx_residual_add_fwd(const float* a, const float* s, float* y, int n, int h,
+                                  int w_, int c, int cs, int down, int relu, void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h >= 0 && w_ >= 0 && c % 4 == 0 && cs % 4 == 0);
+  BPX_CHECK_ARG(cs > 0 && cs <= c && (down == 0 || down == 1));
+  const long long total = (long long)n * h * w_ * (c / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(a && s && y && aligned16(a) && aligned16(s) && aligned16(y));
+  resadd_fwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(s),
+      reinterpret_cast<float4*>(y), total, h, w_, c / 4, cs / 4, down ? 2 : 1, relu);
+  return launch_status();
+}
+
+bpx_status_t bpx_residual_skip_bwd(const float* dz, const float* dmain, const float* mask,
+                                   float* dh, int n, int h, int w_, int c, int cs, int down,
+                                   int accumulate, void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h >= 0 && w_ >= 0 && c % 4 == 0 && cs % 4 == 0);
+  BPX_CHECK_ARG(cs > 0 && cs <= c && (down == 0 || down == 1));
+  BPX_CHECK_ARG(!(dmain && accumulate));
+  const int f = down ? 2 : 1;
+  const long long total = (long long)n * (h * f) * (w_ * f) * (cs / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(dz && mask && dh && aligned16(dz) && aligned16(mask) && aligned16(dh) &&
+                aligned16(dmain));
+  skip_bwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(dz), reinterpret_cast<const float4*>(dmain),
+      reinterpret_cast<const float4*>(mask), reinterpret_cast<float4*>(dh), total, h * f,
+      w_ * f, c / 4, cs / 4, f, accumulate);
+  return launch_status();
+}
+
+bpx_status_t bpx_subsample2_fwd(const float* x, float* y, int n, int h, int w_, int c,
+                                void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h >= 0 && w_ >= 0 && c % 4 == 0);
+  const long long total = (long long)n * h * w_ * (c / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(x && y && aligned16(x) && aligned16(y));
+  subsample2_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), total, h, w_, c / 4);
+  return launch_status();
+}
+
+bpx_status_t bpx_global_avgpool_fwd(const float* x, float* y, int n, int h, int w_, int c,
+                                    void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h > 0 && w_ > 0 && c % 4 == 0);
+  const long long total = (long long)n * (c / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(x && y && aligned16(x) && aligned16(y));
+  gap_fwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), n, h * w_, c / 4,
+      1.0f / (float)(h * w_));
+  return launch_status();
+}
+
+bpx_status_t bpx_global_avgpool_bwd(const float* dy, const float* mask, float* dx, int n,
+                                    int h, int w_, int c, void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h > 0 && w_ > 0 && c % 4 == 0);
+  const long long total = (long long)n * h * w_ * (c / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(dy && dx && aligned16(dy) && aligned16(dx) && aligned16(mask));
+  gap_bwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(mask),
+      reinterpret_cast<float4*>(dx), total, h * w_, c / 4, 1.0f / (float)(h * w_));
+  return launch_status();
+}
+
+}  // extern "C"

@@ -32,7 +32,7 @@ import torch
 from . import ops
 from .comm import LocalComm, TorchComm
 from .costs import shard_range
-from .errors import GraphFormatError
+from .errors import GraphFormatError, UnsupportedTopologyError
 from .graph import CompGraph
 from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
 from .planner import TrainingPlan
@@ -57,6 +57,10 @@ class _Layer:
     dbias: Optional[torch.Tensor] = None
     idx: Optional[torch.Tensor] = None     # pool: first-max position per output
     reshard_in: bool = False               # input arrives through a reshard
+    xs: Optional[torch.Tensor] = None      # down conv: stride-2 subsample of x
+    dxs: Optional[torch.Tensor] = None     # down conv: data gradient at the low resolution
+    s: Optional[torch.Tensor] = None       # add: shortcut input (the skip source's y)
+    skip_i: int = -1                       # add: index of the skip source layer
 
 
 class BurstStep:
@@ -106,6 +110,24 @@ class BurstStep:
             self.pbuckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
         cursor = {g: 0 for g in sizes}
 
+        names = {L.spec.name: i for i, L in enumerate(self.layers)}
+        # residual joins: the diamond (skip source, conv1, conv2, add) must
+        # run on one GPU set -- a shortcut crossing a g change would need its
+        # own reshard pair (not built yet: DESIGN.md, Next)
+        self.join_after: dict[int, int] = {}       # conv1 index -> add index
+        for i, L in enumerate(self.layers):
+            if L.spec.kind != "add":
+                continue
+            L.skip_i = names[L.spec.skip]
+            c1 = L.skip_i + 1
+            if c1 >= i or self.layers[c1].spec.kind != "conv":
+                raise GraphFormatError(f"{L.spec.name}: shortcut does not span a conv chain")
+            if len({self.layers[j].g for j in range(L.skip_i, i + 1)}) != 1:
+                raise UnsupportedTopologyError(
+                    f"{L.spec.name}: a residual diamond spans GPU counts "
+                    f"{sorted({self.layers[j].g for j in range(L.skip_i, i + 1)})}")
+            self.join_after[c1] = i
+
         ws_need = 0
         for i, L in enumerate(self.layers):
             sp = L.spec
@@ -126,6 +148,16 @@ class BurstStep:
                     L.dx = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
                 else:
                     L.dx = prev.dy.view(sp.in_shape(L.b))
+            if sp.down:
+                low = (L.b, sp.hw, sp.hw, sp.cin)
+                L.xs = torch.empty(low, dtype=torch.float32, device=dev)
+                L.dxs = torch.empty(low, dtype=torch.float32, device=dev)
+            if sp.kind == "add":
+                # the join passes its (pre-ReLU) gradient to conv2 unchanged:
+                # conv2's output gradient IS the add's
+                L.s = self.layers[L.skip_i].y
+                prev.dy = L.dy
+                L.dx = L.dy
             ps = sp.param_shapes()
             if ps:
                 w, b = params[sp.name]
@@ -189,8 +221,15 @@ class BurstStep:
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
-        if sp.kind == "conv":
+        if sp.kind == "conv" and sp.down:
+            self.k.subsample2_fwd(L.x, L.xs)
+            self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+        elif sp.kind == "conv":
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+        elif sp.kind == "add":
+            self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu)
+        elif sp.kind == "gap":
+            self.k.global_avgpool_fwd(L.x, L.y)
         elif sp.kind == "pool":
             if L.idx is not None:
                 self.k.maxpool2x2_fwd_idx(L.x, L.y, L.idx)
@@ -199,11 +238,29 @@ class BurstStep:
         else:
             self.k.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
 
+    def _join_bwd(self, i: int) -> None:
+        """Shortcut gradient of the join at ``i`` into its skip source: runs
+        after the block's first conv has written (or, at a transition,
+        produced the low-resolution part of) the source's gradient."""
+        L = self.layers[i]
+        src, c1 = self.layers[L.skip_i], self.layers[L.skip_i + 1]
+        if c1.spec.down:
+            self.k.residual_skip_bwd(L.dy, src.y, src.dy, dmain=c1.dxs, accumulate=False)
+        else:
+            self.k.residual_skip_bwd(L.dy, src.y, src.dy, accumulate=True)
+
     def _bwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
         mask = L.x if sp.in_relu else None
-        if sp.kind == "conv":
+        if sp.kind == "add":
+            return                      # main path: identity (conv2.dy is L.dy)
+        if sp.kind == "gap":
+            self.k.global_avgpool_bwd(L.dy, mask, L.dx)
+        elif sp.kind == "conv" and sp.down:
+            self.k.conv3x3_wgrad(L.xs, L.dy, L.dw, L.dbias, ws=self.ws)
+            self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws)
+        elif sp.kind == "conv":
             self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
                 self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
@@ -253,8 +310,11 @@ class BurstStep:
         if self.layers[-1].active:
             prog.append((("loss", n - 1, "fwd"), self._loss))
         for i in reversed(range(n)):
-            if self.layers[i].active:
+            if self.layers[i].active and self.layers[i].spec.kind != "add":
                 prog.append((("compute", i, "bwd"), lambda i=i: self._bwd(i)))
+            if i in self.join_after and self.layers[i].active:
+                j = self.join_after[i]         # the join's backward = its shortcut gradient
+                prog.append((("compute", j, "bwd"), lambda j=j: self._join_bwd(j)))
             if i and self.layers[i - 1].g != self.layers[i].g:
                 prog.append((("transfer", i, "bwd"), lambda i=i: self._reshard(i, True)))
         for g in sorted(self.buckets, reverse=True):

@@ -26,31 +26,41 @@ from .graph import CompGraph
 @dataclass(frozen=True)
 class LayerSpec:
     name: str
-    kind: str            # conv | pool | dense
-    cin: int             # channels (conv/pool) or input features (dense)
+    kind: str            # conv | pool | dense | add (residual join) | gap (global avg pool)
+    cin: int             # channels (conv/pool/add/gap) or input features (dense)
     cout: int
-    hw: int              # input spatial size (conv/pool); 0 for dense
+    hw: int              # spatial size the layer computes at (pool: input); 0 for dense
     relu: bool           # output passes through ReLU
     in_relu: bool        # input is a ReLU output (dgrad fuses its mask)
+    down: bool = False   # conv: input is 2hw x 2hw, subsampled by 2 first
+    skip: Optional[str] = None   # add: the skip (shortcut) source layer
+    skip_c: int = 0      # add: channels of the skip source (<= cin, zero-padded)
+    skip_down: bool = False      # add: skip source is 2hw x 2hw (subsampled)
 
     @property
     def out_hw(self) -> int:
         return self.hw // 2 if self.kind == "pool" else self.hw
 
+    @property
+    def in_hw(self) -> int:
+        return 2 * self.hw if self.down else self.hw
+
     def in_elems(self) -> int:
         """Input floats per sample."""
-        return self.hw * self.hw * self.cin if self.kind != "dense" else self.cin
+        return self.in_hw * self.in_hw * self.cin if self.kind != "dense" else self.cin
 
     def out_elems(self) -> int:
-        if self.kind == "dense":
+        if self.kind in ("dense", "gap"):
             return self.cout
         return self.out_hw * self.out_hw * self.cout
 
     def in_shape(self, b: int) -> tuple[int, ...]:
-        return (b, self.hw, self.hw, self.cin) if self.kind != "dense" else (b, self.cin)
+        if self.kind == "dense":
+            return (b, self.cin)
+        return (b, self.in_hw, self.in_hw, self.cin)
 
     def out_shape(self, b: int) -> tuple[int, ...]:
-        if self.kind == "dense":
+        if self.kind in ("dense", "gap"):
             return (b, self.cout)
         return (b, self.out_hw, self.out_hw, self.cout)
 
@@ -129,7 +139,84 @@ def mlp_for_chain(graph: CompGraph) -> NetSpec:
     return NetSpec(f"mlp{width}x{len(real)}", 1, width, width, layers)
 
 
-_REGISTRY = {"vgg_like": lambda g: vgg16(), "custom": mlp_for_chain}
+def wideresnet_net(graph: CompGraph) -> NetSpec:
+    """Executable residual net behind the reference's ``wideresnet_like``
+    family (synth.py:126-169), shapes read off the graph itself: channels
+    from each conv's 9*cin*cout parameters, spatial size from its activation
+    bytes.  Builder decisions (the reference family only prices layers,
+    SURVEY.md §8d C3):
+
+    * stem: 3x3 conv 3 -> 64 at the stem's resolution (100x100; the graph's
+      nominal input is 3x400x400 -- the executable net takes the stem's
+      100x100 input directly);
+    * each diamond is a post-activation basic block: conv1 + ReLU, conv2,
+      ``add`` = ReLU(conv2 + shortcut); at a stage transition (hw halves)
+      conv1 reads a stride-2 subsample of its input, and the shortcut is
+      ResNet "option A": stride-2 subsample + zero channel padding (the
+      graph has no projection layer, so the shortcut has no parameters);
+    * ``pool`` = global average pool; ``fc`` = dense (channels -> 1000).
+      The graph gives fc the rest of a 127 M parameter budget; the
+      executable classifier is the real 512 x 1000 layer.
+    """
+    real = [l for l in graph.layers if not l.is_virtual]
+    ids = {l.id for l in real}
+    by_id = {l.id: l for l in real}
+    out_c: dict[int, int] = {}
+    out_hw: dict[int, int] = {}
+    relu_out: dict[int, bool] = {}
+    specs = []
+    input_hw = 0
+    for l in real:
+        preds = [p for p in l.predecessors if p in ids]
+        succs = [by_id[s] for s in l.successors if s in ids]
+        if l.kind == "conv":
+            cin = out_c[preds[0]] if preds else 3
+            cout = l.params_bytes // 4 // (9 * cin)
+            hw = math.isqrt(l.activation_bytes_per_sample // (4 * cout))
+            if 9 * cin * cout * 4 != l.params_bytes or cout * hw * hw * 4 != \
+                    l.activation_bytes_per_sample:
+                raise GraphFormatError(f"{l.name}: not a 3x3 conv shape")
+            if not preds:
+                input_hw = hw
+            ihw = out_hw[preds[0]] if preds else hw
+            if ihw not in (hw, 2 * hw):
+                raise GraphFormatError(f"{l.name}: input {ihw} -> {hw} is not 1x or /2")
+            # a conv feeding only a join is the block's second conv: no ReLU
+            relu = not (len(succs) == 1 and succs[0].kind == "add")
+            specs.append(LayerSpec(l.name, "conv", cin, cout, hw, relu,
+                                   bool(preds) and relu_out[preds[0]], down=ihw == 2 * hw))
+            out_c[l.id], out_hw[l.id], relu_out[l.id] = cout, hw, relu
+        elif l.kind == "add":
+            main = [p for p in preds if by_id[p].kind == "conv"
+                    and len([s for s in by_id[p].successors if s in ids]) == 1]
+            if len(preds) != 2 or len(main) != 1:
+                raise GraphFormatError(f"{l.name}: expected (conv2, shortcut) inputs")
+            m = main[0]
+            sk = preds[0] if preds[1] == m else preds[1]
+            c, hw = out_c[m], out_hw[m]
+            if out_hw[sk] not in (hw, 2 * hw) or out_c[sk] > c:
+                raise GraphFormatError(f"{l.name}: shortcut shape does not fit")
+            specs.append(LayerSpec(l.name, "add", c, c, hw, True, False,
+                                   skip=by_id[sk].name, skip_c=out_c[sk],
+                                   skip_down=out_hw[sk] == 2 * hw))
+            out_c[l.id], out_hw[l.id], relu_out[l.id] = c, hw, True
+        elif l.kind == "pool":
+            p = preds[0]
+            specs.append(LayerSpec(l.name, "gap", out_c[p], out_c[p], out_hw[p], False,
+                                   relu_out[p]))
+            out_c[l.id], out_hw[l.id], relu_out[l.id] = out_c[p], 1, False
+        elif l.kind == "dense":
+            p = preds[0]
+            fout = l.activation_bytes_per_sample // 4
+            specs.append(LayerSpec(l.name, "dense", out_c[p], fout, 0, False, relu_out[p]))
+            out_c[l.id], out_hw[l.id], relu_out[l.id] = fout, 1, False
+        else:
+            raise GraphFormatError(f"{l.name}: kind {l.kind!r} not executable")
+    return NetSpec("wrn", input_hw, 3, specs[-1].cout, tuple(specs))
+
+
+_REGISTRY = {"vgg_like": lambda g: vgg16(), "custom": mlp_for_chain,
+             "wideresnet_like": wideresnet_net}
 
 
 def net_for_graph(graph: CompGraph) -> NetSpec:
@@ -150,12 +237,19 @@ def init_params(net: NetSpec, seed: int = 0) -> dict[str, tuple[torch.Tensor, to
     N(0, 0.01) for dense, zero bias), deterministic in ``seed``."""
     gen = torch.Generator().manual_seed(seed)
     out = {}
+    # residual nets have no normalisation layers: the last conv of each
+    # residual branch (no ReLU of its own) starts scaled by 1/sqrt(blocks),
+    # so the post-activation sum stays O(1) over all diamonds (Fixup-style;
+    # unscaled, 34 diamonds overflow fp32 in the forward pass)
+    blocks = sum(1 for l in net.layers if l.kind == "add")
     for l in net.layers:
         ps = l.param_shapes()
         if ps is None:
             continue
         if l.kind == "conv":
             std = math.sqrt(2.0 / (l.cout * 9))
+            if blocks and not l.relu:
+                std /= math.sqrt(blocks)
         else:
             std = 0.01
         w = torch.randn(ps[0], generator=gen, dtype=torch.float32) * std

@@ -54,6 +54,16 @@ _SIGS = {
                                + [ctypes.c_void_p]),
     "bpx_maxpool2x2_bwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
                                + [ctypes.c_void_p]),
+    "bpx_residual_add_fwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 7
+                             + [ctypes.c_void_p]),
+    "bpx_residual_skip_bwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 7
+                              + [ctypes.c_void_p]),
+    "bpx_subsample2_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
+                           + [ctypes.c_void_p]),
+    "bpx_global_avgpool_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
+                               + [ctypes.c_void_p]),
+    "bpx_global_avgpool_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
+                               + [ctypes.c_void_p]),
     "bpx_softmax_xent": (ctypes.c_int, [_c_float_p, ctypes.c_void_p]
                          + [ctypes.c_int] * 3 + [_c_float_p, _c_float_p, ctypes.c_void_p]),
     "bpx_sgd_update": (ctypes.c_int, [_c_float_p, _c_float_p, ctypes.c_size_t,
@@ -260,6 +270,60 @@ def maxpool2x2_bwd(x, dy, dx):
     n, h, w, c = x.shape
     _check(lib.bpx_maxpool2x2_bwd(_ptr(x), _ptr(dy), _ptr(dx), n, h, w, c,
                                   _stream()), "bpx_maxpool2x2_bwd")
+    return dx
+
+
+def residual_add_fwd(a, s, y, relu=True):
+    """y = relu(a + P(s)): the join of a residual diamond; ``s`` may have
+    fewer channels (zero-padded) and twice the spatial size (subsampled)."""
+    lib = load_library()
+    _f32(a, s, y)
+    n, h, w, c = a.shape
+    cs = s.shape[3]
+    down = 1 if s.shape[1] == 2 * h and h > 0 else 0
+    _check(lib.bpx_residual_add_fwd(_ptr(a), _ptr(s), _ptr(y), n, h, w, c, cs, down,
+                                    int(relu), _stream()), "bpx_residual_add_fwd")
+    return y
+
+
+def residual_skip_bwd(dz, mask, dh, dmain=None, accumulate=True):
+    """Gradient of the join into its skip source (see include/bpx.h)."""
+    lib = load_library()
+    _f32(dz, mask, dh)
+    n, h, w, c = dz.shape
+    cs = dh.shape[3]
+    down = 1 if dh.shape[1] == 2 * h and h > 0 else 0
+    _check(lib.bpx_residual_skip_bwd(_ptr(dz), _ptr(dmain) if dmain is not None else None,
+                                     _ptr(mask), _ptr(dh), n, h, w, c, cs, down,
+                                     int(accumulate), _stream()), "bpx_residual_skip_bwd")
+    return dh
+
+
+def subsample2_fwd(x, y):
+    lib = load_library()
+    _f32(x, y)
+    n, h, w, c = y.shape
+    _check(lib.bpx_subsample2_fwd(_ptr(x), _ptr(y), n, h, w, c, _stream()),
+           "bpx_subsample2_fwd")
+    return y
+
+
+def global_avgpool_fwd(x, y):
+    lib = load_library()
+    _f32(x, y)
+    n, h, w, c = x.shape
+    _check(lib.bpx_global_avgpool_fwd(_ptr(x), _ptr(y), n, h, w, c, _stream()),
+           "bpx_global_avgpool_fwd")
+    return y
+
+
+def global_avgpool_bwd(dy, mask, dx):
+    lib = load_library()
+    _f32(dy, dx)
+    n, h, w, c = dx.shape
+    _check(lib.bpx_global_avgpool_bwd(_ptr(dy), _ptr(mask) if mask is not None else None,
+                                      _ptr(dx), n, h, w, c, _stream()),
+           "bpx_global_avgpool_bwd")
     return dx
 
 

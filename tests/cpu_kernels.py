@@ -116,3 +116,53 @@ def softmax_xent(logits, labels, b_global, loss_out, dlogits):
 
 def sgd_update(w, g, lr):
     w.sub_(lr * g)
+
+
+# ---- residual-net elements (include/bpx.h: bpx_residual_*, subsample2,
+# global_avgpool), same semantics as the CUDA kernels
+def _shortcut(s, h, c):
+    """P(s): stride-2 subsample when s is 2h x 2h, zero channels up to c."""
+    if s.shape[1] == 2 * h:
+        s = s[:, ::2, ::2, :]
+    if s.shape[3] < c:
+        s = F.pad(s, (0, c - s.shape[3]))
+    return s
+
+
+def residual_add_fwd(a, s, y, relu=True):
+    o = a.double() + _shortcut(s.double(), a.shape[1], a.shape[3])
+    y.copy_(F.relu(o) if relu else o)
+    return y
+
+
+def residual_skip_bwd(dz, mask, dh, dmain=None, accumulate=True):
+    f = 2 if dh.shape[1] == 2 * dz.shape[1] else 1
+    cs = dh.shape[3]
+    g = torch.zeros(dh.shape, dtype=torch.float64)
+    low = dz.double()[..., :cs] * (mask.double()[:, ::f, ::f, :] > 0)
+    if dmain is not None:
+        low = low + dmain.double()
+    g[:, ::f, ::f, :] = low
+    if accumulate:
+        g = g + dh.double()
+    dh.copy_(g)
+    return dh
+
+
+def subsample2_fwd(x, y):
+    y.copy_(x[:, ::2, ::2, :])
+    return y
+
+
+def global_avgpool_fwd(x, y):
+    y.copy_(x.double().mean(dim=(1, 2)))
+    return y
+
+
+def global_avgpool_bwd(dy, mask, dx):
+    hw = dx.shape[1] * dx.shape[2]
+    g = (dy.double() / hw)[:, None, None, :].expand(dx.shape)
+    if mask is not None:
+        g = g * (mask > 0)
+    dx.copy_(g)
+    return dx

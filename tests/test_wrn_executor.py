@@ -1,0 +1,97 @@
+"""Branch/join executor for the residual net behind the
+reference's ``wideresnet_like`` family (synth.py:126-169), on CPU.
+
+Drives the real ``BurstStep`` wiring -- shortcut fan-out and gradient
+fan-in, stride-2 stage transitions with option-A shortcuts, global average
+pool -- with the test-only torch op set (tests/cpu_kernels.py) and checks
+loss and every weight gradient against the fp64 oracle (oracle/vgg_ref.py)."""
+
+import pytest
+import torch
+
+from paper_2112_10065_b200 import synth
+from paper_2112_10065_b200.errors import UnsupportedTopologyError
+from paper_2112_10065_b200.network import init_params, net_for_graph, synthetic_batch
+from paper_2112_10065_b200.planner import TrainingPlan
+
+
+def tiny_wrn_graph(batch, stem_c=8, stages=((16, 2, 8), (32, 2, 4)), classes=10):
+    """A reduced wideresnet_like graph built like synth.wideresnet_like:
+    stem, diamonds (conv1, conv2, add), pool, fc; (cout, blocks, hw) per stage."""
+    net = synth._Net(0, synth.PROFILE_BATCHES_SMALL)
+    hw0 = stages[0][2]
+    head = net.layer("stem", "conv", 9 * 3 * stem_c, stem_c * hw0 * hw0 * 4, 1.0, 1, [])
+    cin, k = stem_c, 0
+    for cout, reps, hw in stages:
+        for _ in range(reps):
+            k += 1
+            c1 = net.layer(f"res{k}_conv1", "conv", 9 * cin * cout, cout * hw * hw * 4, 1.0, 1,
+                           [head])
+            c2 = net.layer(f"res{k}_conv2", "conv", 9 * cout * cout, cout * hw * hw * 4, 1.0,
+                           1, [c1])
+            head = net.layer(f"res{k}_add", "add", 0, cout * hw * hw * 4, 0.01, 1, [c2, head])
+            cin = cout
+    pool = net.layer("pool", "pool", 0, cin * 4, 0.01, 1, [head])
+    net.layer("fc", "dense", cin * classes, classes * 4, 1.0, 1, [pool])
+    return net.finish("wideresnet_like", batch, synth.DEFAULT_BANDWIDTH,
+                      synth.DEFAULT_DELAY_US, (3, hw0, hw0))
+
+
+def one_gpu_plan(graph, g=1):
+    ids = [l.id for l in graph.layers if not l.is_virtual]
+    return TrainingPlan(graph.name, g, 2.0, graph.global_batch, tuple((i, g) for i in ids),
+                        0.0, (), ())
+
+
+def test_wideresnet_like_net_structure():
+    net = net_for_graph(synth.wideresnet_like(seed=0, global_batch=32))
+    assert len(net.layers) == 105 and net.input_hw == 100
+    by = net.by_name()
+    assert [l.name for l in net.layers if l.down] == ["res12_conv1", "res23_conv1"]
+    assert [l.name for l in net.layers if l.skip_down] == ["res12_add", "res23_add"]
+    assert by["res1_add"].skip == "stem" and by["res1_add"].skip_c == 64
+    assert by["res12_add"].skip_c == 128 and by["res12_add"].cin == 256
+    assert not by["res5_conv2"].relu and by["res5_conv1"].relu and by["res5_add"].relu
+    assert by["pool"].kind == "gap" and by["fc"].cin == 512 and by["fc"].cout == 1000
+    # conv FLOPs of the graph's own pricing (2*9*cin*cout*hw^2 per conv)
+    g = synth.wideresnet_like(seed=0, global_batch=32)
+    convs = [l for l in net.layers if l.kind == "conv"]
+    assert sum(c.n_params() - c.cout for c in convs) == sum(
+        l.params_bytes // 4 for l in g.layers if l.kind == "conv")
+
+
+def test_tiny_wrn_step_matches_fp64_oracle():
+    import cpu_kernels
+    from oracle import vgg_ref
+    from paper_2112_10065_b200.executor import BurstStep
+    B = 3
+    graph = tiny_wrn_graph(B)
+    net = net_for_graph(graph)
+    params = init_params(net, seed=5)
+    x, y = synthetic_batch(net, B, seed=6)
+    st = BurstStep(one_gpu_plan(graph), graph, params=params, kernels=cpu_kernels, lr=0.0)
+    st.load(x, y)
+    st.forward_backward()
+    ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+    assert abs(st.loss() - ref_loss) <= 1e-6 * abs(ref_loss)
+    grads = st.grads()
+    assert len(grads) == 1 + 2 * 4 + 1
+    for name, (dw, db) in grads.items():
+        assert vgg_ref.normwise_rel(dw, ref[name][0]) < 1e-6, name
+        assert vgg_ref.normwise_rel(db, ref[name][1]) < 1e-6, name
+
+
+class _FakeComm:
+    rank, world = 0, 2
+
+
+def test_diamond_across_gpu_counts_is_rejected():
+    import cpu_kernels
+    from paper_2112_10065_b200.executor import BurstStep
+    graph = tiny_wrn_graph(4)
+    ids = [l.id for l in graph.layers if not l.is_virtual]
+    gs = [2] * len(ids)
+    gs[2] = 1                                   # res1_conv2 on one GPU, its diamond on two
+    p = TrainingPlan(graph.name, 2, 2.0, 4, tuple(zip(ids, gs)), 0.0, (), ())
+    with pytest.raises(UnsupportedTopologyError):
+        BurstStep(p, graph, comm=_FakeComm(), kernels=cpu_kernels, lr=0.0)

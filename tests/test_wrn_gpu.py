@@ -1,0 +1,94 @@
+"""Residual-net (wideresnet_like) on one B200.
+
+Element kernels (libbpx residual join, shortcut gradient, subsample, global
+average pool) against the test-only CPU op set, and a whole reduced
+residual-net training step through the executor against the fp64 oracle
+with the §8c gate (tests/test_step_gpu.py)."""
+
+import pytest
+import torch
+
+import cpu_kernels
+from oracle import vgg_ref
+from paper_2112_10065_b200 import ops
+from paper_2112_10065_b200.executor import BurstStep
+from paper_2112_10065_b200.network import init_params, net_for_graph, synthetic_batch
+from test_wrn_executor import one_gpu_plan, tiny_wrn_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def _rnd(*shape, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randn(shape, generator=g)
+
+
+def _same(got, ref):
+    assert torch.allclose(got.cpu(), ref, rtol=1e-6, atol=1e-6), \
+        (got.cpu() - ref).abs().max().item()
+
+
+@pytest.mark.parametrize("n,h,c,cs,down", [(2, 8, 64, 64, False), (2, 8, 128, 64, False),
+                                           (3, 5, 256, 128, True), (1, 25, 512, 512, False),
+                                           (0, 4, 8, 8, True)])
+def test_residual_join_kernels(n, h, c, cs, down):
+    f = 2 if down else 1
+    a, s = _rnd(n, h, h, c, seed=1), _rnd(n, h * f, h * f, cs, seed=2)
+    y_ref = cpu_kernels.residual_add_fwd(a, s, torch.empty(n, h, h, c))
+    y = ops.residual_add_fwd(a.cuda(), s.cuda(), torch.empty(n, h, h, c, device="cuda"))
+    _same(y, y_ref)
+    dz, mask = _rnd(n, h, h, c, seed=3), _rnd(n, h * f, h * f, cs, seed=4)
+    dh0 = _rnd(n, h * f, h * f, cs, seed=5)
+    for dmain in ((_rnd(n, h, h, cs, seed=6),) if down else ()) + (None,):
+        acc = dmain is None
+        ref = cpu_kernels.residual_skip_bwd(dz, mask, dh0.clone(), dmain=dmain, accumulate=acc)
+        got = ops.residual_skip_bwd(dz.cuda(), mask.cuda(), dh0.clone().cuda(),
+                                    dmain=None if dmain is None else dmain.cuda(),
+                                    accumulate=acc)
+        _same(got, ref)
+
+
+@pytest.mark.parametrize("n,h,c", [(2, 8, 64), (3, 25, 512), (1, 1, 4)])
+def test_subsample_and_global_avgpool(n, h, c):
+    x = _rnd(n, 2 * h, 2 * h, c, seed=7)
+    _same(ops.subsample2_fwd(x.cuda(), torch.empty(n, h, h, c, device="cuda")),
+          x[:, ::2, ::2, :])
+    x = _rnd(n, h, h, c, seed=8)
+    y = ops.global_avgpool_fwd(x.cuda(), torch.empty(n, c, device="cuda"))
+    _same(y, cpu_kernels.global_avgpool_fwd(x, torch.empty(n, c)))
+    dy = _rnd(n, c, seed=9)
+    for mask in (x, None):
+        ref = cpu_kernels.global_avgpool_bwd(dy, mask, torch.empty(n, h, h, c))
+        got = ops.global_avgpool_bwd(dy.cuda(), None if mask is None else mask.cuda(),
+                                     torch.empty(n, h, h, c, device="cuda"))
+        _same(got, ref)
+
+
+@pytest.mark.timeout(600)
+def test_residual_net_step_matches_fp64():
+    B = 2
+    graph = tiny_wrn_graph(B, stem_c=64, stages=((128, 2, 16), (256, 2, 8)), classes=16)
+    net = net_for_graph(graph)
+    params = init_params(net, seed=0)
+    x, y = synthetic_batch(net, B, seed=0)
+    loss64, g64 = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+    loss32, g32 = vgg_ref.forward_backward(net, params, x, y, torch.float32)
+    st = BurstStep(one_gpu_plan(graph), graph, params=params, lr=0.0)
+    st.load(x, y)
+    st.forward_backward()
+    torch.cuda.synchronize()
+    loss = st.loss()
+    assert abs(loss - loss64) / abs(loss64) <= 1e-4, (loss, loss64)
+    for name, (dw, db) in st.grads().items():
+        for got, ref, ref32 in ((dw, g64[name][0], g32[name][0]),
+                                (db, g64[name][1], g32[name][1])):
+            e = vgg_ref.normwise_rel(got, ref)
+            gate = max(1e-3, 2 * vgg_ref.normwise_rel(ref32, ref))
+            assert e <= gate, (name, e, gate)
+    # graph replay is bitwise identical to the eager step
+    g0 = {k: (a.clone(), b.clone()) for k, (a, b) in st.grads().items()}
+    st.capture(warmup=1)
+    st.step()
+    torch.cuda.synchronize()
+    for k, (a, b) in st.grads().items():
+        assert torch.equal(a, g0[k][0]) and torch.equal(b, g0[k][1]), k
