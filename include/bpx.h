@@ -132,6 +132,11 @@ BPX_API bpx_status_t bpx_residual_skip_bwd(const float* dz, const float* dmain,
 /* y[n][h][w][c] = x[n][2h][2w][c] (stride-2 subsample of the stage input) */
 BPX_API bpx_status_t bpx_subsample2_fwd(const float* x, float* y, int n, int h, int w_,
                                 int c, void* stream);
+/* dx[n][2h][2w][c] = dy[n][h][w][c] at even (row, col), 0 elsewhere       */
+BPX_API bpx_status_t bpx_subsample2_bwd(const float* dy, float* dx, int n, int h, int w_,
+                                int c, void* stream);
+/* dst += src (n floats, n % 4 == 0): gradient fan-in across layouts        */
+BPX_API bpx_status_t bpx_accumulate(float* dst, const float* src, size_t n, void* stream);
 /* Global average pool [n][h][w][c] -> [n][c]; bwd: dx = dy / (h*w), masked
  * by (mask > 0) when mask (the pooled ReLU output) is given.               */
 BPX_API bpx_status_t bpx_global_avgpool_fwd(const float* x, float* y, int n, int h, int w_,

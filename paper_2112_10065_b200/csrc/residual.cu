@@ -96,6 +96,33 @@ __global__ void subsample2_kernel(const float4* __restrict__ x, float4* __restri
   }
 }
 
+// dx[n][2h][2w][c] = dy at even (row, col), 0 elsewhere
+__global__ void subsample2_bwd_kernel(const float4* __restrict__ dy, float4* __restrict__ dx,
+                                      long long total, int H, int W, int c4) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % c4);
+    const long long pix = e / c4;
+    const int iw = (int)(pix % W);
+    const long long r = pix / W;
+    const int ih = (int)(r % H);
+    const long long img = r / H;
+    dx[e] = ((ih | iw) & 1) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                            : dy[((img * (H / 2) + ih / 2) * (W / 2) + iw / 2) * c4 + ci];
+  }
+}
+
+__global__ void accumulate_kernel(float4* __restrict__ dst, const float4* __restrict__ src,
+                                  long long n4) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4;
+       e += (long long)gridDim.x * blockDim.x) {
+    float4 a = dst[e];
+    const float4 b = src[e];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    dst[e] = a;
+  }
+}
+
 // one thread per (image, 4 channels): fixed-order sum over the hw pixels
 __global__ void gap_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y, int n,
                                int hw, int c4, float scale) {
@@ -177,6 +204,28 @@ bpx_status_t bpx_subsample2_fwd(const float* x, float* y, int n, int h, int w_, 
   BPX_CHECK_ARG(x && y && aligned16(x) && aligned16(y));
   subsample2_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), total, h, w_, c / 4);
+  return launch_status();
+}
+
+bpx_status_t bpx_subsample2_bwd(const float* dy, float* dx, int n, int h, int w_, int c,
+                                void* stream) {
+  BPX_CHECK_ARG(n >= 0 && h >= 0 && w_ >= 0 && c % 4 == 0);
+  const long long total = (long long)n * (2 * h) * (2 * w_) * (c / 4);
+  if (total == 0) return BPX_OK;
+  BPX_CHECK_ARG(dy && dx && aligned16(dy) && aligned16(dx));
+  subsample2_bwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), total, 2 * h,
+      2 * w_, c / 4);
+  return launch_status();
+}
+
+bpx_status_t bpx_accumulate(float* dst, const float* src, size_t n, void* stream) {
+  BPX_CHECK_ARG(n % 4 == 0);
+  if (n == 0) return BPX_OK;
+  BPX_CHECK_ARG(dst && src && aligned16(dst) && aligned16(src));
+  const long long n4 = (long long)(n / 4);
+  accumulate_kernel<<<grid_for(n4), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), n4);
   return launch_status();
 }
 

@@ -32,7 +32,7 @@ import torch
 from . import ops
 from .comm import LocalComm, TorchComm
 from .costs import shard_range
-from .errors import GraphFormatError, UnsupportedTopologyError
+from .errors import GraphFormatError
 from .graph import CompGraph
 from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
 from .planner import TrainingPlan
@@ -59,8 +59,11 @@ class _Layer:
     reshard_in: bool = False               # input arrives through a reshard
     xs: Optional[torch.Tensor] = None      # down conv: stride-2 subsample of x
     dxs: Optional[torch.Tensor] = None     # down conv: data gradient at the low resolution
-    s: Optional[torch.Tensor] = None       # add: shortcut input (the skip source's y)
+    s: Optional[torch.Tensor] = None       # add: shortcut input (skip source's y, add layout)
     skip_i: int = -1                       # add: index of the skip source layer
+    join: str = ""                         # add: shortcut-gradient path (fused|direct|reshard)
+    dskip: Optional[torch.Tensor] = None   # add: shortcut gradient in the add's layout
+    dskip_src: Optional[torch.Tensor] = None   # add: ... resharded to the source's layout
 
 
 class BurstStep:
@@ -111,9 +114,16 @@ class BurstStep:
         cursor = {g: 0 for g in sizes}
 
         names = {L.spec.name: i for i, L in enumerate(self.layers)}
-        # residual joins: the diamond (skip source, conv1, conv2, add) must
-        # run on one GPU set -- a shortcut crossing a g change would need its
-        # own reshard pair (not built yet: DESIGN.md, Next)
+        # residual joins (branch/join diamonds: skip source S -> conv1 ->
+        # conv2 -> add, plus the shortcut S -> add).  The shortcut gradient
+        # reaches S.dy after conv1's data gradient (and its reshard) wrote it:
+        #   fused   S, conv1 (a stride-2 transition) and add share g: one
+        #           kernel writes S.dy = P^T(conv1's low-res dx) + shortcut;
+        #   direct  S and add share g: the shortcut term is accumulated in place;
+        #   reshard otherwise: the shortcut input is resharded S -> add layout
+        #           in the forward, its gradient add -> S layout in the
+        #           backward and accumulated into S.dy (the reference's
+        #           `transfer` of a branch edge, simulator.py:242-253).
         self.join_after: dict[int, int] = {}       # conv1 index -> add index
         for i, L in enumerate(self.layers):
             if L.spec.kind != "add":
@@ -122,10 +132,13 @@ class BurstStep:
             c1 = L.skip_i + 1
             if c1 >= i or self.layers[c1].spec.kind != "conv":
                 raise GraphFormatError(f"{L.spec.name}: shortcut does not span a conv chain")
-            if len({self.layers[j].g for j in range(L.skip_i, i + 1)}) != 1:
-                raise UnsupportedTopologyError(
-                    f"{L.spec.name}: a residual diamond spans GPU counts "
-                    f"{sorted({self.layers[j].g for j in range(L.skip_i, i + 1)})}")
+            S, C1 = self.layers[L.skip_i], self.layers[c1]
+            if S.g != L.g:
+                L.join = "reshard"
+            elif C1.spec.down and C1.g == S.g:
+                L.join = "fused"
+            else:
+                L.join = "direct"
             self.join_after[c1] = i
 
         ws_need = 0
@@ -154,10 +167,19 @@ class BurstStep:
                 L.dxs = torch.empty(low, dtype=torch.float32, device=dev)
             if sp.kind == "add":
                 # the join passes its (pre-ReLU) gradient to conv2 unchanged:
-                # conv2's output gradient IS the add's
-                L.s = self.layers[L.skip_i].y
-                prev.dy = L.dy
+                # conv2's output gradient IS the add's (same layout), or its
+                # backward transfer when conv2 runs on another GPU count
                 L.dx = L.dy
+                if not L.reshard_in:
+                    prev.dy = L.dy
+                S = self.layers[L.skip_i]
+                sshape = (L.b,) + tuple(S.spec.out_shape(1)[1:])
+                if L.join == "reshard":
+                    L.s = torch.empty(sshape, dtype=torch.float32, device=dev)
+                else:
+                    L.s = S.y
+                if L.join != "fused" and L.join != "direct":
+                    L.dskip = torch.empty(sshape, dtype=torch.float32, device=dev)
             ps = sp.param_shapes()
             if ps:
                 w, b = params[sp.name]
@@ -176,6 +198,11 @@ class BurstStep:
                         L.b, sp.hw, sp.hw, sp.cin, sp.cout))
                 else:
                     ws_need = max(ws_need, self.k.linear_workspace_bytes(L.b, sp.cin, sp.cout))
+        for L in self.layers:
+            if L.join == "reshard":
+                S = self.layers[L.skip_i]
+                if S.active:
+                    L.dskip_src = torch.empty_like(S.y)
         self.ws = self.k.Workspace(dev)
         self.ws.reserve(ws_need)
         last = self.layers[-1]
@@ -239,15 +266,38 @@ class BurstStep:
             self.k.linear_fwd(L.x.view(L.b, sp.cin), L.w, L.bias, L.y, sp.relu, ws=self.ws)
 
     def _join_bwd(self, i: int) -> None:
-        """Shortcut gradient of the join at ``i`` into its skip source: runs
-        after the block's first conv has written (or, at a transition,
-        produced the low-resolution part of) the source's gradient."""
+        """Shortcut gradient of the join at ``i`` (add-active ranks): runs
+        after the block's first conv has written (fused: produced the
+        low-resolution part of) the source's gradient."""
         L = self.layers[i]
         src, c1 = self.layers[L.skip_i], self.layers[L.skip_i + 1]
-        if c1.spec.down:
-            self.k.residual_skip_bwd(L.dy, src.y, src.dy, dmain=c1.dxs, accumulate=False)
+        if L.join == "fused":
+            self.k.residual_skip_bwd(L.dy, L.s, src.dy, dmain=c1.dxs, accumulate=False)
+        elif L.join == "direct":
+            self.k.residual_skip_bwd(L.dy, L.s, src.dy, accumulate=True)
         else:
-            self.k.residual_skip_bwd(L.dy, src.y, src.dy, accumulate=True)
+            self.k.residual_skip_bwd(L.dy, L.s, L.dskip, accumulate=False)
+
+    def _skip_reshard(self, i: int, backward: bool) -> None:
+        L = self.layers[i]
+        S = self.layers[L.skip_i]
+        bps = 4 * S.spec.out_elems()
+        if not backward:
+            self.comm.reshard(S.y if S.active else None, S.g,
+                              L.s if L.active else None, L.g, self.B, bps)
+        else:
+            self.comm.reshard(L.dskip if L.active else None, L.g,
+                              L.dskip_src if S.active else None, S.g, self.B, bps)
+
+    def _skip_accumulate(self, i: int) -> None:
+        L = self.layers[i]
+        self.k.accumulate(self.layers[L.skip_i].dy, L.dskip_src)
+
+    def _fused_down(self, i: int) -> bool:
+        """conv ``i`` is a transition conv whose low-res data gradient the
+        join folds into the source's gradient (no separate upsample)."""
+        j = self.join_after.get(i)
+        return j is not None and self.layers[j].join == "fused"
 
     def _bwd(self, i: int) -> None:
         L = self.layers[i]
@@ -260,6 +310,8 @@ class BurstStep:
         elif sp.kind == "conv" and sp.down:
             self.k.conv3x3_wgrad(L.xs, L.dy, L.dw, L.dbias, ws=self.ws)
             self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws)
+            if not self._fused_down(i):
+                self.k.subsample2_bwd(L.dxs, L.dx)
         elif sp.kind == "conv":
             self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
@@ -305,6 +357,9 @@ class BurstStep:
         for i in range(n):
             if i and self.layers[i - 1].g != self.layers[i].g:
                 prog.append((("transfer", i, "fwd"), lambda i=i: self._reshard(i, False)))
+            if self.layers[i].join == "reshard":
+                prog.append((("transfer", i, "skip_fwd"),
+                             lambda i=i: self._skip_reshard(i, False)))
             if self.layers[i].active:
                 prog.append((("compute", i, "fwd"), lambda i=i: self._fwd(i)))
         if self.layers[-1].active:
@@ -312,11 +367,21 @@ class BurstStep:
         for i in reversed(range(n)):
             if self.layers[i].active and self.layers[i].spec.kind != "add":
                 prog.append((("compute", i, "bwd"), lambda i=i: self._bwd(i)))
-            if i in self.join_after and self.layers[i].active:
-                j = self.join_after[i]         # the join's backward = its shortcut gradient
-                prog.append((("compute", j, "bwd"), lambda j=j: self._join_bwd(j)))
             if i and self.layers[i - 1].g != self.layers[i].g:
                 prog.append((("transfer", i, "bwd"), lambda i=i: self._reshard(i, True)))
+            if i in self.join_after:
+                # the join's backward = its shortcut gradient, after conv1's
+                # data gradient (and its transfer) wrote the source's dy
+                j = self.join_after[i]
+                J = self.layers[j]
+                if J.active:
+                    prog.append((("compute", j, "bwd"), lambda j=j: self._join_bwd(j)))
+                if J.join == "reshard":
+                    prog.append((("transfer", j, "skip_bwd"),
+                                 lambda j=j: self._skip_reshard(j, True)))
+                    if self.layers[J.skip_i].active:
+                        prog.append((("compute", j, "skip_acc"),
+                                     lambda j=j: self._skip_accumulate(j)))
         for g in sorted(self.buckets, reverse=True):
             if g > 1:
                 prog.append((("allreduce", g, "sync"),

@@ -60,6 +60,9 @@ _SIGS = {
                               + [ctypes.c_void_p]),
     "bpx_subsample2_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
                            + [ctypes.c_void_p]),
+    "bpx_subsample2_bwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
+                           + [ctypes.c_void_p]),
+    "bpx_accumulate": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_global_avgpool_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
                                + [ctypes.c_void_p]),
     "bpx_global_avgpool_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
@@ -306,6 +309,25 @@ def subsample2_fwd(x, y):
     _check(lib.bpx_subsample2_fwd(_ptr(x), _ptr(y), n, h, w, c, _stream()),
            "bpx_subsample2_fwd")
     return y
+
+
+def subsample2_bwd(dy, dx):
+    lib = load_library()
+    _f32(dy, dx)
+    n, h, w, c = dy.shape
+    _check(lib.bpx_subsample2_bwd(_ptr(dy), _ptr(dx), n, h, w, c, _stream()),
+           "bpx_subsample2_bwd")
+    return dx
+
+
+def accumulate(dst, src):
+    """dst += src (same number of floats)."""
+    lib = load_library()
+    _f32(dst, src)
+    if dst.numel() != src.numel():
+        raise KernelError("accumulate: size mismatch")
+    _check(lib.bpx_accumulate(_ptr(dst), _ptr(src), dst.numel(), _stream()), "bpx_accumulate")
+    return dst
 
 
 def global_avgpool_fwd(x, y):

@@ -166,3 +166,14 @@ def global_avgpool_bwd(dy, mask, dx):
         g = g * (mask > 0)
     dx.copy_(g)
     return dx
+
+
+def subsample2_bwd(dy, dx):
+    dx.zero_()
+    dx[:, ::2, ::2, :] = dy
+    return dx
+
+
+def accumulate(dst, src):
+    dst.copy_(dst.double() + src.double().reshape(dst.shape))
+    return dst

@@ -10,7 +10,6 @@ import pytest
 import torch
 
 from paper_2112_10065_b200 import synth
-from paper_2112_10065_b200.errors import UnsupportedTopologyError
 from paper_2112_10065_b200.network import init_params, net_for_graph, synthetic_batch
 from paper_2112_10065_b200.planner import TrainingPlan
 
@@ -81,17 +80,74 @@ def test_tiny_wrn_step_matches_fp64_oracle():
         assert vgg_ref.normwise_rel(db, ref[name][1]) < 1e-6, name
 
 
-class _FakeComm:
-    rank, world = 0, 2
+# world 2, ragged B=5, g changing inside diamonds: res1/res2 joins take the
+# shortcut through a reshard, res3 (a stride-2 transition) has its conv1 on
+# another g than its source (un-fused upsample + transfer, then a direct
+# accumulate), res4 the same without the transition
+GS = [2, 1, 2, 1, 1, 1, 2, 1, 2, 2, 1, 1, 2, 1, 1]
+B2 = 5
 
 
-def test_diamond_across_gpu_counts_is_rejected():
-    import cpu_kernels
-    from paper_2112_10065_b200.executor import BurstStep
-    graph = tiny_wrn_graph(4)
-    ids = [l.id for l in graph.layers if not l.is_virtual]
-    gs = [2] * len(ids)
-    gs[2] = 1                                   # res1_conv2 on one GPU, its diamond on two
-    p = TrainingPlan(graph.name, 2, 2.0, 4, tuple(zip(ids, gs)), 0.0, (), ())
-    with pytest.raises(UnsupportedTopologyError):
-        BurstStep(p, graph, comm=_FakeComm(), kernels=cpu_kernels, lr=0.0)
+def _worker(rank, port, q):
+    try:
+        import os
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.set_num_threads(1)
+        import cpu_kernels
+        from oracle import vgg_ref
+        from paper_2112_10065_b200.comm import TorchComm
+        from paper_2112_10065_b200.executor import BurstStep
+        graph = tiny_wrn_graph(B2)
+        net = net_for_graph(graph)
+        params = init_params(net, seed=7)
+        x, y = synthetic_batch(net, B2, seed=8)
+        ids = [l.id for l in graph.layers if not l.is_virtual]
+        p = TrainingPlan(graph.name, 2, 2.0, B2, tuple(zip(ids, GS)), 0.0, (), ())
+        st = BurstStep(p, graph, comm=TorchComm(rank, 2, set(GS)), params=params,
+                       kernels=cpu_kernels, lr=0.0)
+        joins = {L.spec.name: L.join for L in st.layers if L.spec.kind == "add"}
+        st.load(x, y)
+        st.forward_backward()
+        st.sync_and_update()
+        res = {"loss": st.loss(), "joins": joins}
+        if rank == 0:
+            ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+            res["ref_loss"] = ref_loss
+            res["errs"] = {n: max(vgg_ref.normwise_rel(dw, ref[n][0]),
+                                  vgg_ref.normwise_rel(db, ref[n][1]))
+                           for n, (dw, db) in st.grads().items()}
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+def test_world2_diamonds_across_gpu_counts_match_oracle():
+    import socket
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ps = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in out[r], out[r].get("error")
+    r0 = out[0]
+    assert r0["joins"] == {"res1_add": "reshard", "res2_add": "reshard",
+                           "res3_add": "direct", "res4_add": "direct"}
+    assert abs(r0["loss"] - r0["ref_loss"]) <= 1e-6 * abs(r0["ref_loss"])
+    # rank 0 holds every layer's (allreduced) gradient: it is in every group
+    assert len(r0["errs"]) == 10
+    for name, e in r0["errs"].items():
+        assert e < 1e-6, (name, e)
