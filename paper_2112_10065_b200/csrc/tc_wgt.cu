@@ -91,12 +91,22 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN>
+// PAIR: the two CTAs of a cluster (M tiles 2p, 2p+1; same N tile and K
+// split) run one M = 256 tcgen05.mma.cta_group::2 per k-step.  Each CTA keeps
+// its own 128 A rows in its TMEM and loads / splits only HALF of the dz tile
+// (N/2 output channels), which halves the per-SM shared-memory traffic of
+// the B operand (TMA fill, lo pass, MMA reads).  The leader (rank 0) issues
+// the MMAs; its commits arrive on both CTAs' barriers (multicast); the
+// peer's converters and drains arrive on the leader's ready / hfree.
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(Cfg<BN>::NT, 1)
 wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
   using Cf = Cfg<BN>;
   constexpr int BK = Cf::BK, BOX = Cf::BOX, PCH = Cf::PCH;
+  static_assert(!PAIR || Cf::DEC, "pairs run the decoupled-ring layout");
+  constexpr int BNL = PAIR ? BN / 2 : BN;                 // dz columns held by this CTA
+  constexpr uint32_t B_BYTES_L = (uint32_t)(BNL / 32) * BOX;
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -116,13 +126,15 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   const int chunks = nrows / 32;                // 32-row chunks (tap-major)
   const int cpt = g.Cin / 32;                   // chunks per tap
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int nl0 = n0 + (int)rank * BNL;                   // first dz column held here
   const int t0 = blockIdx.z * g.tps;
   const int nst = max(0, min(g.tiles, t0 + g.tps) - t0);
 
   if (tid == 0) {
     for (int s = 0; s < Cf::S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 256);
+      mbar_init(&ready[s], PAIR ? 16 : 256);     // pairs: one arrival per warp, both CTAs
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < Cf::SA; ++s) {
@@ -131,15 +143,20 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
-      mbar_init(&hfree[b], 256);
+      mbar_init(&hfree[b], PAIR ? 16 : 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
+  if (warp == MMA_WARP) {
+    if (PAIR) tmem_alloc2(tmem_slot, 512); else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // leader's ready / hfree as shared::cluster addresses (pairs)
+  const uint32_t ready_l = PAIR ? mapa_rank(ready, 0) : 0u;
+  const uint32_t hfree_l = PAIR ? mapa_rank(hfree, 0) : 0u;
 
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA: x (A)
@@ -176,9 +193,9 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         if (i >= Cf::S) mbar_wait(&empty[s], ((i / Cf::S) - 1) & 1);
         const int p0 = (t0 + i) * BK;
         char* st = Cf::b_tile(smem, s);
-        mbar_expect_tx(&full[s], (uint32_t)Cf::B_BYTES);
-        for (int j = 0; j < BN / 32; ++j)
-          tma_load_2d(st + j * BOX, &tdz, n0 + 32 * j, p0, &full[s]);
+        mbar_expect_tx(&full[s], B_BYTES_L);
+        for (int j = 0; j < BNL / 32; ++j)
+          tma_load_2d(st + j * BOX, &tdz, nl0 + 32 * j, p0, &full[s]);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -187,18 +204,20 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     // barrier check per stage: A and B converters both arrive on ready[s]).
     // (Issuing the dz loads from this warp as well, after a wait for
     // MMA(i-1), measured 8% slower than the separate B producer warp.)
-    {
-      // M=128, N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
-      constexpr uint32_t idesc = make_idesc(BN) | (1u << 16);
+    if (!PAIR || rank == 0) {
+      // M=128 (pairs: 256), N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
+      constexpr uint32_t idesc = PAIR ? ((make_idesc(BN) & ~(0x1Fu << 24)) | (16u << 24) | (1u << 16))
+                                      : (make_idesc(BN) | (1u << 16));
       for (int i = 0; i < nst; ++i) {
         const int s = i % Cf::S;
         const uint32_t ph = (i / Cf::S) & 1;
         const int c = i / PCH, b = c & 1;
         if (i % PCH == 0 && c >= 2) {
-          mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
+          if (PAIR) mbar_wait_cluster(&hfree[b], ((c >> 1) - 1) & 1);
+          else mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
           tc_fence_after();
         }
-        mbar_wait(&ready[s], ph);
+        if (PAIR) mbar_wait_cluster(&ready[s], ph); else mbar_wait(&ready[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
@@ -209,12 +228,23 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const uint64_t dbh = make_desc_mn32(bh + ks * 1024, BOX, 512);
           const uint64_t dbl = make_desc_mn32(bl + ks * 1024, BOX, 512);
           const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
-          mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
-          mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
-          mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          if (PAIR) {
+            mma_ts2_elect(d, al + 8 * ks, dbh, idesc, acc);
+            mma_ts2_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+            mma_ts2_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          } else {
+            mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
+            mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+            mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          }
         }
-        tc_commit_elect(&empty[s]);
-        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+        if (PAIR) {
+          tc_commit2_elect(&empty[s]);
+          if (i % PCH == PCH - 1 || i == nst - 1) tc_commit2_elect(&hfull[b]);
+        } else {
+          tc_commit_elect(&empty[s]);
+          if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+        }
       }
     }
   } else if (warp < CB0) {
@@ -276,17 +306,23 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(&ready[s]);
+      if (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(ready_l + 8u * s);
+      } else {
+        mbar_arrive(&ready[s]);
+      }
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ B converters
     // b_lo = b - tf32(b), elementwise in the swizzled layout; per-channel dz
     // sums (bias gradient) over this split's pixels in CTAs of M tile 0.
     const int bt = tid - CB0 * 32;
-    constexpr int NC4 = BN / 4;                // float4 columns of the tile
+    constexpr int NC4 = BNL / 4;               // float4 columns of this CTA's tile
+    constexpr int RG = 128 / NC4;              // row groups
     const int c4 = bt % NC4, rg = bt / NC4;    // fixed column, row group
     const int box = c4 / 8, gl = (c4 & 7) >> 1, half = c4 & 1;
-    const bool do_bias = bias_part != nullptr && blockIdx.x == 0;
+    const bool do_bias = bias_part != nullptr && blockIdx.x / (PAIR ? 2 : 1) == 0;
     float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = 0; i < nst; ++i) {
       const int s = i % Cf::S;
@@ -294,7 +330,7 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       const char* raw = Cf::b_tile(smem, s);
       char* lo = const_cast<char*>(raw) + Cf::B_BYTES;
 #pragma unroll
-      for (int k = rg; k < BK; k += Cf::RG) {
+      for (int k = rg; k < BK; k += RG) {
         const int off = box * BOX + k * 128 + ((gl ^ (k & 3)) << 5) + half * 16;
         const float4 v = *reinterpret_cast<const float4*>(raw + off);
         float4 h, l;
@@ -304,18 +340,23 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         if (do_bias) { bs.x += v.x; bs.y += v.y; bs.z += v.z; bs.w += v.w; }
       }
       fence_proxy_async();
-      mbar_arrive(&ready[s]);
+      if (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(ready_l + 8u * s);
+      } else {
+        mbar_arrive(&ready[s]);
+      }
     }
     if (do_bias) {
       bias_scr[bt] = bs;
       named_sync(1, 128);
       if (bt < NC4) {
         float4 t = bias_scr[bt];
-        for (int r = 1; r < Cf::RG; ++r) {
+        for (int r = 1; r < RG; ++r) {
           const float4 u = bias_scr[r * NC4 + bt];
           t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
         }
-        *reinterpret_cast<float4*>(bias_part + (long long)blockIdx.z * g.Cout + n0 + 4 * bt) = t;
+        *reinterpret_cast<float4*>(bias_part + (long long)blockIdx.z * g.Cout + nl0 + 4 * bt) = t;
       }
     }
   } else {
@@ -340,7 +381,12 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]);
       }
       tc_fence_before();
-      mbar_arrive(&hfree[b]);
+      if (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(hfree_l + 8u * b);
+      } else {
+        mbar_arrive(&hfree[b]);
+      }
     }
     const int r = m0 + q * 32 + lane;
     if (r < nrows) {
@@ -351,16 +397,25 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    tmem_free(tmem, 512);
+    if (PAIR) tmem_free2(tmem, 512); else tmem_free(tmem, 512);
   }
 }
 
 // ------------------------------------------------------------------ host side
 
 inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
+#ifndef WGT_PAIR
+#define WGT_PAIR 1
+#endif
+// N = 128 tiles run as CTA pairs (M = 256 per cluster) when the M tiles pair
+// up without a padding tile (Cin = 256, 512: 3-4% faster; with a padding
+// tile, Cin = 64, 128, the extra tile costs 10-14%)
+inline bool paired(int cin, int cout) {
+  return WGT_PAIR && bn_for(cout) == 128 && cdiv(9 * cin, 128) % 2 == 0;
+}
 
 inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
   g.Cin = cin; g.Cout = cout; g.H = H; g.W = W;
@@ -368,6 +423,7 @@ inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& n
   g.tiles = (int)cdivll(g.npix, bn_for(cout) == 128 ? Cfg<128>::BK : Cfg<64>::BK);
   g.slab = (long long)cout * 9 * cin;
   mt = cdiv(9 * cin, 128);
+  if (paired(cin, cout)) mt += mt & 1;         // whole pairs (a padding tile computes zeros)
   nt = cout / bn_for(cout);
   const int tiles_mn = mt * nt;
   int want = num_sms() / tiles_mn;
@@ -391,17 +447,34 @@ inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C, i
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g, int mt,
                     int nt, int splits, float* part, float* bias_part, cudaStream_t st) {
   using Cf = Cfg<BN>;
-  auto kern = wgt_kernel<BN>;
+  auto kern = wgt_kernel<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     attr = true;
   }
-  kern<<<dim3(mt, nt, splits), Cf::NT, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+  if (!PAIR) {
+    kern<<<dim3(mt, nt, splits), Cf::NT, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+    return launch_status();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(mt, nt, splits);
+  cfg.blockDim = dim3(Cf::NT);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, tx, tdz, g, part, bias_part) != cudaSuccess)
+    return BPX_ERR_LAUNCH;
   return launch_status();
 }
 
@@ -444,8 +517,9 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
   float* bpart = !dbias ? nullptr
                         : (splits == 1 ? dbias : static_cast<float*>(ws) + (size_t)splits * slab);
   bpx_status_t s = wgt::bn_for(cout) == 128
-      ? wgt::launch<128>(tx, tdz, g, mt, nt, splits, part, bpart, st)
-      : wgt::launch<64>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+      ? (wgt::paired(cin, cout) ? wgt::launch<128, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+                           : wgt::launch<128, false>(tx, tdz, g, mt, nt, splits, part, bpart, st))
+      : wgt::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
   if (s != BPX_OK || splits == 1) return s;
   s = split_reduce(part, splits, slab, dw, st);
   if (s != BPX_OK || !dbias) return s;
