@@ -65,6 +65,16 @@ BPX_API bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float
                              float* y, int n, int h, int w_, int cin, int cout,
                              int relu, void* ws, size_t ws_bytes, void* stream);
 BPX_API size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout);
+/* Same op with the weights' 3xTF32 low part supplied by the caller
+ * (w_lo = w - tf32(w), from bpx_tf32_split_lo; NULL = split here): a
+ * training step splits every weight once per update instead of once per
+ * call.  bpx_conv3x3_dgrad_presplit likewise.                              */
+BPX_API bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w,
+                                      const float* w_lo, const float* bias, float* y,
+                                      int n, int h, int w_, int cin, int cout, int relu,
+                                      void* ws, size_t ws_bytes, void* stream);
+/* lo[i] = w[i] - tf32(w[i]) (truncated tf32: the value the tensor core reads), n % 4 == 0 */
+BPX_API bpx_status_t bpx_tf32_split_lo(const float* w, float* lo, size_t n, void* stream);
 
 /* dx = conv3x3_transpose(dz, w) [* (mask_src > 0) if mask_src != NULL].
  * dz:[n,h,w,cout] dx,mask_src:[n,h,w,cin].  mask_src is the layer input
@@ -74,6 +84,10 @@ BPX_API bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w,
                                int w_, int cin, int cout, void* ws,
                                size_t ws_bytes, void* stream);
 BPX_API size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout);
+BPX_API bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w,
+                                        const float* w_lo, const float* mask_src, float* dx,
+                                        int n, int h, int w_, int cin, int cout, void* ws,
+                                        size_t ws_bytes, void* stream);
 
 /* dw[cout,3,3,cin] = sum_pixels dz (x) im2col(x);  dbias[cout] = sum dz.  */
 BPX_API bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw,

@@ -71,12 +71,13 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
 namespace bpx {
 bool fdt_conv_ok(int cin, int cout, int w);
 size_t fdt_conv_ws(int n, int h, int w, int cin, int cout);
-bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                          int h, int w_, int cin, int cout, int relu, void* ws,
-                          size_t ws_bytes, cudaStream_t st);
-bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
-                            int n, int h, int w_, int cin, int cout, void* ws,
-                            size_t ws_bytes, cudaStream_t st);
+// w_lo (nullable): w - tf32(w) split by the caller (bpx_tf32_split_lo)
+bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* w_lo, const float* bias,
+                          float* y, int n, int h, int w_, int cin, int cout, int relu,
+                          void* ws, size_t ws_bytes, cudaStream_t st);
+bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* w_lo,
+                            const float* mask, float* dx, int n, int h, int w_, int cin,
+                            int cout, void* ws, size_t ws_bytes, cudaStream_t st);
 }  // namespace bpx
 
 // TMA-fed tcgen05 dense fwd / dgrad for batches <= 32 (tc_dense.cu).

@@ -503,9 +503,11 @@ inline void tile2d(int H, int W, int& tw, int& th) {
     if (W % w == 0 && H % (128 / w) == 0) { tw = w; th = 128 / w; return; }
 }
 
+// wlo_ready: `wlo` already holds w - tf32(w) (the caller split the weights
+// once per update); otherwise the split runs here into the workspace.
 template <int BN, int KS, int NS, bool DG, class EPI>
-bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n, int H, int W,
-                 int Cin, int Cout, EPI epi, cudaStream_t st) {
+bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, float* part,
+                 int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
   using Cf = Cfg<BN, KS, NS>;
   Geo g;
   g.H = H; g.W = W;
@@ -575,11 +577,15 @@ bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n,
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
-  const long long n4 = (long long)Cout * 9 * Cin / 4;
-  int sgrid = (int)cdivll(n4, 256);
-  if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
-  split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
-                                         reinterpret_cast<float4*>(wlo), n4);
+  int nk = 1;
+  if (!wlo_ready) {
+    const long long n4 = (long long)Cout * 9 * Cin / 4;
+    int sgrid = (int)cdivll(n4, 256);
+    if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
+    split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
+                                           reinterpret_cast<float4*>(wlo), n4);
+    ++nk;
+  }
   auto kern = fdt_kernel<BN, KS, NS, DG, EPI>;
   static bool attr = false;
   if (!attr) {
@@ -588,20 +594,21 @@ bpx_status_t run(const float* a, const float* w, float* wlo, float* part, int n,
   }
   const int grid = g.units < num_sms() ? g.units : num_sms();
   kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
-  if (g.ksplit == 1) return launch_status(2);
+  if (g.ksplit == 1) return launch_status(nk);
   const long long groups = (long long)g.npix * (g.N / 8);
   int fg = (int)cdivll(groups, 256);
   if (fg > 8 * num_sms()) fg = 8 * num_sms();
   fdt_finish<<<fg, 256, 0, st>>>(part, g.ksplit, g.npix, g.N, epi);
-  return launch_status(3);
+  return launch_status(nk + 1);
 }
 
 template <bool DG, class EPI>
-bpx_status_t dispatch(const float* a, const float* w, float* wlo, float* part, int n, int H,
-                      int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
+bpx_status_t dispatch(const float* a, const float* w, float* wlo, bool ready, float* part,
+                      int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
   const int N = DG ? Cin : Cout;
-  if (N % 128 == 0) return run<128, 32, 4, DG>(a, w, wlo, part, n, H, W, Cin, Cout, epi, st);
-  return run<64, 64, 3, DG>(a, w, wlo, part, n, H, W, Cin, Cout, epi, st);
+  if (N % 128 == 0)
+    return run<128, 32, 4, DG>(a, w, wlo, ready, part, n, H, W, Cin, Cout, epi, st);
+  return run<64, 64, 3, DG>(a, w, wlo, ready, part, n, H, W, Cin, Cout, epi, st);
 }
 
 }  // namespace fdt
@@ -633,34 +640,50 @@ size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
   return (wlo + part) * sizeof(float);
 }
 
-bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                          int h, int w_, int cin, int cout, int relu, void* ws,
-                          size_t ws_bytes, cudaStream_t st) {
-  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y))
+bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* w_lo, const float* bias,
+                          float* y, int n, int h, int w_, int cin, int cout, int relu,
+                          void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y) ||
+      !aligned16(w_lo))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EBiasAct epi{y, bias, relu};
-  float* wlo = static_cast<float*>(ws);
-  return fdt::dispatch<false>(x, w, wlo, wlo + (size_t)cout * 9 * cin, n, h, w_, cin, cout, epi,
-                              st);
+  float* scratch = static_cast<float*>(ws);
+  float* wlo = w_lo ? const_cast<float*>(w_lo) : scratch;
+  return fdt::dispatch<false>(x, w, wlo, w_lo != nullptr, scratch + (size_t)cout * 9 * cin, n,
+                              h, w_, cin, cout, epi, st);
 }
 
-bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* mask, float* dx,
-                            int n, int h, int w_, int cin, int cout, void* ws,
-                            size_t ws_bytes, cudaStream_t st) {
+bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* w_lo,
+                            const float* mask, float* dx, int n, int h, int w_, int cin,
+                            int cout, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!fdt_conv_ok(cin, cout, w_) || !aligned16(dz) || !aligned16(w) || !aligned16(dx) ||
-      (mask && !aligned16(mask)))
+      (mask && !aligned16(mask)) || !aligned16(w_lo))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EMask epi{dx, mask};
-  float* wlo = static_cast<float*>(ws);
-  return fdt::dispatch<true>(dz, w, wlo, wlo + (size_t)cout * 9 * cin, n, h, w_, cin, cout, epi,
-                             st);
+  float* scratch = static_cast<float*>(ws);
+  float* wlo = w_lo ? const_cast<float*>(w_lo) : scratch;
+  return fdt::dispatch<true>(dz, w, wlo, w_lo != nullptr, scratch + (size_t)cout * 9 * cin, n,
+                             h, w_, cin, cout, epi, st);
 }
 
 }  // namespace bpx
+
+extern "C" bpx_status_t bpx_tf32_split_lo(const float* w, float* lo, size_t n, void* stream) {
+  using namespace bpx;
+  BPX_CHECK_ARG(n % 4 == 0);
+  if (n == 0) return BPX_OK;
+  BPX_CHECK_ARG(w && lo && aligned16(w) && aligned16(lo));
+  const long long n4 = (long long)(n / 4);
+  int grid = (int)cdivll(n4, 256);
+  if (grid > 4 * num_sms()) grid = 4 * num_sms();
+  fdt::split_lo_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(w), reinterpret_cast<float4*>(lo), n4);
+  return launch_status();
+}
 
 #ifdef FDT_PROF
 // Profiling builds only (BPX_NVCC_EXTRA=-DFDT_PROF): MMA-issuer cycles of the

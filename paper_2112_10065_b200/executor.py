@@ -55,6 +55,7 @@ class _Layer:
     bias: Optional[torch.Tensor] = None
     dw: Optional[torch.Tensor] = None
     dbias: Optional[torch.Tensor] = None
+    w_lo: Optional[torch.Tensor] = None    # conv: w - tf32(w), refreshed after each update
     idx: Optional[torch.Tensor] = None     # pool: first-max position per output
     reshard_in: bool = False               # input arrives through a reshard
     xs: Optional[torch.Tensor] = None      # down conv: stride-2 subsample of x
@@ -198,6 +199,27 @@ class BurstStep:
                         L.b, sp.hw, sp.hw, sp.cin, sp.cout))
                 else:
                     ws_need = max(ws_need, self.k.linear_workspace_bytes(L.b, sp.cin, sp.cout))
+        # conv weights' 3xTF32 low parts: one split launch per bucket over
+        # its contiguous conv span, after every update (fwd and dgrad then
+        # reuse it instead of splitting per call)
+        self.lo_spans: list = []
+        if hasattr(self.k, "tf32_split_lo"):
+            spans: dict[int, list] = {}
+            for L in self.layers:
+                if L.active and L.spec.kind == "conv":
+                    off = L.w.data_ptr() - self.pbuckets[L.g].data_ptr()
+                    a, b = off // 4, off // 4 + L.w.numel()
+                    sp = spans.setdefault(L.g, [a, b])
+                    sp[0], sp[1] = min(sp[0], a), max(sp[1], b)
+            for g, (a, b) in spans.items():
+                a, b = a // 4 * 4, (b + 3) // 4 * 4
+                lo = torch.empty(b - a, dtype=torch.float32, device=dev)
+                self.lo_spans.append((self.pbuckets[g][a:b], lo))
+                for L in self.layers:
+                    if L.active and L.spec.kind == "conv" and L.g == g:
+                        o = (L.w.data_ptr() - self.pbuckets[g].data_ptr()) // 4 - a
+                        L.w_lo = lo[o:o + L.w.numel()].view(L.w.shape)
+            self._split_lo()
         for L in self.layers:
             if L.join == "reshard":
                 S = self.layers[L.skip_i]
@@ -248,11 +270,12 @@ class BurstStep:
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
+        lo = {"w_lo": L.w_lo} if L.w_lo is not None else {}
         if sp.kind == "conv" and sp.down:
             self.k.subsample2_fwd(L.x, L.xs)
-            self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+            self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
         elif sp.kind == "conv":
-            self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws)
+            self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
         elif sp.kind == "add":
             self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu)
         elif sp.kind == "gap":
@@ -309,13 +332,15 @@ class BurstStep:
             self.k.global_avgpool_bwd(L.dy, mask, L.dx)
         elif sp.kind == "conv" and sp.down:
             self.k.conv3x3_wgrad(L.xs, L.dy, L.dw, L.dbias, ws=self.ws)
-            self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws)
+            self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
+                                 **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
             if not self._fused_down(i):
                 self.k.subsample2_bwd(L.dxs, L.dx)
         elif sp.kind == "conv":
             self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
-                self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws)
+                self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws,
+                                     **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
         elif sp.kind == "pool":
             if L.idx is not None:
                 self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx)
@@ -396,6 +421,11 @@ class BurstStep:
     def _sgd(self) -> None:
         for g in sorted(self.buckets):
             self.k.sgd_update(self.pbuckets[g], self.buckets[g], self.lr)
+        self._split_lo()
+
+    def _split_lo(self) -> None:
+        for w, lo in self.lo_spans:
+            self.k.tf32_split_lo(w, lo)
 
     def run_ops(self, prog) -> None:
         for key, fn in prog:

@@ -31,6 +31,11 @@ _SIGS = {
     "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
+    "bpx_conv3x3_fwd_presplit": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_int] * 6
+                                 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_int] * 5
+                                   + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_tf32_split_lo": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
                           + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_dgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
@@ -169,30 +174,42 @@ def _ws(ws: Optional[Workspace], nbytes: int, device):
 
 # ---------------------------------------------------------------- layers
 
-def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None):
+def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None, w_lo=None):
+    """``w_lo`` (optional): w - tf32(w) from ``tf32_split_lo``, reused across
+    calls until the weights change."""
     lib = load_library()
-    _f32(x, w, bias, y)
+    _f32(x, w, bias, y, w_lo)
     n, h, wd, cin = x.shape
     cout = w.shape[0]
     need = lib.bpx_conv3x3_fwd_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, x.device)
-    _check(lib.bpx_conv3x3_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(y), n, h, wd,
-                               cin, cout, int(relu), wp, wb, _stream()),
+    _check(lib.bpx_conv3x3_fwd_presplit(_ptr(x), _ptr(w), _ptr(w_lo), _ptr(bias), _ptr(y), n,
+                                        h, wd, cin, cout, int(relu), wp, wb, _stream()),
            "bpx_conv3x3_fwd")
     return y
 
 
-def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None):
+def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, w_lo=None):
     lib = load_library()
-    _f32(dz, w, mask_src, dx)
+    _f32(dz, w, mask_src, dx, w_lo)
     n, h, wd, cout = dz.shape
     cin = w.shape[3]
     need = lib.bpx_conv3x3_dgrad_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, dz.device)
-    _check(lib.bpx_conv3x3_dgrad(_ptr(dz), _ptr(w), _ptr(mask_src), _ptr(dx), n,
-                                 h, wd, cin, cout, wp, wb, _stream()),
+    _check(lib.bpx_conv3x3_dgrad_presplit(_ptr(dz), _ptr(w), _ptr(w_lo), _ptr(mask_src),
+                                          _ptr(dx), n, h, wd, cin, cout, wp, wb, _stream()),
            "bpx_conv3x3_dgrad")
     return dx
+
+
+def tf32_split_lo(w, lo):
+    """lo = w - tf32(w) elementwise (same number of floats, multiple of 4)."""
+    lib = load_library()
+    _f32(w, lo)
+    if w.numel() != lo.numel() or w.numel() % 4:
+        raise KernelError("tf32_split_lo: sizes must match and be a multiple of 4")
+    _check(lib.bpx_tf32_split_lo(_ptr(w), _ptr(lo), w.numel(), _stream()), "bpx_tf32_split_lo")
+    return lo
 
 
 def conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):
