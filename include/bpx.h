@@ -151,6 +151,27 @@ BPX_API bpx_status_t bpx_subsample2_bwd(const float* dy, float* dx, int n, int h
                                 int c, void* stream);
 /* dst += src (n floats, n % 4 == 0): gradient fan-in across layouts        */
 BPX_API bpx_status_t bpx_accumulate(float* dst, const float* src, size_t n, void* stream);
+/* ---- branch/join elements of the four-tower net behind `inception_like`
+ * (synth.py:172-226).  Pool tower: 3x3 / stride-1 / pad-1 max pool over the
+ * first cs channels of x [n][h][w][c] -> y, idx [n][h][w][cs] (idx = first
+ * max position 0..8, row-major window); bwd writes all c channels of dx
+ * (0 beyond cs), gathering each input's gradient in fixed order.           */
+BPX_API bpx_status_t bpx_maxpool3x3_fwd_idx(const float* x, float* y, uint8_t* idx, int n,
+                                    int h, int w_, int c, int cs, void* stream);
+BPX_API bpx_status_t bpx_maxpool3x3_bwd_idx(const uint8_t* idx, const float* dy, float* dx,
+                                    int n, int h, int w_, int c, int cs, void* stream);
+/* Channel concat of k <= 4 NHWC parts (cs[i] channels each, multiples of 4)
+ * over npix pixels; bwd slices dy back into the parts.                     */
+BPX_API bpx_status_t bpx_concat_fwd(const float* const* parts, const int* cs, int k, float* y,
+                            long long npix, void* stream);
+BPX_API bpx_status_t bpx_concat_bwd(const float* dy, float* const* parts, const int* cs, int k,
+                            long long npix, void* stream);
+/* y[n][i][j][c] = x[n][2i+off][2j+off][c], off in {0, 1} (35 -> 17 keeps the
+ * odd pixels); bwd: dx = dy at those pixels, 0 elsewhere.                   */
+BPX_API bpx_status_t bpx_subsample_fwd(const float* x, float* y, int n, int hin, int win,
+                               int h, int w_, int c, int off, void* stream);
+BPX_API bpx_status_t bpx_subsample_bwd(const float* dy, float* dx, int n, int hin, int win,
+                               int h, int w_, int c, int off, void* stream);
 /* Global average pool [n][h][w][c] -> [n][c]; bwd: dx = dy / (h*w), masked
  * by (mask > 0) when mask (the pooled ReLU output) is given.               */
 BPX_API bpx_status_t bpx_global_avgpool_fwd(const float* x, float* y, int n, int h, int w_,

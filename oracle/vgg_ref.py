@@ -7,9 +7,10 @@ The reference toolkit has no forward/backward at all (it prices a
 `compute` op per layer: /root/reference/pkg/src/burstplan/simulator.py:254-261,
 synth.py:86-123), so this is a restatement of the *paper's* step
  for the networks of `paper_2112_10065_b200.network`
-(VGG-16, and the residual net behind `wideresnet_like`: conv with an
-optional stride-2 input subsample, residual `add` with a ResNet option-A
-shortcut, global average pool):
+(VGG-16; the residual net behind `wideresnet_like`: conv with an optional
+stride-2 input subsample, residual `add` with a ResNet option-A shortcut,
+global average pool; the four-tower net behind `inception_like`: 1x1 convs,
+3x3/s1 max pool over a channel subset, channel concat, branch inputs):
 forward layer by layer, mean softmax cross-entropy over the global batch,
 backward, per-layer weight gradients.  Numerics parity is therefore
 "unpinned" against the reference (no golden vectors exist there); it is
@@ -43,13 +44,27 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
     flat = False
     outs = {}
     for l in net.layers:
+        src = getattr(l, "src", None)
+        if src is not None:                  # branch edge: input from a named layer
+            h = outs[src]
+            flat = h.dim() == 2
+        if getattr(l, "down", False):        # stride-2 subsample (offset 0 or 1)
+            off = l.sub_off
+            h = h[:, :, off:off + 2 * l.hw:2, off:off + 2 * l.hw:2]
         if l.kind == "conv":
             w, b = leaves[l.name]
-            if getattr(l, "down", False):
-                h = h[:, :, ::2, ::2]
             h = F.conv2d(h, w.permute(0, 3, 1, 2), b, padding=1)
             if l.relu:
                 h = F.relu(h)
+        elif l.kind == "conv1x1":
+            w, b = leaves[l.name]
+            h = F.conv2d(h, w.permute(0, 3, 1, 2), b)
+            if l.relu:
+                h = F.relu(h)
+        elif l.kind == "pool3":              # 3x3/s1/p1 max over the first cout channels
+            h = F.max_pool2d(h[:, :l.cout], 3, 1, 1)
+        elif l.kind == "concat":
+            h = torch.cat([outs[n] for n in l.srcs], dim=1)
         elif l.kind == "pool":
             h = F.max_pool2d(h, 2, 2)
         elif l.kind == "add":            # residual join, ResNet option-A shortcut

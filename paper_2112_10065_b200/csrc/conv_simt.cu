@@ -93,6 +93,7 @@ bpx_status_t simt_conv_wgrad(const float* x, const float* dz, float* dw, float* 
 
 static int dense_splits(int M, int N, int K) {
   long long tiles = (long long)cdiv(M, 128) * cdiv(N, N <= 32 ? 32 : 128);
+  if (tiles <= 0) return 1;                   // empty shard: nothing to split
   return pick_splits(tiles, K, 512);
 }
 

@@ -632,6 +632,7 @@ bpx_status_t tc_conv_wgrad(const float* x, const float* dz, float* dw, float* db
 
 static int dense_splits(int M, int N, int K) {
   long long tiles = (long long)cdiv(M, BM) * cdiv(N, bn_for(N));
+  if (tiles <= 0) return 1;                   // empty shard: nothing to split
   return tc::pick_splits(tiles, K, 256);
 }
 size_t tc_linear_fwd_ws(int b, int in, int out) {
@@ -640,8 +641,16 @@ size_t tc_linear_fwd_ws(int b, int in, int out) {
 size_t tc_linear_dgrad_ws(int b, int in, int out) {
   return (size_t)dense_splits(in, b, out) * in * b * sizeof(float);
 }
+// split-K partials over the batch (pixel-batched 1x1 convs: b = pixels),
+// then the bias column sums (which reuse the space after the reduce)
+static int wgrad_dense_splits(int b, int in, int out) {
+  return pick_splits((long long)cdiv(out, BM) * cdiv(in, 128), b, 512);
+}
 size_t tc_linear_wgrad_ws(int b, int in, int out) {
-  return colsum_workspace_floats(b, out) * sizeof(float);
+  const int splits = wgrad_dense_splits(b, in, out);
+  const size_t part = splits > 1 ? (size_t)splits * out * in : 0;
+  const size_t cs = colsum_workspace_floats(b, out);
+  return (part > cs ? part : cs) * sizeof(float);
 }
 
 // out[n][m] = act(sum_z part[z][m][n] + bias[m]) * mask
@@ -705,9 +714,18 @@ bpx_status_t tc_linear_wgrad(const float* x, const float* dy, float* dw, float* 
   }
   MatMN la{dy, out, out};
   MatMN lb{x, in, in};
-  EPartial epi{dw, in, 0};
-  int splits = 1;
-  bpx_status_t s = launch<128>(la, lb, epi, out, in, b, splits, st);
+  int splits = wgrad_dense_splits(b, in, out);
+  bpx_status_t s;
+  if (splits == 1) {
+    EPartial epi{dw, in, 0};
+    s = launch<128>(la, lb, epi, out, in, b, splits, st);
+  } else {
+    float* part = static_cast<float*>(ws);
+    const size_t slab = (size_t)out * in;
+    EPartial epi{part, in, (long long)slab};
+    s = launch<128>(la, lb, epi, out, in, b, splits, st);
+    if (s == BPX_OK) s = split_reduce(part, splits, slab, dw, st);
+  }
   if (s != BPX_OK || !dbias) return s;
   return colsum(dy, b, out, dbias, static_cast<float*>(ws),
                 colsum_workspace_floats(b, out), st);

@@ -485,6 +485,7 @@ bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g,
 bool wgt_conv_ok(int cin, int cout) { return cin % 32 == 0 && cout % 64 == 0; }
 
 size_t wgt_conv_ws(int n, int h, int w, int cin, int cout) {
+  if (!wgt_conv_ok(cin, cout)) return 0;      // the planner assumes a supported shape
   wgt::Geo g;
   int mt, nt, splits;
   wgt::plan(n, h, w, cin, cout, g, mt, nt, splits);

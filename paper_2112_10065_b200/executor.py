@@ -32,7 +32,7 @@ import torch
 from . import ops
 from .comm import LocalComm, TorchComm
 from .costs import shard_range
-from .errors import GraphFormatError
+from .errors import GraphFormatError, UnsupportedTopologyError
 from .graph import CompGraph
 from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
 from .planner import TrainingPlan
@@ -56,6 +56,11 @@ class _Layer:
     dw: Optional[torch.Tensor] = None
     dbias: Optional[torch.Tensor] = None
     w_lo: Optional[torch.Tensor] = None    # conv: w - tf32(w), refreshed after each update
+    src_i: int = -1                        # input layer (-1: the network input / concat)
+    srcs_i: tuple = ()                     # concat: joined layers
+    dx_acc: bool = False                   # dx is private: accumulate into the source's dy
+    cat_dst: tuple = ()                    # concat bwd targets (source dy or private)
+    cat_acc: tuple = ()                    # concat: (source index, private buffer) pairs
     idx: Optional[torch.Tensor] = None     # pool: first-max position per output
     reshard_in: bool = False               # input arrives through a reshard
     xs: Optional[torch.Tensor] = None      # down conv: stride-2 subsample of x
@@ -142,26 +147,70 @@ class BurstStep:
                 L.join = "direct"
             self.join_after[c1] = i
 
+        # input edges: the previous layer (a chain edge, resharded when g
+        # changes), a named earlier layer (a branch edge), or several
+        # (concat).  Branch edges stay on one GPU set.  A layer feeding
+        # several consumers gets its gradient from all of them: the consumer
+        # whose backward runs first (the highest index) writes the source's
+        # dy, the others write private buffers that are accumulated into it.
+        consumers: dict[int, list] = {}
+        for i, L in enumerate(self.layers):
+            sp = L.spec
+            if sp.kind == "concat":
+                L.srcs_i = tuple(names[n] for n in sp.srcs)
+                edges = L.srcs_i
+            else:
+                L.src_i = names[sp.src] if sp.src is not None else i - 1
+                edges = (L.src_i,) if L.src_i >= 0 else ()
+            for j in edges:
+                if (j != i - 1 or sp.kind == "concat") and self.layers[j].g != L.g:
+                    raise UnsupportedTopologyError(
+                        f"{sp.name}: branch edge from {self.layers[j].spec.name} crosses "
+                        f"GPU counts {self.layers[j].g} -> {L.g}")
+                consumers.setdefault(j, []).append(i)
+        for j, cs in consumers.items():
+            if len(cs) > 1 and any(self.layers[c].g != self.layers[j].g for c in cs):
+                raise UnsupportedTopologyError(
+                    f"{self.layers[j].spec.name}: fan-out across GPU counts")
+
         ws_need = 0
         for i, L in enumerate(self.layers):
             sp = L.spec
             if not L.active:
                 continue
-            prev = self.layers[i - 1] if i else None
-            L.reshard_in = prev is not None and prev.g != L.g
-            if prev is None or L.reshard_in:
+            src = self.layers[L.src_i] if L.src_i >= 0 else None
+            prev = src
+            L.reshard_in = src is not None and src.g != L.g
+            if sp.kind == "concat":
+                L.x = None
+            elif src is None or L.reshard_in:
                 L.x = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
             else:
-                L.x = prev.y.view(sp.in_shape(L.b))
+                L.x = src.y.view(sp.in_shape(L.b))
             L.y = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
             if sp.kind == "pool" and hasattr(self.k, "maxpool2x2_fwd_idx"):
                 L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
+            if sp.kind == "pool3":
+                L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
             L.dy = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
-            if i > 0:
-                if L.reshard_in:
+            if src is not None:
+                last = consumers[L.src_i][-1] == i
+                if L.reshard_in or not last:
                     L.dx = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
+                    L.dx_acc = not L.reshard_in
                 else:
-                    L.dx = prev.dy.view(sp.in_shape(L.b))
+                    L.dx = src.dy.view(sp.in_shape(L.b))
+            if sp.kind == "concat":
+                dst, acc = [], []
+                for j in L.srcs_i:
+                    S = self.layers[j]
+                    if consumers[j][-1] == i:
+                        dst.append(S.dy)
+                    else:
+                        buf = torch.empty_like(S.dy)
+                        dst.append(buf)
+                        acc.append((j, buf))
+                L.cat_dst, L.cat_acc = tuple(dst), tuple(acc)
             if sp.down:
                 low = (L.b, sp.hw, sp.hw, sp.cin)
                 L.xs = torch.empty(low, dtype=torch.float32, device=dev)
@@ -197,6 +246,9 @@ class BurstStep:
                 if sp.kind == "conv":
                     ws_need = max(ws_need, self.k.conv_workspace_bytes(
                         L.b, sp.hw, sp.hw, sp.cin, sp.cout))
+                elif sp.kind == "conv1x1":
+                    ws_need = max(ws_need, self.k.linear_workspace_bytes(
+                        L.b * sp.hw * sp.hw, sp.cin, sp.cout))
                 else:
                     ws_need = max(ws_need, self.k.linear_workspace_bytes(L.b, sp.cin, sp.cout))
         # conv weights' 3xTF32 low parts: one split launch per bucket over
@@ -272,8 +324,17 @@ class BurstStep:
         sp = L.spec
         lo = {"w_lo": L.w_lo} if L.w_lo is not None else {}
         if sp.kind == "conv" and sp.down:
-            self.k.subsample2_fwd(L.x, L.xs)
+            self._sub_fwd(L)
             self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
+        elif sp.kind == "conv1x1":
+            x = self._sub_fwd(L) if sp.down else L.x
+            P = L.b * sp.hw * sp.hw
+            self.k.linear_fwd(x.reshape(P, sp.cin), L.w.view(sp.cout, sp.cin), L.bias,
+                              L.y.view(P, sp.cout), sp.relu, ws=self.ws)
+        elif sp.kind == "pool3":
+            self.k.maxpool3x3_fwd_idx(self._sub_fwd(L) if sp.down else L.x, L.y, L.idx)
+        elif sp.kind == "concat":
+            self.k.concat_fwd([self.layers[j].y for j in L.srcs_i], L.y)
         elif sp.kind == "conv":
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
         elif sp.kind == "add":
@@ -316,6 +377,35 @@ class BurstStep:
         L = self.layers[i]
         self.k.accumulate(self.layers[L.skip_i].dy, L.dskip_src)
 
+    def _sub_fwd(self, L) -> torch.Tensor:
+        """Stride-2 subsample of a down layer's input into L.xs."""
+        off = L.spec.sub_off
+        if off == 0 and hasattr(self.k, "subsample2_fwd"):
+            self.k.subsample2_fwd(L.x, L.xs)
+        else:
+            self.k.subsample_fwd(L.x, L.xs, off)
+        return L.xs
+
+    def _sub_bwd(self, L) -> None:
+        off = L.spec.sub_off
+        if off == 0 and hasattr(self.k, "subsample2_bwd"):
+            self.k.subsample2_bwd(L.dxs, L.dx)
+        else:
+            self.k.subsample_bwd(L.dxs, L.dx, off)
+
+    def _fanin(self, i: int) -> None:
+        """Accumulate this consumer's private input gradient(s) into the
+        source's dy (a fan-out source's non-first consumers)."""
+        L = self.layers[i]
+        if L.dx_acc:
+            self.k.accumulate(self.layers[L.src_i].dy, L.dx)
+        for j, buf in L.cat_acc:
+            self.k.accumulate(self.layers[j].dy, buf)
+
+    def _chain_transfer(self, i: int) -> bool:
+        L = self.layers[i]
+        return i > 0 and L.src_i == i - 1 and self.layers[i - 1].g != L.g
+
     def _fused_down(self, i: int) -> bool:
         """conv ``i`` is a transition conv whose low-res data gradient the
         join folds into the source's gradient (no separate upsample)."""
@@ -328,6 +418,26 @@ class BurstStep:
         mask = L.x if sp.in_relu else None
         if sp.kind == "add":
             return                      # main path: identity (conv2.dy is L.dy)
+        if sp.kind == "concat":
+            self.k.concat_bwd(L.dy, list(L.cat_dst))
+            return
+        if sp.kind == "conv1x1":
+            P = L.b * sp.hw * sp.hw
+            x2 = (L.xs if sp.down else L.x).reshape(P, sp.cin)
+            dy2, w2 = L.dy.view(P, sp.cout), L.w.view(sp.cout, sp.cin)
+            self.k.linear_wgrad(x2, dy2, L.dw.view(sp.cout, sp.cin), L.dbias, ws=self.ws)
+            if L.src_i >= 0:
+                dxt = L.dxs if sp.down else L.dx
+                self.k.linear_dgrad(dy2, w2, x2 if sp.in_relu else None, dxt.view(P, sp.cin),
+                                    ws=self.ws)
+                if sp.down:
+                    self._sub_bwd(L)
+            return
+        if sp.kind == "pool3":
+            self.k.maxpool3x3_bwd_idx(L.idx, L.dy, L.dxs if sp.down else L.dx)
+            if sp.down:
+                self._sub_bwd(L)
+            return
         if sp.kind == "gap":
             self.k.global_avgpool_bwd(L.dy, mask, L.dx)
         elif sp.kind == "conv" and sp.down:
@@ -335,7 +445,7 @@ class BurstStep:
             self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
                                  **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
             if not self._fused_down(i):
-                self.k.subsample2_bwd(L.dxs, L.dx)
+                self._sub_bwd(L)
         elif sp.kind == "conv":
             self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
             if i > 0:
@@ -380,7 +490,7 @@ class BurstStep:
         prog = []
         n = len(self.layers)
         for i in range(n):
-            if i and self.layers[i - 1].g != self.layers[i].g:
+            if self._chain_transfer(i):
                 prog.append((("transfer", i, "fwd"), lambda i=i: self._reshard(i, False)))
             if self.layers[i].join == "reshard":
                 prog.append((("transfer", i, "skip_fwd"),
@@ -392,7 +502,9 @@ class BurstStep:
         for i in reversed(range(n)):
             if self.layers[i].active and self.layers[i].spec.kind != "add":
                 prog.append((("compute", i, "bwd"), lambda i=i: self._bwd(i)))
-            if i and self.layers[i - 1].g != self.layers[i].g:
+                if self.layers[i].dx_acc or self.layers[i].cat_acc:
+                    prog.append((("compute", i, "fanin"), lambda i=i: self._fanin(i)))
+            if self._chain_transfer(i):
                 prog.append((("transfer", i, "bwd"), lambda i=i: self._reshard(i, True)))
             if i in self.join_after:
                 # the join's backward = its shortcut gradient, after conv1's

@@ -26,7 +26,7 @@ from .graph import CompGraph
 @dataclass(frozen=True)
 class LayerSpec:
     name: str
-    kind: str            # conv | pool | dense | add (residual join) | gap (global avg pool)
+    kind: str            # conv | conv1x1 | pool | pool3 | dense | add | gap | concat
     cin: int             # channels (conv/pool/add/gap) or input features (dense)
     cout: int
     hw: int              # spatial size the layer computes at (pool: input); 0 for dense
@@ -36,6 +36,9 @@ class LayerSpec:
     skip: Optional[str] = None   # add: the skip (shortcut) source layer
     skip_c: int = 0      # add: channels of the skip source (<= cin, zero-padded)
     skip_down: bool = False      # add: skip source is 2hw x 2hw (subsampled)
+    src: Optional[str] = None    # input layer (None: the previous layer)
+    srcs: tuple = ()             # concat: the joined layers, in channel order
+    ihw: int = 0                 # down: input size when not 2*hw (2*hw+1: odd pixels kept)
 
     @property
     def out_hw(self) -> int:
@@ -43,7 +46,14 @@ class LayerSpec:
 
     @property
     def in_hw(self) -> int:
-        return 2 * self.hw if self.down else self.hw
+        if not self.down:
+            return self.hw
+        return self.ihw or 2 * self.hw
+
+    @property
+    def sub_off(self) -> int:
+        """Offset of the stride-2 subsample of a down layer (0 or 1)."""
+        return self.in_hw - 2 * self.hw
 
     def in_elems(self) -> int:
         """Input floats per sample."""
@@ -67,6 +77,8 @@ class LayerSpec:
     def param_shapes(self) -> Optional[tuple[tuple[int, ...], tuple[int, ...]]]:
         if self.kind == "conv":
             return (self.cout, 3, 3, self.cin), (self.cout,)
+        if self.kind == "conv1x1":
+            return (self.cout, 1, 1, self.cin), (self.cout,)
         if self.kind == "dense":
             return (self.cout, self.cin), (self.cout,)
         return None
@@ -79,6 +91,8 @@ class LayerSpec:
         """Algorithmic fwd FLOPs per sample (2 per MAC; bias/ReLU excluded)."""
         if self.kind == "conv":
             return 2 * 9 * self.cin * self.cout * self.hw * self.hw
+        if self.kind == "conv1x1":
+            return 2 * self.cin * self.cout * self.hw * self.hw
         if self.kind == "dense":
             return 2 * self.cin * self.cout
         return 0
@@ -215,8 +229,76 @@ def wideresnet_net(graph: CompGraph) -> NetSpec:
     return NetSpec("wrn", input_hw, 3, specs[-1].cout, tuple(specs))
 
 
+INCEPTION_CH, INCEPTION_HALF = 64, 32     # synth.py:172-226: stem / tower widths
+
+
+def inception_net(graph: CompGraph) -> NetSpec:
+    """Executable four-tower net behind the reference's ``inception_like``
+    family (synth.py:172-226).  The family rescales conv parameters to a
+    24 M budget, so channels come from its own constants (stem 64, towers
+    32, concat 4 x 32) and resolutions from the activation bytes (35 -> 17
+    -> 8).  Builder decisions: 3x3 convs and the ``_1x1`` convs (run as
+    pixel-batched dense ops) carry a ReLU; ``stem_pool`` and each module's
+    ``pool_proj`` are 3x3 / stride-1 max pools, the latter over the first 32
+    channels of the module input (a parameter-free projection); where the
+    resolution drops, each tower's first layer reads a stride-2 subsample
+    of the module input keeping the odd pixels (35 -> 17 -> 8); the
+    classifier is dense on the NHWC-flattened last concat (8*8*128 -> 1000)."""
+    real = [l for l in graph.layers if not l.is_virtual]
+    ids = {l.id for l in real}
+    by_id = {l.id: l for l in real}
+    c_of: dict[int, int] = {}
+    hw_of: dict[int, int] = {}
+    specs = []
+    input_hw = 0
+    for l in real:
+        preds = [p for p in l.predecessors if p in ids]
+        src = by_id[preds[0]] if preds else None
+        tower = l.name.startswith("m")
+        if l.kind in ("conv", "pool"):
+            cout = INCEPTION_HALF if tower else (INCEPTION_CH if l.kind == "conv" or src is None
+                                                  else c_of[src.id])
+            hw = math.isqrt(l.activation_bytes_per_sample // (4 * cout))
+            if cout * hw * hw * 4 != l.activation_bytes_per_sample:
+                raise GraphFormatError(f"{l.name}: activation bytes do not fit {cout} channels")
+            cin = c_of[src.id] if src else 3
+            ihw = hw_of[src.id] if src else hw
+            if not src:
+                input_hw = hw
+            if ihw not in (hw, 2 * hw, 2 * hw + 1):
+                raise GraphFormatError(f"{l.name}: input {ihw} -> {hw} is not 1x or /2")
+            down = ihw != hw
+            if l.kind == "conv":
+                kind = "conv1x1" if l.name.endswith("_1x1") else "conv"
+                specs.append(LayerSpec(l.name, kind, cin, cout, hw, True, src is not None,
+                                       down=down, src=src.name if src else None,
+                                       ihw=ihw if down else 0))
+            else:
+                if cout > cin:
+                    raise GraphFormatError(f"{l.name}: pool projects {cin} -> {cout}")
+                specs.append(LayerSpec(l.name, "pool3", cin, cout, hw, False, False, down=down,
+                                       src=src.name, ihw=ihw if down else 0))
+        elif l.kind == "concat":
+            hws = {hw_of[p] for p in preds}
+            if len(hws) != 1 or not 1 <= len(preds) <= 4:
+                raise GraphFormatError(f"{l.name}: concat inputs differ in size")
+            cout = sum(c_of[p] for p in preds)
+            hw = hws.pop()
+            specs.append(LayerSpec(l.name, "concat", cout, cout, hw, False, False,
+                                   srcs=tuple(by_id[p].name for p in preds)))
+        elif l.kind == "dense":
+            cin = c_of[src.id] * hw_of[src.id] ** 2
+            cout = l.activation_bytes_per_sample // 4
+            specs.append(LayerSpec(l.name, "dense", cin, cout, 0, False, True, src=src.name))
+            hw = 1
+        else:
+            raise GraphFormatError(f"{l.name}: kind {l.kind!r} not executable")
+        c_of[l.id], hw_of[l.id] = cout, hw
+    return NetSpec("inception", input_hw, 3, specs[-1].cout, tuple(specs))
+
+
 _REGISTRY = {"vgg_like": lambda g: vgg16(), "custom": mlp_for_chain,
-             "wideresnet_like": wideresnet_net}
+             "wideresnet_like": wideresnet_net, "inception_like": inception_net}
 
 
 def net_for_graph(graph: CompGraph) -> NetSpec:
@@ -233,8 +315,9 @@ def net_for_graph(graph: CompGraph) -> NetSpec:
 
 
 def init_params(net: NetSpec, seed: int = 0) -> dict[str, tuple[torch.Tensor, torch.Tensor]]:
-    """torchvision-style init on CPU (kaiming_normal fan_out/relu for convs,
-    N(0, 0.01) for dense, zero bias), deterministic in ``seed``."""
+    """torchvision-style init on CPU (kaiming_normal fan_out/relu for convs --
+    fan_in for the four-tower net -- N(0, 0.01) for dense, zero bias),
+    deterministic in ``seed``."""
     gen = torch.Generator().manual_seed(seed)
     out = {}
     # residual nets have no normalisation layers: the last conv of each
@@ -242,12 +325,18 @@ def init_params(net: NetSpec, seed: int = 0) -> dict[str, tuple[torch.Tensor, to
     # so the post-activation sum stays O(1) over all diamonds (Fixup-style;
     # unscaled, 34 diamonds overflow fp32 in the forward pass)
     blocks = sum(1 for l in net.layers if l.kind == "add")
+    # four-tower nets narrow 128 -> 32 channels in their 1x1 towers: fan-out
+    # init would grow the forward variance ~4x per module (fp32 logits in
+    # the thousands after 14 modules), so they use fan-in (the forward-
+    # preserving Kaiming mode)
+    fan_in = any(l.kind == "concat" for l in net.layers)
     for l in net.layers:
         ps = l.param_shapes()
         if ps is None:
             continue
-        if l.kind == "conv":
-            std = math.sqrt(2.0 / (l.cout * 9))
+        if l.kind in ("conv", "conv1x1"):
+            k = 9 if l.kind == "conv" else 1
+            std = math.sqrt(2.0 / ((l.cin if fan_in else l.cout) * k))
             if blocks and not l.relu:
                 std /= math.sqrt(blocks)
         else:

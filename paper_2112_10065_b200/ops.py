@@ -68,6 +68,18 @@ _SIGS = {
     "bpx_subsample2_bwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
                            + [ctypes.c_void_p]),
     "bpx_accumulate": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_maxpool3x3_fwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 5
+                               + [ctypes.c_void_p]),
+    "bpx_maxpool3x3_bwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 5
+                               + [ctypes.c_void_p]),
+    "bpx_concat_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                      _c_float_p, ctypes.c_longlong, ctypes.c_void_p]),
+    "bpx_concat_bwd": (ctypes.c_int, [_c_float_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p]),
+    "bpx_subsample_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 7
+                          + [ctypes.c_void_p]),
+    "bpx_subsample_bwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 7
+                          + [ctypes.c_void_p]),
     "bpx_global_avgpool_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
                                + [ctypes.c_void_p]),
     "bpx_global_avgpool_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
@@ -345,6 +357,70 @@ def accumulate(dst, src):
         raise KernelError("accumulate: size mismatch")
     _check(lib.bpx_accumulate(_ptr(dst), _ptr(src), dst.numel(), _stream()), "bpx_accumulate")
     return dst
+
+
+def maxpool3x3_fwd_idx(x, y, idx):
+    """3x3 / stride-1 / pad-1 max pool over the first y.shape[3] channels of x."""
+    lib = load_library()
+    _f32(x, y)
+    n, h, w, c = x.shape
+    _check(lib.bpx_maxpool3x3_fwd_idx(_ptr(x), _ptr(y), _ptr(idx), n, h, w, c, y.shape[3],
+                                      _stream()), "bpx_maxpool3x3_fwd_idx")
+    return y
+
+
+def maxpool3x3_bwd_idx(idx, dy, dx):
+    lib = load_library()
+    _f32(dy, dx)
+    n, h, w, c = dx.shape
+    _check(lib.bpx_maxpool3x3_bwd_idx(_ptr(idx), _ptr(dy), _ptr(dx), n, h, w, c, dy.shape[3],
+                                      _stream()), "bpx_maxpool3x3_bwd_idx")
+    return dx
+
+
+def _part_arrays(parts):
+    k = len(parts)
+    ptrs = (ctypes.c_void_p * 4)(*[_ptr(t) for t in parts] + [None] * (4 - k))
+    cs = (ctypes.c_int * 4)(*[t.shape[-1] for t in parts] + [0] * (4 - k))
+    return ptrs, cs, k
+
+
+def concat_fwd(parts, y):
+    """y[..., :] = cat(parts, channel dim) (NHWC, same pixel count)."""
+    lib = load_library()
+    _f32(y, *parts)
+    ptrs, cs, k = _part_arrays(parts)
+    npix = y.numel() // y.shape[-1]
+    _check(lib.bpx_concat_fwd(ptrs, cs, k, _ptr(y), npix, _stream()), "bpx_concat_fwd")
+    return y
+
+
+def concat_bwd(dy, parts):
+    lib = load_library()
+    _f32(dy, *parts)
+    ptrs, cs, k = _part_arrays(parts)
+    npix = dy.numel() // dy.shape[-1]
+    _check(lib.bpx_concat_bwd(_ptr(dy), ptrs, cs, k, npix, _stream()), "bpx_concat_bwd")
+    return parts
+
+
+def subsample_fwd(x, y, off):
+    """y[:, i, j] = x[:, 2i+off, 2j+off]."""
+    lib = load_library()
+    _f32(x, y)
+    n, hin, win, c = x.shape
+    _check(lib.bpx_subsample_fwd(_ptr(x), _ptr(y), n, hin, win, y.shape[1], y.shape[2], c, off,
+                                 _stream()), "bpx_subsample_fwd")
+    return y
+
+
+def subsample_bwd(dy, dx, off):
+    lib = load_library()
+    _f32(dy, dx)
+    n, hin, win, c = dx.shape
+    _check(lib.bpx_subsample_bwd(_ptr(dy), _ptr(dx), n, hin, win, dy.shape[1], dy.shape[2], c,
+                                 off, _stream()), "bpx_subsample_bwd")
+    return dx
 
 
 def global_avgpool_fwd(x, y):

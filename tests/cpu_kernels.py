@@ -177,3 +177,64 @@ def subsample2_bwd(dy, dx):
 def accumulate(dst, src):
     dst.copy_(dst.double() + src.double().reshape(dst.shape))
     return dst
+
+
+# ---- four-tower (inception_like) elements: bpx_maxpool3x3_*, bpx_concat_*,
+# bpx_subsample_*
+def maxpool3x3_fwd_idx(x, y, idx):
+    cs = y.shape[3]
+    xs = _nchw(x[..., :cs])
+    o, ind = F.max_pool2d(xs, 3, 1, 1, return_indices=True)
+    y.copy_(_nhwc(o))
+    # flat index in the (h, w) plane -> window position (dy+1)*3 + (dx+1)
+    h, w = x.shape[1], x.shape[2]
+    oh = torch.arange(h).view(1, 1, h, 1)
+    ow = torch.arange(w).view(1, 1, 1, w)
+    ih, iw = ind // w, ind % w
+    idx.copy_(_nhwc((ih - oh + 1) * 3 + (iw - ow + 1)).to(torch.uint8))
+    return y
+
+
+def maxpool3x3_bwd_idx(idx, dy, dx):
+    n, h, w, c = dx.shape
+    cs = dy.shape[3]
+    g = torch.zeros((n, h, w, c), dtype=torch.float64)
+    k = idx.long()
+    for t in range(9):
+        ddy, ddx = t // 3 - 1, t % 3 - 1
+        sel = (k == t).double() * dy.double()        # outputs whose max sits at tap t
+        for oh in range(h):
+            ih = oh + ddy
+            if not 0 <= ih < h:
+                continue
+            lo, hi = max(0, -ddx), min(w, w - ddx)
+            g[:, ih, lo + ddx:hi + ddx, :cs] += sel[:, oh, lo:hi, :]
+    dx.copy_(g)
+    return dx
+
+
+def concat_fwd(parts, y):
+    y.copy_(torch.cat([p.double() for p in parts], dim=-1))
+    return y
+
+
+def concat_bwd(dy, parts):
+    o = 0
+    for p in parts:
+        c = p.shape[-1]
+        p.copy_(dy[..., o:o + c])
+        o += c
+    return parts
+
+
+def subsample_fwd(x, y, off):
+    h, w = y.shape[1], y.shape[2]
+    y.copy_(x[:, off:off + 2 * h:2, off:off + 2 * w:2, :])
+    return y
+
+
+def subsample_bwd(dy, dx, off):
+    h, w = dy.shape[1], dy.shape[2]
+    dx.zero_()
+    dx[:, off:off + 2 * h:2, off:off + 2 * w:2, :] = dy
+    return dx

@@ -69,3 +69,17 @@ def test_argument_validation_without_gpu(lib):
     assert lib.bpx_conv3x3_fwd(None, None, None, None, 1, 8, 8, 8, 8, 1, None, 0,
                                None) == 1
     assert lib.bpx_reshard_pull(None, None, None, None, None, 65, None) == 1
+
+
+@pytest.mark.parametrize("n,h,cin,cout", [(2, 17, 32, 32), (2, 8, 32, 32), (1, 5, 4, 4),
+                                          (2, 35, 128, 32), (2, 9, 16, 16), (3, 7, 3, 64),
+                                          (2, 224, 64, 64), (0, 4, 8, 8)])
+def test_workspace_queries_any_shape(lib, n, h, cin, cout):
+    """Workspace queries are host-only and must answer for every shape the
+    dispatch may see (the first engine's planner may not apply to it)."""
+    for f in ("bpx_conv3x3_fwd_workspace", "bpx_conv3x3_dgrad_workspace",
+              "bpx_conv3x3_wgrad_workspace"):
+        assert getattr(lib, f)(n, h, h, cin, cout) >= 0
+    for f in ("bpx_linear_fwd_workspace", "bpx_linear_dgrad_workspace",
+              "bpx_linear_wgrad_workspace"):
+        assert getattr(lib, f)(n * h * h, cin, cout) >= 0

@@ -1,7 +1,10 @@
-"""One-B200 timing of the residual net behind wideresnet_like (C3 shape:
-B=32, 34 diamonds at 100/50/25) through the executor:
-captured step, CUDA events, samples/s and TFLOP/s of the algorithmic work.
-usage: python tools/wrn_bench.py [--batch 32] [--steps 5] [--warmup 3]"""
+"""One-B200 timing of the branch/join nets through the executor: the
+residual net behind wideresnet_like (C3 shape: B=32, 34 diamonds at
+100/50/25) or the four-tower net behind inception_like (C4 foreground: B=32,
+14 modules at 35/17/8), SURVEY.md §8d.  Captured step, CUDA events,
+samples/s and TFLOP/s of the algorithmic work.
+usage: python tools/wrn_bench.py [--family wideresnet_like|inception_like]
+       [--batch 32] [--steps 5] [--warmup 3]"""
 import argparse
 import json
 import os
@@ -18,11 +21,13 @@ from paper_2112_10065_b200.planner import plan                       # noqa: E40
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--family", default="wideresnet_like",
+                    choices=("wideresnet_like", "inception_like"))
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
-    g = synth.wideresnet_like(seed=0, global_batch=a.batch)
+    g = getattr(synth, a.family)(seed=0, global_batch=a.batch)
     p = plan(g, 1, 2.0)
     st = BurstStep(p, g, seed=0, lr=1e-3)
     x, y = synthetic_batch(st.net, a.batch, seed=0)
@@ -39,7 +44,7 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     flops = st.net.train_flops_per_sample() * a.batch
-    print(json.dumps({"workload": f"wideresnet_like B={a.batch} (residual net, "
+    print(json.dumps({"workload": f"{a.family} B={a.batch} ({st.net.name} net, "
                                   f"{len(st.net.layers)} layers) on 1 GPU",
                       "samples_per_s": a.batch / (ms / 1e3), "ms_per_step": ms,
                       "tflops": flops / (ms / 1e3) / 1e12, "loss": st.loss()}))
