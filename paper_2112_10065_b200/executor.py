@@ -153,25 +153,13 @@ class BurstStep:
         # several consumers gets its gradient from all of them: the consumer
         # whose backward runs first (the highest index) writes the source's
         # dy, the others write private buffers that are accumulated into it.
-        consumers: dict[int, list] = {}
+        consumers = branch_topology([L.spec for L in self.layers], [L.g for L in self.layers])
         for i, L in enumerate(self.layers):
             sp = L.spec
             if sp.kind == "concat":
                 L.srcs_i = tuple(names[n] for n in sp.srcs)
-                edges = L.srcs_i
             else:
                 L.src_i = names[sp.src] if sp.src is not None else i - 1
-                edges = (L.src_i,) if L.src_i >= 0 else ()
-            for j in edges:
-                if (j != i - 1 or sp.kind == "concat") and self.layers[j].g != L.g:
-                    raise UnsupportedTopologyError(
-                        f"{sp.name}: branch edge from {self.layers[j].spec.name} crosses "
-                        f"GPU counts {self.layers[j].g} -> {L.g}")
-                consumers.setdefault(j, []).append(i)
-        for j, cs in consumers.items():
-            if len(cs) > 1 and any(self.layers[c].g != self.layers[j].g for c in cs):
-                raise UnsupportedTopologyError(
-                    f"{self.layers[j].spec.name}: fan-out across GPU counts")
 
         ws_need = 0
         for i, L in enumerate(self.layers):
@@ -612,6 +600,34 @@ class BurstStep:
     def params(self) -> dict:
         return {L.spec.name: (L.w, L.bias) for L in self.layers
                 if L.active and L.w is not None}
+
+
+def branch_topology(specs, gs) -> dict:
+    """Input edges of every layer -> {source index: [consumer indices]}.
+
+    Raises UnsupportedTopologyError unless every branch edge (an input that
+    is not the previous layer, or a concat part) and every fan-out stays on
+    one GPU count; chain edges may change g (they reshard).  The
+    reference's own plans for the branch/join families (C3, C4 at G=8,
+    amp 2..8) satisfy this (tests/test_inception_executor.py)."""
+    names = {sp.name: i for i, sp in enumerate(specs)}
+    consumers: dict[int, list] = {}
+    for i, sp in enumerate(specs):
+        if sp.kind == "concat":
+            edges = tuple(names[n] for n in sp.srcs)
+        else:
+            j = names[sp.src] if sp.src is not None else i - 1
+            edges = (j,) if j >= 0 else ()
+        for j in edges:
+            if (j != i - 1 or sp.kind == "concat") and gs[j] != gs[i]:
+                raise UnsupportedTopologyError(
+                    f"{sp.name}: branch edge from {specs[j].name} crosses GPU counts "
+                    f"{gs[j]} -> {gs[i]}")
+            consumers.setdefault(j, []).append(i)
+    for j, cs in consumers.items():
+        if len(cs) > 1 and any(gs[c] != gs[j] for c in cs):
+            raise UnsupportedTopologyError(f"{specs[j].name}: fan-out across GPU counts")
+    return consumers
 
 
 def _pad4(n: int) -> int:

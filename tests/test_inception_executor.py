@@ -84,3 +84,85 @@ def test_tiny_inception_step_matches_fp64_oracle():
     for name, (dw, db) in grads.items():
         assert vgg_ref.normwise_rel(dw, ref[name][0]) < 1e-6, name
         assert vgg_ref.normwise_rel(db, ref[name][1]) < 1e-6, name
+
+
+def test_reference_plans_of_branch_join_families_are_executable():
+    """The reference planner's plans for C3 (wideresnet_like) and C4
+    (inception_like) at G=8 keep branch edges and fan-outs on one GPU
+    count, so the executor takes them as they are."""
+    from paper_2112_10065_b200.executor import branch_topology
+    from paper_2112_10065_b200.planner import plan
+    for fam, amps in (("inception_like", (2.0, 4.0, 8.0)), ("wideresnet_like", (2.0, 4.0))):
+        g = getattr(synth, fam)(seed=0, global_batch=32)
+        net = net_for_graph(g)
+        for amp in amps:
+            p = plan(g, 8, amp)
+            gs = [gg for lid, gg in p.assignments if not g.layer(lid).is_virtual]
+            branch_topology(net.layers, gs)          # raises if not executable
+
+
+# world 2, ragged B=5: the amp-2 plan's shape (stem on 2 GPUs, modules on 1)
+# plus the classifier back on 2 -- chain transfers into and out of the
+# branch/join section
+def _worker(rank, port, q):
+    try:
+        import os
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.set_num_threads(1)
+        import cpu_kernels
+        from oracle import vgg_ref
+        from paper_2112_10065_b200.comm import TorchComm
+        from paper_2112_10065_b200.executor import BurstStep
+        B = 5
+        graph = tiny_inception_graph(B, modules=2)
+        net = net_for_graph(graph)
+        ids = [l.id for l in graph.layers if not l.is_virtual]
+        gs = [2 if (l.name.startswith("stem") and l.name != "stem_conv5") or l.name == "fc"
+              else 1 for l in net.layers]
+        params = init_params(net, seed=5)
+        x, y = synthetic_batch(net, B, seed=6)
+        p = TrainingPlan(graph.name, 2, 2.0, B, tuple(zip(ids, gs)), 0.0, (), ())
+        st = BurstStep(p, graph, comm=TorchComm(rank, 2, set(gs)), params=params,
+                       kernels=cpu_kernels, lr=0.0)
+        st.load(x, y)
+        st.forward_backward()
+        st.sync_and_update()
+        res = {"loss": st.loss()}
+        if rank == 0:
+            ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+            res["ref_loss"] = ref_loss
+            res["errs"] = {n: max(vgg_ref.normwise_rel(dw, ref[n][0]),
+                                  vgg_ref.normwise_rel(db, ref[n][1]))
+                           for n, (dw, db) in st.grads().items()}
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+def test_world2_four_tower_net_matches_oracle():
+    import socket
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ps = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert "error" not in out[r], out[r].get("error")
+    r0 = out[0]
+    assert abs(r0["loss"] - r0["ref_loss"]) <= 1e-6 * abs(r0["ref_loss"])
+    assert len(r0["errs"]) == 3 + 2 * 6 + 1
+    for name, e in r0["errs"].items():
+        assert e < 1e-6, (name, e)
