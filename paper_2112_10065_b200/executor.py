@@ -575,7 +575,11 @@ class BurstStep:
         ops so background work can be held off around them).  Returns
         [(first_index, keys, graph)]."""
         prog = self.program()
+        # the eager warm-up must not leave its own op events behind: per-op
+        # timing would add the warm-up's durations to every replay's
+        record, self.op_events = self.op_events, None
         self._warm(prog, warmup)
+        self.op_events = record
         bounds = sorted({0, len(prog)} | {c for c in cut if 0 < c < len(prog)})
         segs = []
         for a, b in zip(bounds, bounds[1:]):

@@ -74,3 +74,19 @@ def test_pareto_sweep_rows_match_reference_schema():
     assert abs(part["fg_speedup"] - 1.0) < 0.25
     tab = pareto_to_table(rows).splitlines()
     assert tab[0].split("\t") == list(PARETO_HEADER) and len(tab) == 3
+
+
+@pytest.mark.timeout(600)
+def test_calibration_report_prices_the_program_with_measurements():
+    """§8f-4: the measurement-priced simulation of the op program lands
+    near the measured iteration (the unmodeled loss + SGD time aside); the
+    reference's synthetic A100-class profile does not."""
+    from paper_2112_10065_b200.simulate import calibration_report
+    g = synth.vgg_like(seed=0, global_batch=8)
+    p = plan(g, 1, 2.0)
+    rep = calibration_report(p, g, 1, SimConfig(warmup_iterations=1), 4)
+    meas = rep["measured_iteration_us"]
+    assert meas > 0 and rep["calibrated_iteration_us"] > 0
+    unmodeled = sum(rep["unmodeled_us"].values())
+    assert abs(rep["calibrated_iteration_us"] + unmodeled - meas) < 0.25 * meas, rep
+    assert all(o["measured_us"] > 0 for o in rep["ops"] if ".compute." in o["op"])
