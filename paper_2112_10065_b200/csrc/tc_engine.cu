@@ -532,7 +532,8 @@ bool tc_conv_wgrad_ok(int n, int h, int w, int cin, int cout) {
   return cin % 8 == 0 && cout % 4 == 0;
 }
 bool tc_linear_ok(int b, int in, int out) {
-  return in % 4 == 0 && out % 4 == 0 && b <= 256;
+  // the [M][b] partials are written as float4 rows: b % 4 == 0
+  return in % 4 == 0 && out % 4 == 0 && b <= 256 && b % 4 == 0;
 }
 
 size_t tc_conv_fwd_ws(int, int, int, int, int) { return 0; }

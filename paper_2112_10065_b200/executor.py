@@ -136,12 +136,12 @@ class BurstStep:
                 continue
             L.skip_i = names[L.spec.skip]
             c1 = L.skip_i + 1
-            if c1 >= i or self.layers[c1].spec.kind != "conv":
+            if c1 >= i or self.layers[c1].spec.kind not in ("conv", "conv1x1"):
                 raise GraphFormatError(f"{L.spec.name}: shortcut does not span a conv chain")
             S, C1 = self.layers[L.skip_i], self.layers[c1]
             if S.g != L.g:
                 L.join = "reshard"
-            elif C1.spec.down and C1.g == S.g:
+            elif C1.spec.down and C1.spec.kind == "conv" and C1.g == S.g:
                 L.join = "fused"
             else:
                 L.join = "direct"

@@ -184,12 +184,13 @@ def wideresnet_net(graph: CompGraph) -> NetSpec:
         preds = [p for p in l.predecessors if p in ids]
         succs = [by_id[s] for s in l.successors if s in ids]
         if l.kind == "conv":
+            k = 1 if l.name.endswith("_1x1") else 9      # bottleneck 1x1 convs (resnet50_like)
             cin = out_c[preds[0]] if preds else 3
-            cout = l.params_bytes // 4 // (9 * cin)
+            cout = l.params_bytes // 4 // (k * cin)
             hw = math.isqrt(l.activation_bytes_per_sample // (4 * cout))
-            if 9 * cin * cout * 4 != l.params_bytes or cout * hw * hw * 4 != \
+            if k * cin * cout * 4 != l.params_bytes or cout * hw * hw * 4 != \
                     l.activation_bytes_per_sample:
-                raise GraphFormatError(f"{l.name}: not a 3x3 conv shape")
+                raise GraphFormatError(f"{l.name}: not a {'1x1' if k == 1 else '3x3'} conv shape")
             if not preds:
                 input_hw = hw
             ihw = out_hw[preds[0]] if preds else hw
@@ -197,12 +198,15 @@ def wideresnet_net(graph: CompGraph) -> NetSpec:
                 raise GraphFormatError(f"{l.name}: input {ihw} -> {hw} is not 1x or /2")
             # a conv feeding only a join is the block's second conv: no ReLU
             relu = not (len(succs) == 1 and succs[0].kind == "add")
-            specs.append(LayerSpec(l.name, "conv", cin, cout, hw, relu,
+            if k == 1 and ihw != hw:
+                raise GraphFormatError(f"{l.name}: strided 1x1 convs are not built")
+            specs.append(LayerSpec(l.name, "conv" if k == 9 else "conv1x1", cin, cout, hw, relu,
                                    bool(preds) and relu_out[preds[0]], down=ihw == 2 * hw))
             out_c[l.id], out_hw[l.id], relu_out[l.id] = cout, hw, relu
         elif l.kind == "add":
             main = [p for p in preds if by_id[p].kind == "conv"
-                    and len([s for s in by_id[p].successors if s in ids]) == 1]
+                    and len([s for s in by_id[p].successors if s in ids]) == 1
+                    and p != preds[-1]]
             if len(preds) != 2 or len(main) != 1:
                 raise GraphFormatError(f"{l.name}: expected (conv2, shortcut) inputs")
             m = main[0]
@@ -298,7 +302,8 @@ def inception_net(graph: CompGraph) -> NetSpec:
 
 
 _REGISTRY = {"vgg_like": lambda g: vgg16(), "custom": mlp_for_chain,
-             "wideresnet_like": wideresnet_net, "inception_like": inception_net}
+             "wideresnet_like": wideresnet_net, "inception_like": inception_net,
+             "resnet50_like": wideresnet_net}
 
 
 def net_for_graph(graph: CompGraph) -> NetSpec:

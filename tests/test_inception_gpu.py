@@ -97,7 +97,8 @@ def test_four_tower_net_step_matches_fp64():
 
 
 @pytest.mark.parametrize("b,fin,fout", [(4000, 128, 32), (2452, 64, 32), (39200, 128, 32),
-                                        (578, 64, 32), (1000, 128, 32)])
+                                        (578, 64, 32), (1000, 128, 32), (98, 2048, 512),
+                                        (50, 64, 32)])
 def test_pixel_batched_dense(b, fin, fout):
     """The 1x1 convs run as dense ops with batch = pixels (tensor-core engine
     for the forward); parity with fp64 like the other dense shapes."""

