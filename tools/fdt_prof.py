@@ -16,9 +16,14 @@ for name in ("conv1_2", "conv2_2", "conv3_2", "conv4_2", "conv5_1"):
     w = torch.randn(l.param_shapes()[0], device="cuda") * 0.02
     bias = torch.zeros(l.cout, device="cuda")
     y = torch.empty(l.out_shape(b), device="cuda")
-    ops.conv3x3_fwd(x, w, bias, y, True, ws)
-    torch.cuda.synchronize()
-    out = (ctypes.c_ulonglong * 6)()
-    f(out)
-    tot, acc, a, bb, iss, n = list(out)
-    print(f"{name}: stages/CTA-thread {n/148:.0f}  per stage cycles: total {tot/n:.0f}  wait_acc {acc/n:.0f}  wait_A {a/n:.0f}  wait_B {bb/n:.0f}  issue {iss/n:.0f}")
+    for op in ("fwd", "dgrad"):
+        if op == "fwd":
+            ops.conv3x3_fwd(x, w, bias, y, True, ws)
+        else:
+            dy = torch.randn(l.out_shape(b), device="cuda")
+            ops.conv3x3_dgrad(dy, w, x, torch.empty_like(x), ws)
+        torch.cuda.synchronize()
+        out = (ctypes.c_ulonglong * 6)()
+        f(out)
+        tot, acc, a, bb, iss, n = list(out)
+        print(f"{name} {op}: stages/CTA-thread {n/148:.0f}  per stage cycles: total {tot/n:.0f}  wait_acc {acc/n:.0f}  wait_A {a/n:.0f}  wait_B {bb/n:.0f}  issue {iss/n:.0f}")
