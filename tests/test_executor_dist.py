@@ -9,6 +9,7 @@ weight gradient against the single-process fp64 oracle."""
 import os
 import socket
 
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -101,3 +102,69 @@ def test_burst_executor_world2_matches_oracle():
     assert len(r0["errs"]) == 16
     for name, e in r0["errs"].items():
         assert e < 1e-6, (name, e)                # fp32 buffers, fp64 compute
+
+
+def _worker_n(rank, world, port, q, gs):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.set_num_threads(1)
+        from paper_2112_10065_b200.comm import TorchComm
+        from paper_2112_10065_b200.executor import BurstStep
+        import cpu_kernels
+        from oracle import vgg_ref
+        B4 = 11
+        net = tiny_vgg()
+        params = init_params(net, seed=11)
+        graph = synth.vgg_like(seed=0, global_batch=B4)
+        ids = [l.id for l in graph.layers if not l.is_virtual]
+        p = TrainingPlan("vgg_like", world, 2.0, B4, tuple(zip(ids, gs)), 0.0, (), ())
+        x, y = synthetic_batch(net, B4, seed=12)
+        st = BurstStep(p, graph, comm=TorchComm(rank, world, set(gs)), params=params, net=net,
+                       kernels=cpu_kernels, lr=0.0)
+        st.load(x, y)
+        st.forward_backward()
+        st.sync_and_update()
+        res = {"loss": st.loss()}
+        if rank == 0:
+            ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+            res["ref_loss"] = ref_loss
+            res["errs"] = {n: max(vgg_ref.normwise_rel(dw, ref[n][0]),
+                                  vgg_ref.normwise_rel(db, ref[n][1]))
+                           for n, (dw, db) in st.grads().items()}
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_real_plan_matches_oracle(world):
+    """The planner's own plan for VGG-16 at G=4 ([4]*14 + [1]*7) and G=8
+    (config C1: [8]*10 + [4]*4 + [1]*7, allreduce groups of 8 and 4) on that
+    many gloo ranks, ragged B=11 (ceil shards 2/2/.../1, empty shards)."""
+    from paper_2112_10065_b200.planner import plan
+    g = synth.vgg_like(seed=0, global_batch=32)
+    gs = [gg for lid, gg in plan(g, world, 2.0).assignments if not g.layer(lid).is_virtual]
+    assert len(set(gs)) >= 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ps = [ctx.Process(target=_worker_n, args=(r, world, port, q, gs)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert "error" not in out[r], out[r].get("error")
+    r0 = out[0]
+    assert abs(r0["loss"] - r0["ref_loss"]) <= 1e-6 * abs(r0["ref_loss"])
+    assert len(r0["errs"]) == 16
+    for name, e in r0["errs"].items():
+        assert e < 1e-6, (name, e)
