@@ -564,10 +564,7 @@ class BurstStep:
         self._warm(prog, warmup)
         if record:          # external events become record nodes in the graph
             self.op_events = []
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.run_ops(prog)
-        self.graph = g
+        self.graph = self._graph_or_eager(prog, None)
 
     def capture_segments(self, cut: set, warmup: int = 1, pool=None) -> list:
         """Capture the step as consecutive graphs, starting a new graph at
@@ -583,11 +580,27 @@ class BurstStep:
         bounds = sorted({0, len(prog)} | {c for c in cut if 0 < c < len(prog)})
         segs = []
         for a, b in zip(bounds, bounds[1:]):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, pool=pool):
-                self.run_ops(prog[a:b])
-            segs.append((a, [k for k, _ in prog[a:b]], g))
+            segs.append((a, [k for k, _ in prog[a:b]], self._graph_or_eager(prog[a:b], pool)))
         return segs
+
+    def _graph_or_eager(self, ops, pool):
+        """A CUDA graph of ``ops``; if capture fails (e.g. a communication
+        backend whose ops cannot be captured), the same ops replayed
+        eagerly -- identical results, more launch overhead -- with a
+        warning instead of a crash."""
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, pool=pool):
+                self.run_ops(ops)
+            return g
+        except Exception as exc:                      # pragma: no cover (multi-GPU only)
+            import sys
+            torch.cuda.synchronize()
+            if self.op_events is not None:
+                self.op_events.clear()
+            print(f"[bpx] CUDA-graph capture failed ({type(exc).__name__}: {exc}); "
+                  "replaying the op program eagerly", file=sys.stderr)
+            return _EagerReplay(self, ops)
 
     def loss(self) -> float:
         """Global mean loss (sum of shard partials over the last layer's g)."""
@@ -604,6 +617,16 @@ class BurstStep:
     def params(self) -> dict:
         return {L.spec.name: (L.w, L.bias) for L in self.layers
                 if L.active and L.w is not None}
+
+
+class _EagerReplay:
+    """Stands in for a captured CUDA graph: replay() runs the ops."""
+
+    def __init__(self, step: "BurstStep", ops):
+        self.step, self.ops = step, list(ops)
+
+    def replay(self) -> None:
+        self.step.run_ops(self.ops)
 
 
 def branch_topology(specs, gs) -> dict:
