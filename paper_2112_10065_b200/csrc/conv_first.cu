@@ -11,8 +11,13 @@
 //     tcgen05.st them;
 //   * one warp issues the 3xTF32 MMAs (B = the 64 x 32 weight tile, hi and
 //     lo, built once per CTA in shared memory, K-major 128-B swizzle);
-//   * drain warps add the bias, apply the ReLU and store 256-byte rows.
+//   * drain warps add the bias, apply the ReLU and write the tile into a
+//     double-buffered, 128-B-swizzled staging area; one thread stores it
+//     with two TMA tensor stores (32 channels x 128 pixels each) -- the
+//     128-pixel output tile is contiguous in y, and per-thread 256-byte row
+//     stores reached only ~2.7 TB/s.
 // One 32-K MMA chain per tile needs no chunk promotion.
+#include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "simt_api.h"
 
@@ -21,19 +26,25 @@ namespace c1 {
 using namespace tcx;
 
 constexpr int COUT = 64, R = 27, KP = 32;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 constexpr int NTHREADS = 9 * 32;       // warp 0 MMA, 1-4 gather, 5-8 drain
-constexpr int SMEM = 1024 + 2 * COUT * KP * 4 + 128;
+constexpr int STAGE_OUT = 128 * COUT * 4;      // one output tile (two 16 KB boxes)
+constexpr int SMEM = 1024 + 2 * COUT * KP * 4 + 2 * STAGE_OUT + 128;
 
 __global__ void __launch_bounds__(NTHREADS, 1)
 c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
-              const float* __restrict__ bias, float* __restrict__ y, int H, int W,
-              long long npix, int relu) {
+              const float* __restrict__ bias, const __grid_constant__ CUtensorMap ty, int H,
+              int W, long long npix, int relu) {
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   char* bh = smem;                        // 64 rows x 128 B, 128-B swizzle
   char* bl = smem + COUT * KP * 4;
-  uint64_t* aready = reinterpret_cast<uint64_t*>(bl + COUT * KP * 4);
+  char* ostage = bl + COUT * KP * 4;      // 2 x (2 boxes of 128 pixels x 128 B), swizzled
+  uint64_t* aready = reinterpret_cast<uint64_t*>(ostage + 2 * STAGE_OUT);
   uint64_t* dfull = aready + 2;
   uint64_t* tfree = dfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 2);
@@ -128,17 +139,22 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
     }
   } else {
     const int q = warp & 3, r = q * 32 + lane;
+    const int dtid = (warp - 5) * 32 + lane;          // 0..127 within the drain warps
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16);
     float bv[COUT];
 #pragma unroll
     for (int j = 0; j < COUT; ++j) bv[j] = bias ? __ldg(bias + j) : 0.f;
+    if (dtid == 0) tma_prefetch_desc(&ty);
     int it = 0;
     for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int b = it & 1;
+      char* st = ostage + b * STAGE_OUT;
+      if (it >= 2) {            // the store issued from this staging buffer 2 tiles ago
+        if (dtid == 0) bulk_wait_read<1>();
+        named_bar(1, 128);
+      }
       mbar_wait(&dfull[b], (it >> 1) & 1);
       tc_fence_after();
-      const long long p = t * 128 + r;
-      float* dst = y + p * COUT;
 #pragma unroll
       for (int j = 0; j < COUT; j += 8) {
         uint32_t rr[8];
@@ -150,15 +166,26 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
           const float s = __uint_as_float(rr[u]) + bv[j + u];
           o[u] = relu ? fmaxf(s, 0.f) : s;
         }
-        if (p < npix) {
-          *reinterpret_cast<float4*>(dst + j) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(dst + j + 4) = make_float4(o[4], o[5], o[6], o[7]);
-        }
+        // box j/32, row r, 16-B granule (j%32)/4 (+1), 128-B swizzle
+        char* row = st + (j >> 5) * (STAGE_OUT / 2) + r * 128;
+        const int g0 = (j & 31) >> 2;
+        *reinterpret_cast<float4*>(row + ((g0 ^ (r & 7)) << 4)) =
+            make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(row + (((g0 + 1) ^ (r & 7)) << 4)) =
+            make_float4(o[4], o[5], o[6], o[7]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tfree[b]);
+      fence_proxy_async();
+      named_bar(1, 128);
+      if (dtid == 0) {
+        tma_store_2d(&ty, 0, (int)(t * 128), st);
+        tma_store_2d(&ty, 32, (int)(t * 128), st + STAGE_OUT / 2);
+        bulk_commit();
+      }
     }
+    if (dtid == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -176,7 +203,19 @@ bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, floa
                          int h, int w_, int relu, cudaStream_t st) {
   const long long npix = (long long)n * h * w_;
   if (npix == 0) return launch_status(0);
-  if (!aligned16(y)) return BPX_ERR_UNSUPPORTED;
+  if (!aligned16(y) || npix > 0x7fffffffLL) return BPX_ERR_UNSUPPORTED;
+  CUtensorMap ty;                  // y as [pixels][64]: box 32 channels x 128 pixels
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)c1::COUT, (cuuint64_t)npix};
+    const cuuint64_t strides[1] = {(cuuint64_t)c1::COUT * 4};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode_tiled(&ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return BPX_ERR_UNSUPPORTED;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(c1::c1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -185,7 +224,7 @@ bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, floa
   }
   const long long tiles = (npix + 127) / 128;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, y, h, w_, npix, relu);
+  c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, ty, h, w_, npix, relu);
   return launch_status();
 }
 
