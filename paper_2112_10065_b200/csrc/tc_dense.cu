@@ -260,11 +260,13 @@ inline bool encode2d(CUtensorMap* m, const float* p, long long inner, long long 
 
 inline int nb_for(int batch) { return batch <= 16 ? 16 : 32; }   // M=128 MMAs take N % 16 == 0
 
-// split count: about four waves of CTAs on the SMs, at least 4 stages each
-inline void geometry(int M, int K, int& splits, int& kslice) {
+// split count: one wave of CTAs for the forward, two for the data gradient
+// (its four MN-major boxes per stage keep more CTAs busy), at least 4
+// stages each (B200 A/B at fc1/fc2, B = 4 and 32: 4 waves was 8-25 % slower)
+inline void geometry(int M, int K, bool dg, int& splits, int& kslice) {
   const int mt = cdiv(M, 128);
   const int kst = cdiv(K, BK);
-  int want = cdiv(4 * num_sms(), mt);
+  int want = dg ? cdiv(2 * num_sms(), mt) : num_sms() / mt;
   if (want > kst / 4) want = kst / 4;
   if (want < 1) want = 1;
   kslice = cdiv(kst, want) * BK;
@@ -289,7 +291,7 @@ bpx_status_t run(bool dg, const float* W, const float* act, int batch, int M, in
                  const float* bias, int relu, const float* mask, float* out, float* ws,
                  size_t ws_floats, cudaStream_t st) {
   int splits, kslice;
-  geometry(M, K, splits, kslice);
+  geometry(M, K, dg, splits, kslice);
   const int mt = cdiv(M, 128);
   const int nb = nb_for(batch);
   const size_t need = (size_t)batch * K + (size_t)splits * batch * M;
@@ -329,8 +331,8 @@ bool dtc_linear_ok(int b, int in, int out) {
 size_t dtc_linear_ws(int b, int in, int out) {
   if (!dtc_linear_ok(b, in, out)) return 0;
   int s1, k1, s2, k2;
-  dtc::geometry(out, in, s1, k1);           // fwd: M = out, K = in
-  dtc::geometry(in, out, s2, k2);           // dgrad: M = in, K = out
+  dtc::geometry(out, in, false, s1, k1);    // fwd: M = out, K = in
+  dtc::geometry(in, out, true, s2, k2);     // dgrad: M = in, K = out
   const size_t a = (size_t)b * in + (size_t)s1 * b * out;
   const size_t c = (size_t)b * out + (size_t)s2 * b * in;
   return ((a > c ? a : c) + 4) * sizeof(float);
