@@ -81,6 +81,7 @@ struct Cfg {
 };
 
 struct Geo {
+  const float* x;            // gather-A mode (9*Cin <= 32): the input itself
   int Cin, Cout, H, W;
   long long npix;
   int tiles, tps;            // 32-pixel tiles in total / per split
@@ -98,14 +99,23 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 // the B operand (TMA fill, lo pass, MMA reads).  The leader (rank 0) issues
 // the MMAs; its commits arrive on both CTAs' barriers (multicast); the
 // peer's converters and drains arrive on the leader's ready / hfree.
-template <int BN, bool PAIR>
+// GA (gather A; 9*Cin <= 32 rows, the first conv): the im2col rows are not
+// 32-channel TMA boxes.  Every TMEM lane quadrant q holds all 9*Cin rows but
+// only the pixels [16q, 16q+16) of each stage (its other columns stay zero,
+// stored once per slot), so four converter warps gather 16 pixels each
+// straight from x (L2-resident); the drain sums the four partial rows.
+template <int BN, bool PAIR, bool GA = false>
 __global__ void __launch_bounds__(Cfg<BN>::NT, 1)
 wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
   using Cf = Cfg<BN>;
   constexpr int BK = Cf::BK, BOX = Cf::BOX, PCH = Cf::PCH;
   static_assert(!PAIR || Cf::DEC, "pairs run the decoupled-ring layout");
+  static_assert(!GA || (!Cf::DEC && !PAIR && Cf::BK == 64), "gather-A: joint ring, 64 px");
   constexpr int BNL = PAIR ? BN / 2 : BN;                 // dz columns held by this CTA
+  // gather-A leaves the x half of every joint slot free: dz gets 2*S ring
+  // slots (the extra ones in those halves), the TMEM A slots stay S
+  constexpr int SB = GA ? 2 * Cf::S : Cf::S;
   constexpr uint32_t B_BYTES_L = (uint32_t)(BNL / 32) * BOX;
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
@@ -127,19 +137,22 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   const int cpt = g.Cin / 32;                   // chunks per tap
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  auto btile = [&](int sb) -> char* {
+    return (GA && sb >= Cf::S) ? Cf::a_tile(smem, sb - Cf::S) : Cf::b_tile(smem, sb);
+  };
   const int nl0 = n0 + (int)rank * BNL;                   // first dz column held here
   const int t0 = blockIdx.z * g.tps;
   const int nst = max(0, min(g.tiles, t0 + g.tps) - t0);
 
   if (tid == 0) {
-    for (int s = 0; s < Cf::S; ++s) {
+    for (int s = 0; s < SB; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&ready[s], PAIR ? 16 : 256);     // pairs: one arrival per warp, both CTAs
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < Cf::SA; ++s) {
       mbar_init(&afull[s], 1);
-      mbar_init(&afree[s], 128);
+      mbar_init(&afree[s], GA ? 1 : 128);      // GA: TMEM A slot freed by the MMA
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
@@ -164,16 +177,24 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       tma_prefetch_desc(&tx);
       if (!Cf::DEC) tma_prefetch_desc(&tdz);
       int na = 0;
-      for (int c = 0; c < 4; ++c) na += (m0 / 32 + c) < chunks;
+      if (!GA)
+        for (int c = 0; c < 4; ++c) na += (m0 / 32 + c) < chunks;
       const uint32_t bytes = (uint32_t)(na * BOX) + (Cf::DEC ? 0u : (uint32_t)Cf::B_BYTES);
-      for (int i = 0; i < nst; ++i) {
+      for (int i = 0; i < nst && GA; ++i) {       // gather-A: the dz ring only
+        const int sb = i % SB;
+        if (i >= SB) mbar_wait(&empty[sb], ((i / SB) - 1) & 1);
+        mbar_expect_tx(&full[sb], (uint32_t)Cf::B_BYTES);
+        for (int j = 0; j < BN / 32; ++j)
+          tma_load_2d(btile(sb) + j * BOX, &tdz, n0 + 32 * j, (t0 + i) * BK, &full[sb]);
+      }
+      for (int i = 0; i < nst && !GA; ++i) {
         const int s = i % Cf::SA;
         uint64_t* bar = Cf::DEC ? &afull[s] : &full[s];
         if (i >= Cf::SA) mbar_wait(Cf::DEC ? &afree[s] : &empty[s], ((i / Cf::SA) - 1) & 1);
         const int p0 = (t0 + i) * BK;
         char* st = Cf::a_tile(smem, s);
         mbar_expect_tx(bar, bytes);
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 4 && !GA; ++c) {
           const int gc = m0 / 32 + c;
           if (gc >= chunks) break;
           const int tap = gc / cpt, ci0 = (gc - tap * cpt) * 32;
@@ -209,8 +230,8 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       constexpr uint32_t idesc = PAIR ? ((make_idesc(BN) & ~(0x1Fu << 24)) | (16u << 24) | (1u << 16))
                                       : (make_idesc(BN) | (1u << 16));
       for (int i = 0; i < nst; ++i) {
-        const int s = i % Cf::S;
-        const uint32_t ph = (i / Cf::S) & 1;
+        const int s = i % SB, sa = i % Cf::S;     // dz ring slot, TMEM A slot
+        const uint32_t ph = (i / SB) & 1;
         const int c = i / PCH, b = c & 1;
         if (i % PCH == 0 && c >= 2) {
           if (PAIR) mbar_wait_cluster(&hfree[b], ((c >> 1) - 1) & 1);
@@ -220,8 +241,8 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         if (PAIR) mbar_wait_cluster(&ready[s], ph); else mbar_wait(&ready[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
-        const uint32_t ah = tmem + Cf::A_COL + s * 2 * BK, al = ah + BK;
-        const uint32_t bh = smem_u32(Cf::b_tile(smem, s));
+        const uint32_t ah = tmem + Cf::A_COL + sa * 2 * BK, al = ah + BK;
+        const uint32_t bh = smem_u32(btile(s));
         const uint32_t bl = bh + Cf::B_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
@@ -243,9 +264,62 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           if (i % PCH == PCH - 1 || i == nst - 1) tc_commit2_elect(&hfull[b]);
         } else {
           tc_commit_elect(&empty[s]);
+          if (GA) tc_commit_elect(&afree[sa]);
           if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
         }
       }
+    }
+  } else if (GA && warp < CB0) {
+    // ------------------------------------------------------------ A gather (GA)
+    const int q = warp & 3;
+    const bool rv = lane < nrows;
+    const int tap = rv ? lane / g.Cin : 4, ci = rv ? lane - (lane / g.Cin) * g.Cin : 0;
+    const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+    const long long sh = ((long long)dy * g.W + dx) * g.Cin + ci;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
+    const long long hw = (long long)g.H * g.W;
+    // software-pipelined: stage i+1's loads are issued right after stage i's
+    // TMEM stores, so their latency overlaps the wait for the next slot
+    float v[16];
+    uint32_t okm = 0;
+    auto gather = [&](int i) {
+      const long long pb = (long long)(t0 + i) * BK + 16 * q;    // this quadrant's pixels
+      const int rem = (int)(pb % hw);
+      int oh = rem / g.W, ow = rem - (rem / g.W) * g.W;
+      okm = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {      // all loads unconditional: in flight together
+        const long long pp = pb + k;
+        const bool ok = rv && pp < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
+                        (unsigned)(ow + dx) < (unsigned)g.W;
+        okm |= (uint32_t)ok << k;
+        v[k] = __ldg(g.x + (ok ? pp * g.Cin + sh : 0));
+        if (++ow == g.W) { ow = 0; if (++oh == g.H) oh = 0; }
+      }
+    };
+    if (nst > 0) gather(0);
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % Cf::S;                      // TMEM A slot
+      float hi[16], lo[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) split((okm >> k) & 1u ? v[k] : 0.f, hi[k], lo[k]);
+      if (i >= Cf::S) mbar_wait(&afree[s], ((i / Cf::S) - 1) & 1);   // MMA(i - S) done
+      tc_fence_after();
+      const uint32_t a = lanebase + s * 2 * BK;
+      if (i < Cf::S) {                              // first use of the slot: zero columns
+        float z[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) z[k] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2 * BK; c += 16)
+          if ((c & (BK - 1)) != 16 * q) tmem_st16(a + c, z);
+      }
+      tmem_st16(a + 16 * q, hi);
+      tmem_st16(a + BK + 16 * q, lo);
+      if (i + 1 < nst) gather(i + 1);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&ready[i % SB]);
     }
   } else if (warp < CB0) {
     // ------------------------------------------------------------ A converters
@@ -325,9 +399,9 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     const bool do_bias = bias_part != nullptr && blockIdx.x / (PAIR ? 2 : 1) == 0;
     float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = 0; i < nst; ++i) {
-      const int s = i % Cf::S;
-      mbar_wait(&full[s], (i / Cf::S) & 1);
-      const char* raw = Cf::b_tile(smem, s);
+      const int s = i % SB;
+      mbar_wait(&full[s], (i / SB) & 1);
+      const char* raw = btile(s);
       char* lo = const_cast<char*>(raw) + Cf::B_BYTES;
 #pragma unroll
       for (int k = rg; k < BK; k += RG) {
@@ -388,11 +462,30 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         mbar_arrive(&hfree[b]);
       }
     }
-    const int r = m0 + q * 32 + lane;
-    if (r < nrows) {
-      float* o = part + (long long)blockIdx.z * g.slab + r;
+    if (GA) {
+      // sum the four quadrants' partial rows through shared memory (the
+      // rings are idle: every MMA has completed once the last hfull fired)
+      float* red = reinterpret_cast<float*>(smem);      // [4][32][BN]
 #pragma unroll
-      for (int j = 0; j < CW; ++j) o[(long long)(n0 + hf * CW + j) * nrows] = acc[j];
+      for (int j = 0; j < CW; ++j) red[(q * 32 + lane) * BN + hf * CW + j] = acc[j];
+      named_sync(2, 32 * (Cf::NT / 32 - DR0));
+      if (q == 0 && lane < nrows) {
+        float* o = part + (long long)blockIdx.z * g.slab + lane;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          const int col = hf * CW + j;
+          const float t = red[lane * BN + col] + red[(32 + lane) * BN + col] +
+                          red[(64 + lane) * BN + col] + red[(96 + lane) * BN + col];
+          o[(long long)(n0 + col) * nrows] = t;
+        }
+      }
+    } else {
+      const int r = m0 + q * 32 + lane;
+      if (r < nrows) {
+        float* o = part + (long long)blockIdx.z * g.slab + r;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) o[(long long)(n0 + hf * CW + j) * nrows] = acc[j];
+      }
     }
   }
 
@@ -447,11 +540,11 @@ inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C, i
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, bool GA = false>
 bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g, int mt,
                     int nt, int splits, float* part, float* bias_part, cudaStream_t st) {
   using Cf = Cfg<BN>;
-  auto kern = wgt_kernel<BN, PAIR>;
+  auto kern = wgt_kernel<BN, PAIR, GA>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
@@ -482,7 +575,11 @@ bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g,
 
 // ============================================================ entry points
 
-bool wgt_conv_ok(int cin, int cout) { return cin % 32 == 0 && cout % 64 == 0; }
+// Cin % 32 == 0: x tiles by TMA; 9*Cin <= 32 (the first conv): gather-A mode
+bool wgt_conv_ok(int cin, int cout) {
+  if (cin % 32 == 0) return cout % 64 == 0;
+  return 9 * cin <= 32 && cout % 64 == 0 && cout % 128 != 0;   // gather-A runs N = 64 tiles
+}
 
 size_t wgt_conv_ws(int n, int h, int w, int cin, int cout) {
   if (!wgt_conv_ok(cin, cout)) return 0;      // the planner assumes a supported shape
@@ -509,18 +606,22 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
   wgt::Geo g;
   int mt, nt, splits;
   wgt::plan(n, h, w_, cin, cout, g, mt, nt, splits);
+  g.x = x;
+  const bool ga = cin % 32 != 0;
   CUtensorMap tx, tdz;
   const int bk = wgt::bn_for(cout) == 128 ? wgt::Cfg<128>::BK : wgt::Cfg<64>::BK;
-  if (!wgt::encode_rows(&tx, x, g.npix, cin, bk) ||
+  if ((!ga && !wgt::encode_rows(&tx, x, g.npix, cin, bk)) ||
       !wgt::encode_rows(&tdz, dz, g.npix, cout, bk))
     return BPX_ERR_INVALID_ARGUMENT;
+  if (ga) tx = tdz;                          // unused by the gather path
   float* part = splits == 1 ? dw : static_cast<float*>(ws);
   float* bpart = !dbias ? nullptr
                         : (splits == 1 ? dbias : static_cast<float*>(ws) + (size_t)splits * slab);
   bpx_status_t s = wgt::bn_for(cout) == 128
       ? (wgt::paired(cin, cout) ? wgt::launch<128, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
                            : wgt::launch<128, false>(tx, tdz, g, mt, nt, splits, part, bpart, st))
-      : wgt::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+      : (ga ? wgt::launch<64, false, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+            : wgt::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st));
   if (s != BPX_OK || splits == 1) return s;
   s = split_reduce(part, splits, slab, dw, st);
   if (s != BPX_OK || !dbias) return s;
