@@ -217,6 +217,12 @@ BPX_API bpx_status_t bpx_allreduce_sum_prefix(const float* const* peers, int g,
  * the local pad reach `epoch`.  pads[r] = rank r's pad (g uint32 slots).   */
 BPX_API bpx_status_t bpx_signal_barrier(uint32_t* const* pads, int rank, int g,
                                 uint32_t epoch, void* stream);
+/* Same barrier for CUDA-graph replay: the epoch is this rank's device
+ * counter for the group (*counter), incremented by the kernel, so each
+ * replay waits for the next epoch.  Every participant calls it in the same
+ * sequence.                                                                */
+BPX_API bpx_status_t bpx_signal_barrier_dev(uint32_t* const* pads, uint32_t* counter,
+                                    int rank, int g, void* stream);
 
 /* ---- engine-pinned variants (tests / benchmarks): force the FFMA
  * implicit-GEMM engine regardless of shape, same semantics as above.      */

@@ -111,6 +111,133 @@ class TorchComm:
         self.dist.barrier()
 
 
+class PeerComm:
+    """P2P backend of the step's communication (north_star (2)-(3)): peer
+    memory instead of NCCL for the data path, every op graph-capturable.
+
+    Each rank owns one device arena -- signal pads, per-group-size epoch
+    counters and a staging area -- whose CUDA IPC handle is exchanged once
+    through torch.distributed (any backend: only handles and scalars go
+    through it).  Peers map each other's arenas (NVLink peer addresses on a
+    multi-GPU box; the same device for two processes sharing one GPU).
+
+    * reshard (the `transfer` op, simulator.py:242-253): each source rank
+      stages its shard, a device barrier over the participants, then every
+      destination rank pulls its contiguous runs (costs.reshard_segments)
+      from the sources' staging areas with ``bpx_reshard_pull``, and a second
+      barrier before the staging areas may be reused;
+    * allreduce over ranks [0, g) (`allreduce`, :264-278): stage, barrier,
+      one-shot pull-sum in rank order (``bpx_allreduce_sum_prefix``: the
+      same bits on every rank), barrier.
+    Barriers are ``bpx_signal_barrier_dev`` (device-resident epochs), so a
+    captured step replays correctly.  Call ``prepare`` (collective) before
+    use: BurstStep does, with its largest shard and gradient bucket.
+
+    Processes must load their kernels eagerly (``CUDA_MODULE_LOADING=EAGER``
+    before CUDA initialises): with lazy loading, a kernel's first launch can
+    wait on the device while a peer's barrier kernel spins waiting on this
+    process -- a deadlock."""
+
+    def __init__(self, rank: int, world: int, group_sizes=(), device=None):
+        import os
+        import warnings
+        if os.environ.get("CUDA_MODULE_LOADING", "").upper() != "EAGER":
+            warnings.warn("PeerComm: set CUDA_MODULE_LOADING=EAGER before CUDA starts; "
+                          "lazy kernel loading can deadlock with device barriers")
+        self.rank, self.world = rank, world
+        self.host = TorchComm(rank, world, ())   # handle exchange, scalars, host barrier
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        self.arena = None
+
+    def prepare(self, stage_bytes: int) -> None:
+        from . import ops
+        W = self.world
+        pad_bytes = 4 * W * (W + 1)               # pads for group sizes 1..W, W slots each
+        cnt_bytes = 4 * (W + 1)                   # one epoch counter per group size
+        head = (pad_bytes + cnt_bytes + 255) // 256 * 256
+        size = head + max(16, (stage_bytes + 255) // 256 * 256)
+        if self.arena is not None and self.arena.numel() >= size:
+            return
+        self.arena = torch.zeros(size, dtype=torch.uint8, device=self.device)
+        self.head = head
+        self.pad_bytes = pad_bytes
+        handle = self.arena.untyped_storage()._share_cuda_()
+        handles = [None] * W
+        self.host.dist.all_gather_object(handles, handle)
+        self.peer_storages = []
+        self.peer_base = []
+        for r in range(W):
+            if r == self.rank:
+                self.peer_base.append(self.arena.data_ptr())
+                self.peer_storages.append(None)
+            else:
+                st = torch.UntypedStorage._new_shared_cuda(*handles[r])
+                self.peer_storages.append(st)     # keeps the mapping alive
+                # the handle covers the caching allocator's block; the arena
+                # starts at the storage's offset inside it (handle[3])
+                self.peer_base.append(st.data_ptr())
+        self.host.dist.barrier()
+        self._ops = ops
+
+    # layout helpers (the same offsets in every rank's arena)
+    def _pads(self, g: int) -> list:
+        return [b + 4 * self.world * g for b in self.peer_base[:g]]
+
+    def _counter(self, g: int) -> int:
+        return self.arena.data_ptr() + self.pad_bytes + 4 * g
+
+    def _stage(self, r: int) -> int:
+        return self.peer_base[r] + self.head
+
+    def _barrier(self, g: int) -> None:
+        if g > 1 and self.rank < g:
+            self._ops.signal_barrier_dev(self._pads(g), self._counter(g), self.rank)
+
+    def _stage_view(self, nbytes: int) -> torch.Tensor:
+        return self.arena[self.head:self.head + nbytes]
+
+    def reshard(self, src: Optional[torch.Tensor], g: int, dst: Optional[torch.Tensor],
+                h: int, B: int, bytes_per_sample: int) -> None:
+        P = max(g, h)
+        if self.rank >= P:
+            return
+        if src is not None and self.rank < g:
+            sb = _bytes(src)
+            self._stage_view(sb.numel()).copy_(sb)
+        self._barrier(P)
+        if dst is not None and self.rank < h:
+            cg, ch = ceil_div(B, g), ceil_div(B, h)
+            srcs, soff, doff, nb = [], [], [], []
+            for p, q, s0, n in reshard_segments(B, g, h):
+                if q != self.rank:
+                    continue
+                srcs.append(self._stage(p))
+                soff.append((s0 - p * cg) * bytes_per_sample)
+                doff.append((s0 - q * ch) * bytes_per_sample)
+                nb.append(n * bytes_per_sample)
+            for k in range(0, len(nb), 64):
+                self._ops.reshard_pull(srcs[k:k + 64], soff[k:k + 64], dst, doff[k:k + 64],
+                                       nb[k:k + 64])
+        self._barrier(P)
+
+    def allreduce(self, flat: torch.Tensor, g: int) -> None:
+        if g <= 1 or self.rank >= g:
+            return
+        self._stage_view(flat.numel() * 4).copy_(_bytes(flat))
+        self._barrier(g)
+        self._ops.allreduce_sum_prefix([self._stage(r) for r in range(g)], flat, flat.numel())
+        self._barrier(g)
+
+    def max_scalar(self, value: float, device) -> float:
+        return self.host.max_scalar(value, device)
+
+    def sum_scalar(self, value: float, device) -> float:
+        return self.host.sum_scalar(value, device)
+
+    def barrier(self):
+        self.host.barrier()
+
+
 class LocalComm:
     """world_size 1: every layer has g == 1, nothing crosses a GPU."""
 

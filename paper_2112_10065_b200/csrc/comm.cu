@@ -87,6 +87,30 @@ __global__ void signal_barrier_kernel(PadTable t) {
   }
 }
 
+// Graph-replayable variant: the epoch lives in device memory (this rank's
+// counter for the group), incremented by the kernel itself, so every replay
+// of a captured barrier waits for the NEXT epoch instead of a frozen one.
+struct PadTableDev {
+  unsigned int* pad[kMaxPeers];
+  unsigned int* counter;
+  int g, rank;
+};
+
+__global__ void signal_barrier_dev_kernel(PadTableDev t) {
+  __shared__ unsigned int e;
+  if (threadIdx.x == 0) e = ++(*t.counter);
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid < t.g) {
+    __threadfence_system();
+    volatile unsigned int* slot = t.pad[tid] + t.rank;
+    *slot = e;
+    volatile unsigned int* mine = t.pad[t.rank] + tid;
+    while ((int)(*mine - e) < 0) { }
+    __threadfence_system();
+  }
+}
+
 }  // namespace bpx
 
 using namespace bpx;
@@ -158,6 +182,20 @@ bpx_status_t bpx_signal_barrier(uint32_t* const* pads, int rank, int g, uint32_t
   }
   t.g = g; t.rank = rank; t.epoch = epoch;
   signal_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t);
+  return launch_status();
+}
+
+bpx_status_t bpx_signal_barrier_dev(uint32_t* const* pads, uint32_t* counter, int rank, int g,
+                                    void* stream) {
+  BPX_CHECK_ARG(pads && counter && g >= 1 && g <= kMaxPeers && rank >= 0 && rank < g);
+  PadTableDev t{};
+  for (int r = 0; r < g; ++r) {
+    BPX_CHECK_ARG(pads[r] != nullptr);
+    t.pad[r] = pads[r];
+  }
+  t.counter = counter;
+  t.g = g; t.rank = rank;
+  signal_barrier_dev_kernel<<<1, 32, 0, as_stream(stream)>>>(t);
   return launch_status();
 }
 

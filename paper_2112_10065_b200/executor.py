@@ -33,7 +33,7 @@ from . import ops
 from .comm import LocalComm, TorchComm
 from .costs import shard_range
 from .errors import GraphFormatError, UnsupportedTopologyError
-from .graph import CompGraph
+from .graph import CompGraph, ceil_div
 from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
 from .planner import TrainingPlan
 from .timeline import (FG_TASK, SimConfig, SimMetrics, SimTrace, compile_timeline,
@@ -265,6 +265,23 @@ class BurstStep:
                 S = self.layers[L.skip_i]
                 if S.active:
                     L.dskip_src = torch.empty_like(S.y)
+        if hasattr(self.comm, "prepare"):
+            # P2P backend: one staging area per rank, sized from the plan only
+            # (identical on every rank: the call is collective)
+            stage = 0
+            for i, L in enumerate(self.layers):
+                if self._chain_transfer(i):
+                    bps = 4 * L.spec.in_elems()
+                    stage = max(stage, ceil_div(self.B, self.layers[i - 1].g) * bps,
+                                ceil_div(self.B, L.g) * bps)
+                if L.join == "reshard":
+                    bps = 4 * self.layers[L.skip_i].spec.out_elems()
+                    stage = max(stage, ceil_div(self.B, L.g) * bps,
+                                ceil_div(self.B, self.layers[L.skip_i].g) * bps)
+            for g, n in sizes.items():
+                if g > 1:
+                    stage = max(stage, 4 * n)
+            self.comm.prepare(stage)
         self.ws = self.k.Workspace(dev)
         self.ws.reserve(ws_need)
         last = self.layers[-1]
@@ -666,8 +683,14 @@ def _pad4(n: int) -> int:
 
 
 def _dist_comm(plan_gs):
+    """NCCL/gloo collectives by default; ``BPX_COMM=peer`` selects the P2P
+    backend (comm.PeerComm: libbpx pull kernels over IPC-mapped peer memory,
+    needs CUDA_MODULE_LOADING=EAGER)."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if os.environ.get("BPX_COMM", "").lower() == "peer":
+            from .comm import PeerComm
+            return PeerComm(dist.get_rank(), dist.get_world_size(), plan_gs)
         return TorchComm(dist.get_rank(), dist.get_world_size(), plan_gs)
     return LocalComm()
 

@@ -95,6 +95,8 @@ _SIGS = {
     "bpx_allreduce_sum_prefix": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
                                                 ctypes.c_void_p, ctypes.c_size_t,
                                                 ctypes.c_void_p]),
+    "bpx_signal_barrier_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_void_p]),
     "bpx_signal_barrier": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_uint32,
                                           ctypes.c_void_p]),
@@ -545,3 +547,11 @@ def simt_conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):
                                       wd, cin, cout, wp, wb, _stream()),
            "bpx_simt_conv3x3_wgrad")
     return dw
+
+
+def signal_barrier_dev(pad_ptrs: Sequence[int], counter_ptr: int, rank: int):
+    """Graph-replayable cross-GPU barrier (device-resident epoch counter)."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(pad_ptrs))(*pad_ptrs)
+    _check(lib.bpx_signal_barrier_dev(ctypes.cast(arr, ctypes.c_void_p), counter_ptr, rank,
+                                      len(pad_ptrs), _stream()), "bpx_signal_barrier_dev")
