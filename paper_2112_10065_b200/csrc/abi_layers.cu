@@ -127,8 +127,10 @@ size_t bpx_linear_dgrad_workspace(int b, int in, int out) {
   return m > d ? m : d;
 }
 size_t bpx_linear_wgrad_workspace(int b, int in, int out) {
-  return max3(simt_linear_wgrad_ws(b, in, out), tc_linear_wgrad_ws(b, in, out),
-              dns_linear_ws(b, in, out));
+  size_t m = max3(simt_linear_wgrad_ws(b, in, out), tc_linear_wgrad_ws(b, in, out),
+                  dns_linear_ws(b, in, out));
+  size_t d = dwt_linear_ws(b, in, out);
+  return m > d ? m : d;
 }
 
 bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, float* y,
@@ -171,6 +173,13 @@ bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float*
                               void* stream) {
   BPX_CHECK_ARG(x && dy && dw && b >= 0 && in > 0 && out > 0 && aligned16(dw));
   cudaStream_t st = as_stream(stream);
+  // tensor-core engine above 8 rows: both engines are bound by writing dW,
+  // but the FFMA outer product's math grows with b (B200, fc1: 189 vs 93 us
+  // at b = 32, 118 vs 91 at 16; at b <= 8 the FFMA kernel is ~14 us faster)
+  if (b > 8 && dwt_linear_ok(b, in, out)) {
+    bpx_status_t s = dwt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (dns_linear_ok(b, in, out))
     return dns_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))

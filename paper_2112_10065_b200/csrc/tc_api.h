@@ -82,6 +82,10 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* w_lo,
 
 // TMA-fed tcgen05 dense fwd / dgrad for batches <= 32 (tc_dense.cu).
 namespace bpx {
+bool dwt_linear_ok(int b, int in, int out);
+size_t dwt_linear_ws(int b, int in, int out);
+bpx_status_t dwt_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias, int b,
+                              int in, int out, void* ws, size_t ws_bytes, cudaStream_t st);
 bool dtc_linear_ok(int b, int in, int out);
 size_t dtc_linear_ws(int b, int in, int out);
 bpx_status_t dtc_linear_fwd(const float* x, const float* w, const float* bias, float* y, int b,

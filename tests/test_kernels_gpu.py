@@ -130,7 +130,8 @@ def test_conv_matches_ffma_engine():
 @pytest.mark.parametrize("b,fin,fout,relu", [(4, 25088, 4096, True), (32, 4096, 4096, True),
                                              (32, 4096, 1000, False), (3, 64, 40, True),
                                              (1, 128, 1000, False), (17, 256, 384, True),
-                                             (2, 512, 128, False)], ids=str)
+                                             (2, 512, 128, False), (12, 100, 36, True),
+                                             (32, 25088, 4096, True)], ids=str)
 def test_linear_fwd_bwd(b, fin, fout, relu):
     x = relu_input(b, fin, seed=15)
     w = rnd(fout, fin, seed=16, scale=0.01)
