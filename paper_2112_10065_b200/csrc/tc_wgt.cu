@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(Cfg<BN>::NT, 1)
 wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
   using Cf = Cfg<BN>;
+  // N = 64 tiles: both a_hi products as one N = 128 MMA, the accumulator
+  // columns (2 x 64) serving as one merged buffer instead of a ping-pong pair
+  constexpr bool MG = BN == 64 && !PAIR && !GA;
   constexpr int BK = Cf::BK, BOX = Cf::BOX, PCH = Cf::PCH;
   static_assert(!PAIR || Cf::DEC, "pairs run the decoupled-ring layout");
   static_assert(!GA || (!Cf::DEC && !PAIR && Cf::BK == 64), "gather-A: joint ring, 64 px");
@@ -229,11 +232,16 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       // M=128 (pairs: 256), N=BN, tf32 x tf32 -> f32, A from TMEM, B MN-major (bit 16)
       constexpr uint32_t idesc = PAIR ? ((make_idesc(BN) & ~(0x1Fu << 24)) | (16u << 24) | (1u << 16))
                                       : (make_idesc(BN) | (1u << 16));
+      constexpr uint32_t idesc_mg = make_idesc(2 * BN) | (1u << 16);
       for (int i = 0; i < nst; ++i) {
         const int s = i % SB, sa = i % Cf::S;     // dz ring slot, TMEM A slot
         const uint32_t ph = (i / SB) & 1;
-        const int c = i / PCH, b = c & 1;
-        if (i % PCH == 0 && c >= 2) {
+        const int c = i / PCH, b = MG ? 0 : c & 1;
+        if (MG && i % PCH == 0 && c >= 1) {        // one merged buffer: wait for its drain
+          mbar_wait(&hfree[0], (c - 1) & 1);
+          tc_fence_after();
+        }
+        if (!MG && i % PCH == 0 && c >= 2) {
           if (PAIR) mbar_wait_cluster(&hfree[b], ((c >> 1) - 1) & 1);
           else mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
           tc_fence_after();
@@ -249,7 +257,13 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const uint64_t dbh = make_desc_mn32(bh + ks * 1024, BOX, 512);
           const uint64_t dbl = make_desc_mn32(bl + ks * 1024, BOX, 512);
           const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
-          if (PAIR) {
+          if (MG) {
+            // [b_hi | b_lo] as one N = 128 operand (the lo tile follows the
+            // raw one at the same MN-atom stride): one A read for both a_hi
+            // products, then a_lo * b_hi into the left half
+            mma_ts_elect(d, ah + 8 * ks, dbh, idesc_mg, acc);
+            mma_ts_elect(d, al + 8 * ks, dbh, idesc, 1u);
+          } else if (PAIR) {
             mma_ts2_elect(d, al + 8 * ks, dbh, idesc, acc);
             mma_ts2_elect(d, ah + 8 * ks, dbl, idesc, 1u);
             mma_ts2_elect(d, ah + 8 * ks, dbh, idesc, 1u);
@@ -443,16 +457,24 @@ wgt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     for (int j = 0; j < CW; ++j) acc[j] = 0.f;
     const int nch = (nst + PCH - 1) / PCH;
     for (int c = 0; c < nch; ++c) {
-      const int b = c & 1;
-      mbar_wait(&hfull[b], (c >> 1) & 1);
+      const int b = MG ? 0 : c & 1;
+      mbar_wait(&hfull[b], MG ? (c & 1) : ((c >> 1) & 1));
       tc_fence_after();
 #pragma unroll
       for (int j = 0; j < CW; j += 8) {
         uint32_t r[8];
         tmem_ld8(lanebase + b * BN + j, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (MG) {                       // + the a_hi * b_lo half
+          uint32_t r2[8];
+          tmem_ld8(lanebase + BN + j, r2);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]);
+          for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]) + __uint_as_float(r2[t]);
+        } else {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]);
+        }
       }
       tc_fence_before();
       if (PAIR) {
