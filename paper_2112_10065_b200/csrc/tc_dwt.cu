@@ -4,8 +4,9 @@
 // K = the batch (<= 32), so the GEMM is one 32-K step per output tile and the
 // kernel is bound by WRITING dW (fc1: 411 MB per pass), not by math.  A prep
 // kernel transposes dy and x into K-major rows of 32 floats (zero-padded
-// past the batch) and splits them into TF32 hi/lo once; the persistent main
-// kernel then streams 128 x 256 output tiles:
+// past the batch) and splits them into TF32 hi/lo once (the same launch
+// emits the bias gradient, the column sums of dy, from its smem tile); the
+// persistent main kernel then streams 128 x 256 output tiles:
 //
 //   warp 0  TMA: A hi/lo (128 x 32) + B hi/lo (256 x 32) per tile
 //   warp 1  MMA (SS form, 3xTF32: 4 k-steps x 3 products into one TMEM
@@ -16,9 +17,10 @@
 //           16-B stores, four full 128-B rows of dW per store instruction
 //           (TMA tensor stores of 32 x 32 boxes issue-stalled at ~5 TB/s)
 //
-// The reference's FFMA outer product for this op is dns::outer64_kernel
-// (dense_ffma.cu); both restate the dense layer's weight gradient of the
-// reference's VGG model.
+// This is the weight gradient of the reference's dense layers (the VGG
+// model's fc1-fc3).  Batches <= 8 stay on the FFMA outer
+// product (dns::outer_kernel, dense_ffma.cu), which writes faster when the
+// math is that small (routing: bpx_linear_wgrad, abi_layers.cu).
 #include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "tc_api.h"
