@@ -218,11 +218,105 @@ def _roofline(dom, tf32_peak, peak_src, step_ms, flops_step, gemm_ms):
     }
 
 
+def _golden_loss(batch):
+    """fp64 oracle loss of the first step at the seed-0 init and batch
+    (tests/golden/vgg16_step_fp64.json, oracle/gen_golden_step.py)."""
+    with open(os.path.join(ROOT, "tests", "golden", "vgg16_step_fp64.json")) as fh:
+        return json.load(fh)["batches"][str(batch)]["loss"]
+
+
+def dp_overlapped_us(graph, g):
+    """Predicted uniform-DP iteration with each layer's gradient allreduce
+    overlapped with the remaining backward (one allreduce channel, buckets
+    issued as layers finish their backward), on the same comp/sync prices
+    as forced_plan (which charges every allreduce serially).  Builder model:
+    a layer's backward is 2/3 of its comp(i, g) (dgrad + wgrad vs fwd)."""
+    from paper_2112_10065_b200.costs import CostModel, make_context
+    cm = CostModel(make_context(graph, g, candidates=sorted({1, g})))
+    ids = [lid for lid in graph.topo_order() if not graph.layer(lid).is_virtual]
+    t = sum(cm.comp(lid, g) / 3.0 for lid in ids)
+    ar = 0.0
+    for lid in reversed(ids):
+        t += 2.0 * cm.comp(lid, g) / 3.0
+        s_ = cm.sync(lid, g)
+        if s_ > 0:
+            ar = max(ar, t) + s_
+    return max(t, ar)
+
+
+def b200_plan_report(world):
+    """BP vs DP on B200-measured layer costs: plan the
+    VGG-16 profile measured on B200 (profiles/b200_vgg16_graph.json, the
+    reference's profile schema) at this world size for a range of amp
+    limits; amp* = the limit with the smallest predicted iteration.  DP is
+    priced serially (forced_plan, the reference's charging,
+    simulator.py:918-942) and with backward-overlapped allreduce."""
+    from paper_2112_10065_b200.graph import load_graph
+    from paper_2112_10065_b200.planner import plan
+    from paper_2112_10065_b200.timeline import forced_plan
+    path = os.path.join(ROOT, "profiles", "b200_vgg16_graph.json")
+    if not os.path.exists(path):
+        return None
+    g = load_graph(path)
+    if g.global_batch != GLOBAL_BATCH:
+        from dataclasses import replace
+        g = replace(g, global_batch=GLOBAL_BATCH)
+    rows = []
+    for amp in (1.5, 2.0, 3.0, 4.0, 8.0, 16.0):
+        try:
+            p = plan(g, world, amp)
+        except Exception as exc:          # infeasible amp limits are reported
+            rows.append({"amp": amp, "error": type(exc).__name__})
+            continue
+        rows.append({"amp": amp, "bp_predicted_us": p.predicted_iteration_us,
+                     "gpus_per_layer": [gi for _, gi in p.assignments]})
+    ok = [r for r in rows if "bp_predicted_us" in r]
+    best = min(ok, key=lambda r: r["bp_predicted_us"]) if ok else None
+    dp = forced_plan(g, world, world)
+    return {"profile": "profiles/b200_vgg16_graph.json (tools/profile_b200.py)",
+            "amps": rows, "amp_star": best["amp"] if best else None,
+            "bp_star_predicted_us": best["bp_predicted_us"] if best else None,
+            "dp_serial_predicted_us": dp.predicted_iteration_us,
+            "dp_overlapped_predicted_us": dp_overlapped_us(g, world),
+            "bp_star_over_dp_serial": (dp.predicted_iteration_us / best["bp_predicted_us"])
+            if best else None,
+            "bp_star_over_dp_overlapped": (dp_overlapped_us(g, world) / best["bp_predicted_us"])
+            if best else None}
+
+
+def host_timings(world):
+    """The reference's CPU-side hot path timed on this host: plan() (median
+    of 20, single-threaded pure Python) and the simulated
+    two-phase BP+Col run of the same op program (simulate_two_phase, the
+    bit-exact restatement of simulator.py:959-977)."""
+    from paper_2112_10065_b200 import synth
+    from paper_2112_10065_b200.planner import plan
+    from paper_2112_10065_b200.simulate import simulate_two_phase
+    from paper_2112_10065_b200.timeline import SimConfig, compile_timeline
+    g = synth.vgg_like(seed=0, global_batch=GLOBAL_BATCH)
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        p = plan(g, world, AMP_LIMIT)
+        ts.append(time.perf_counter() - t0)
+    cfg = SimConfig()
+    tl = compile_timeline(p, g, world, synth.small_bg_model(), cfg)
+    t0 = time.perf_counter()
+    simulate_two_phase(tl, cfg)
+    sim_s = time.perf_counter() - t0
+    return {"plan_ms_median_of_20": 1e3 * statistics.median(ts),
+            "simulate_two_phase_bp_col_s": sim_s, "cores": 1,
+            "what": f"plan(vgg_like B=32, {world}, amp {AMP_LIMIT}) and the two-phase "
+                    "BP+Col simulation of its op program, pure Python, one thread"}
+
+
 def bench_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
         return 0
-    sample = 4        # bounded sample per step (~1-2 s of CPU work)
+    # the same workload as our arm's step: one VGG-16 fwd+bwd over the whole
+    # 32-sample global batch per step (~2 s on 16 host cores)
+    sample = GLOBAL_BATCH
     thr, threads, dt = cpu_step_samples_per_s(sample, steps=args.steps, warm=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": thr, "unit": "samples/s",
@@ -234,7 +328,7 @@ def bench_reference(args):
                    "global_batch": GLOBAL_BATCH, "sample_batch_per_step": sample},
         "cpu_baseline": {"value": thr, "unit": "samples/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{sample} samples per step x {args.steps} steps "
+                         "sample": f"the full {sample}-sample step x {args.steps} steps "
                                    "(oracle/vgg_ref.py torch fp32; the reference "
                                    "burstplan has no fwd/bwd, simulator.py:254-261)"},
         "e2e": {"value": thr, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -265,14 +359,28 @@ def bench_ours(args):
     st.load(xh, yh)
     torch.cuda.synchronize()
 
-    # launches per step (eager pass, host counter in libbpx)
-    c0 = ops.launch_count()
+    # launches per step (eager pass, host counter in libbpx); this first
+    # step runs at the seed-0 init, so its loss is checked against the
+    # committed fp64 oracle loss (SURVEY.md §8c gate |dL|/L <= 1e-4)
+    c0, l0 = ops.launch_count(), ops.legacy_engine_calls()
     st.forward_backward()
     st.sync_and_update()
     torch.cuda.synchronize()
     launches_per_step = ops.launch_count() - c0
+    legacy_per_step = ops.legacy_engine_calls() - l0
+    first_loss = st.loss()
+    try:
+        gold = _golden_loss(GLOBAL_BATCH)
+        parity = {"loss": first_loss, "loss_fp64_oracle": gold,
+                  "rel_err": abs(first_loss - gold) / abs(gold), "gate": 1e-4,
+                  "source": "tests/golden/vgg16_step_fp64.json (oracle/vgg_ref.py fp64, "
+                            "seed-0 init and batch)"}
+        parity["ok"] = parity["rel_err"] <= parity["gate"]
+    except Exception as exc:
+        parity = {"ok": False, "error": f"{type(exc).__name__}: {exc}"}
 
-    st.capture(warmup=1)
+    st.capture(warmup=1)          # raises if the step cannot be captured
+    captured = isinstance(st.graph, torch.cuda.CUDAGraph)
 
     for _ in range(args.warmup):
         st.step()
@@ -340,9 +448,9 @@ def bench_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            thr, threads, dt = cpu_step_samples_per_s(8, steps=2, warm=1)
+            thr, threads, dt = cpu_step_samples_per_s(GLOBAL_BATCH, steps=1, warm=1)
             cpu = {"value": thr, "unit": "samples/s", "cores": threads, "kind": "port",
-                   "sample": f"2 timed steps x 8 samples of the VGG-16 fwd+bwd step "
+                   "sample": f"1 timed step x {GLOBAL_BATCH} samples of the VGG-16 fwd+bwd step "
                              f"({dt:.1f} s), oracle/vgg_ref.py torch fp32 on all host "
                              "threads; the reference burstplan prices this step "
                              "instead of computing it (simulator.py:254-261)"}
@@ -360,16 +468,21 @@ def bench_ours(args):
                        "gpus_per_layer": [g for _, g in p.assignments],
                        "parallelism": f"burst{world}",
                        "l2": "working set ~2.2 GB > 126 MB L2, no flush needed",
-                       "cuda_graph": True},
+                       "cuda_graph": captured},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 4},
             "gpu_launches": launches_per_step * args.steps,
+            "legacy_engine_calls_per_step": legacy_per_step,
+            "parity_checked": bool(parity.get("ok")),
+            "parity": parity,
             "roofline": _roofline(dom, tf32_peak, peak_src, ms / args.steps,
                                   flops_step, gemm_ms),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "bp_col": col,
             "uniform_dp": dp,
+            "b200_plans": b200_plan_report(world),
+            "host_timings": None if args.no_cpu else host_timings(world),
             "loss": trace.loss,
         }
         print(json.dumps(result), flush=True)

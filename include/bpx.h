@@ -53,6 +53,14 @@ BPX_API int bpx_abi_version(void);
 /* Kernel launches this process issued through libbpx so far (host count;
  * a CUDA-graph replay re-runs the captured launches without counting). */
 BPX_API long long bpx_launch_count(void);
+/* Engine that served the calling thread's last conv3x3 / linear call:
+ * "fdt" (TMA fwd/dgrad), "wgt" (TMA wgrad), "c1" (conv1_1 fwd), "dtc"
+ * (dense fwd/dgrad), "dwt" (dense wgrad), "dns" (dense FFMA, <= 8 rows or
+ * 1000 outputs), "tc" (pixel-batched 1x1 convs); legacy: "simt", "ts",
+ * "wg", "small".  Static storage.                                         */
+BPX_API const char* bpx_last_engine(void);
+/* conv3x3 / linear calls this process sent to a legacy engine.            */
+BPX_API long long bpx_legacy_engine_calls(void);
 /* 1 if the current device is sm_100 (the only supported target). */
 BPX_API int bpx_device_supported(void);
 

@@ -6,7 +6,24 @@
 
 using namespace bpx;
 
+// Which engine served the calling thread's last conv/dense call, and how many
+// calls this process sent to a legacy engine (the FFMA implicit GEMM, the
+// per-thread-gather TS engine, the SS engine, the old wgrad engine, the
+// small-Cin FFMA kernels): tests assert that every VGG-16 op at the
+// benchmarked per-GPU batches takes a TMA tensor-core engine, and bench.py
+// reports the legacy count of its step.
+static thread_local const char* g_engine = "";
+static long long g_legacy_calls = 0;
+static inline void use(const char* e) { g_engine = e; }
+static inline void legacy(const char* e) {
+  g_engine = e;
+  __atomic_add_fetch(&g_legacy_calls, 1, __ATOMIC_RELAXED);
+}
+
 extern "C" {
+
+const char* bpx_last_engine(void) { return g_engine; }
+long long bpx_legacy_engine_calls(void) { return __atomic_load_n(&g_legacy_calls, __ATOMIC_RELAXED); }
 
 size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
   size_t a = tc_conv_fwd_ws(n, h, w_, cin, cout), b = ts_conv_ws(cin, cout);
@@ -30,21 +47,23 @@ bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const floa
   BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w) && aligned16(w_lo));
   cudaStream_t st = as_stream(stream);
   if (c1_conv_fwd_ok(cin, cout)) {
+    use("c1");
     bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (small_conv_fwd_ok(cin, cout))
-    return small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
+    return legacy("small"), small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(x)) {
+    use("fdt");
     bpx_status_t s = fdt_conv_fwd(x, w, w_lo, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes,
                                   st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (ts_conv_ok(cin, cout))
-    return ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+    return legacy("ts"), ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
   if (tc_conv_fwd_ok(n, h, w_, cin, cout))
-    return tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
-  return simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
+    return legacy("tc"), tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+  return legacy("simt"), simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
 }
 
 size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
@@ -69,15 +88,16 @@ bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w, const f
   BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w) && aligned16(w_lo));
   cudaStream_t st = as_stream(stream);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(dz) && (!mask_src || aligned16(mask_src))) {
+    use("fdt");
     bpx_status_t s = fdt_conv_dgrad(dz, w, w_lo, mask_src, dx, n, h, w_, cin, cout, ws,
                                     ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (ts_conv_ok(cin, cout))
-    return ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return legacy("ts"), ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_dgrad_ok(n, h, w_, cin, cout))
-    return tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
-  return simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st);
+    return legacy("tc"), tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+  return legacy("simt"), simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st);
 }
 
 size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
@@ -100,14 +120,14 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   cudaStream_t st = as_stream(stream);
   if (wgt_conv_ok(cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
       (!dbias || aligned16(dbias)))
-    return wgt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return use("wgt"), wgt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (small_conv_wgrad_ok(cin, cout) && aligned16(dz))
-    return small_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return legacy("small"), small_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (wg_conv_ok(cin, cout))
-    return wg_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return legacy("wg"), wg_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (tc_conv_wgrad_ok(n, h, w_, cin, cout))
-    return tc_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
-  return simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return legacy("tc"), tc_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+  return legacy("simt"), simt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
 }
 
 static size_t max3(size_t a, size_t b, size_t c) {
@@ -139,17 +159,18 @@ bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, f
   BPX_CHECK_ARG(x && w && y && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
   if (dtc_linear_ok(b, in, out)) {
+    use("dtc");
     bpx_status_t s = dtc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (dns_linear_ok(b, in, out))
-    return dns_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+    return use("dns"), dns_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
   // pixel-batched dense ops (the 1x1 convs of the four-tower net: b = pixels)
   // also go to the tensor-core engine: the FFMA fallback's fwd orientation
   // took ~3 ms at b = 39200, in = 128, out = 32
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))
-    return tc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
-  return simt_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+    return use("tc"), tc_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+  return legacy("simt"), simt_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
 }
 
 bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask_src,
@@ -158,14 +179,15 @@ bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask
   BPX_CHECK_ARG(dy && w && dx && b >= 0 && in > 0 && out > 0 && aligned16(w));
   cudaStream_t st = as_stream(stream);
   if (dtc_linear_ok(b, in, out)) {
+    use("dtc");
     bpx_status_t s = dtc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (dns_linear_ok(b, in, out))
-    return dns_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+    return use("dns"), dns_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))
-    return tc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
-  return simt_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+    return use("tc"), tc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+  return legacy("simt"), simt_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
 }
 
 bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias,
@@ -177,14 +199,15 @@ bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float*
   // but the FFMA outer product's math grows with b (B200, fc1: 189 vs 93 us
   // at b = 32, 118 vs 91 at 16; at b <= 8 the FFMA kernel is ~14 us faster)
   if (b > 8 && dwt_linear_ok(b, in, out)) {
+    use("dwt");
     bpx_status_t s = dwt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (dns_linear_ok(b, in, out))
-    return dns_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+    return use("dns"), dns_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))
-    return tc_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
-  return simt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+    return use("tc"), tc_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+  return legacy("simt"), simt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
 }
 
 // Engine-pinned variants for tests and benchmarks (same semantics).

@@ -32,7 +32,7 @@ import torch
 from . import ops
 from .comm import LocalComm, TorchComm
 from .costs import shard_range
-from .errors import GraphFormatError, UnsupportedTopologyError
+from .errors import GraphCaptureError, GraphFormatError, UnsupportedTopologyError
 from .graph import CompGraph, ceil_div
 from .network import LayerSpec, NetSpec, init_params, net_for_graph, synthetic_batch
 from .planner import TrainingPlan
@@ -601,22 +601,27 @@ class BurstStep:
         return segs
 
     def _graph_or_eager(self, ops, pool):
-        """A CUDA graph of ``ops``; if capture fails (e.g. a communication
-        backend whose ops cannot be captured), the same ops replayed
-        eagerly -- identical results, more launch overhead -- with a
-        warning instead of a crash."""
+        """A CUDA graph of ``ops``.  A failed capture is fatal
+        (GraphCaptureError): replaying eagerly would silently change what
+        is measured.  ``BPX_ALLOW_EAGER_REPLAY=1`` opts into the eager
+        replay (same results, more launch overhead) for debugging."""
         g = torch.cuda.CUDAGraph()
         try:
             with torch.cuda.graph(g, pool=pool):
                 self.run_ops(ops)
             return g
-        except Exception as exc:                      # pragma: no cover (multi-GPU only)
+        except Exception as exc:                      # pragma: no cover (GPU only)
             import sys
             torch.cuda.synchronize()
             if self.op_events is not None:
                 self.op_events.clear()
+            if os.environ.get("BPX_ALLOW_EAGER_REPLAY", "") != "1":
+                raise GraphCaptureError(
+                    f"CUDA-graph capture of the step failed ({type(exc).__name__}: {exc})"
+                ) from exc
             print(f"[bpx] CUDA-graph capture failed ({type(exc).__name__}: {exc}); "
-                  "replaying the op program eagerly", file=sys.stderr)
+                  "replaying the op program eagerly (BPX_ALLOW_EAGER_REPLAY=1)",
+                  file=sys.stderr)
             return _EagerReplay(self, ops)
 
     def loss(self) -> float:

@@ -28,6 +28,8 @@ _SIGS = {
     "bpx_abi_version": (ctypes.c_int, []),
     "bpx_device_supported": (ctypes.c_int, []),
     "bpx_launch_count": (ctypes.c_longlong, []),
+    "bpx_last_engine": (ctypes.c_char_p, []),
+    "bpx_legacy_engine_calls": (ctypes.c_longlong, []),
     "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
@@ -134,6 +136,17 @@ def load_library(path: str = LIB_PATH):
 def launch_count() -> int:
     """Kernel launches issued through libbpx by this process so far."""
     return int(load_library().bpx_launch_count())
+
+
+def last_engine() -> str:
+    """Engine that served this thread's last conv3x3 / linear call
+    (fdt, wgt, c1, dtc, dwt, dns, tc; legacy: simt, ts, wg, small)."""
+    return load_library().bpx_last_engine().decode()
+
+
+def legacy_engine_calls() -> int:
+    """conv / dense calls this process sent to a legacy engine."""
+    return int(load_library().bpx_legacy_engine_calls())
 
 
 def _check(status: int, what: str) -> None:

@@ -42,3 +42,24 @@ def test_own_arm_fails_without_gpu():
     p = _run("--steps", "1", "--warmup", "3", timeout=300)
     assert not [l for l in p.stdout.splitlines() if l.startswith("{")], p.stdout[-1000:]
     assert "CUDA" in p.stderr or "NVIDIA" in p.stderr or "cuda" in p.stderr
+
+
+def test_b200_plan_report_picks_the_fastest_amp():
+    sys.path.insert(0, ROOT)
+    import bench
+    for world in (2, 4, 8):
+        r = bench.b200_plan_report(world)
+        ok = [a for a in r["amps"] if "bp_predicted_us" in a]
+        assert ok and r["bp_star_predicted_us"] == min(a["bp_predicted_us"] for a in ok)
+        assert all(max(a["gpus_per_layer"]) <= world for a in ok)
+        # overlapping the allreduce with the backward never predicts slower
+        assert r["dp_overlapped_predicted_us"] <= r["dp_serial_predicted_us"]
+    one = bench.b200_plan_report(1)
+    assert one["dp_overlapped_predicted_us"] == pytest.approx(one["dp_serial_predicted_us"])
+
+
+def test_host_timings_of_the_planner_and_simulator():
+    sys.path.insert(0, ROOT)
+    import bench
+    h = bench.host_timings(8)
+    assert 0 < h["plan_ms_median_of_20"] < 1000 and h["simulate_two_phase_bp_col_s"] > 0

@@ -259,3 +259,54 @@ def test_signal_barrier_single_rank():
     ops.signal_barrier([pad.data_ptr()], 0, 7)
     torch.cuda.synchronize()
     assert pad.item() == 7
+
+
+# ---- engine dispatch at the benchmarked per-GPU batches ----------------------
+# Every VGG-16 conv / dense op at b = 32 (bench, N=1), 8 and 4 (the C1 plan's
+# 4- and 8-GPU segments) must be served by a TMA tensor-core engine (or, for
+# the <= 8-row dense weight gradient and the 1000-output classifier, the
+# dense FFMA kernels chosen for them by measurement) -- never by a legacy
+# engine (simt / ts / tc / wg / small).
+ALLOWED = {
+    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgt"}},
+    "dense": {"fwd": {"dtc", "dns"}, "dgrad": {"dtc", "dns"}, "wgrad": {"dwt", "dns"}},
+}
+
+
+@pytest.mark.parametrize("b", [4, 8, 32])
+def test_vgg16_ops_take_tensor_core_engines(b):
+    from paper_2112_10065_b200.network import vgg16
+    net = vgg16()
+    ws = ops.Workspace(torch.device(DEV))
+    seen = []
+    for i, sp in enumerate(net.layers):
+        if sp.kind not in ("conv", "dense"):
+            continue
+        x = torch.zeros(sp.in_shape(b), device=DEV)
+        dy = torch.zeros(sp.out_shape(b), device=DEV)
+        y = torch.empty_like(dy)
+        dx = torch.empty_like(x)
+        shapes = sp.param_shapes()
+        w = torch.zeros(shapes[0], device=DEV)
+        bias = torch.zeros(shapes[1], device=DEV)
+        dw, db = torch.empty_like(w), torch.empty_like(bias)
+        calls = []
+        if sp.kind == "conv":
+            ws.reserve(ops.conv_workspace_bytes(b, sp.hw, sp.hw, sp.cin, sp.cout))
+            calls.append(("fwd", lambda: ops.conv3x3_fwd(x, w, bias, y, relu=True, ws=ws)))
+            calls.append(("wgrad", lambda: ops.conv3x3_wgrad(x, dy, dw, db, ws=ws)))
+            if i > 0:
+                calls.append(("dgrad", lambda: ops.conv3x3_dgrad(dy, w, x, dx, ws=ws)))
+        else:
+            ws.reserve(ops.linear_workspace_bytes(b, sp.cin, sp.cout))
+            x2, dx2 = x.view(b, sp.cin), dx.view(b, sp.cin)
+            calls.append(("fwd", lambda: ops.linear_fwd(x2, w, bias, y, sp.relu, ws=ws)))
+            calls.append(("wgrad", lambda: ops.linear_wgrad(x2, dy, dw, db, ws=ws)))
+            calls.append(("dgrad", lambda: ops.linear_dgrad(dy, w, x2, dx2, ws=ws)))
+        for op, fn in calls:
+            fn()
+            eng = ops.last_engine()
+            seen.append((sp.name, op, eng))
+            assert eng in ALLOWED[sp.kind][op], (b, sp.name, op, eng)
+        torch.cuda.synchronize()
+    assert len(seen) == 3 * 16 - 1
