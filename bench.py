@@ -340,10 +340,22 @@ def bench_reference(args):
 
 def bench_ours(args):
     world, rank, local = _dist()
+    # fewer GPUs than ranks (the 1-GPU lease): every rank shares cuda:0 and
+    # the data path runs through the P2P backend (PeerComm over CUDA IPC;
+    # NCCL cannot place two ranks on one GPU), gloo carrying only handles
+    # and scalars.  A correctness run of the multi-GPU program, not a
+    # throughput number (config.shared_gpu).
+    shared = world > 1 and torch.cuda.device_count() < world
+    if shared:
+        os.environ["BPX_COMM"] = "peer"
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2112_10065_b200 import ops, synth
     from paper_2112_10065_b200.executor import BurstStep, _dist_comm, run
     from paper_2112_10065_b200.network import synthetic_batch
@@ -395,6 +407,7 @@ def bench_ours(args):
         e1.record()
         torch.cuda.synchronize()
     comm.barrier()
+    comm.check()
     ms = e0.elapsed_time(e1)
     ms = comm.max_scalar(ms, st.device)
     value = GLOBAL_BATCH * args.steps / (ms / 1000.0)
@@ -467,6 +480,8 @@ def bench_ours(args):
                        "global_batch": GLOBAL_BATCH,
                        "gpus_per_layer": [g for _, g in p.assignments],
                        "parallelism": f"burst{world}",
+                       "comm": type(comm).__name__,
+                       "shared_gpu": shared,
                        "l2": "working set ~2.2 GB > 126 MB L2, no flush needed",
                        "cuda_graph": captured},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
@@ -496,6 +511,10 @@ def bench_ours(args):
 
 
 def main():
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # the P2P backend's device barriers spin: every kernel must be loaded
+        # before the first one (PeerComm docstring); set before CUDA starts
+        os.environ["CUDA_MODULE_LOADING"] = "EAGER"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -232,6 +232,17 @@ BPX_API bpx_status_t bpx_signal_barrier(uint32_t* const* pads, int rank, int g,
 BPX_API bpx_status_t bpx_signal_barrier_dev(uint32_t* const* pads, uint32_t* counter,
                                     int rank, int g, void* stream);
 
+/* Bounded barrier of the P2P backend: the device-epoch protocol of
+ * bpx_signal_barrier_dev over pads[0..g) (pads[r] = rank r's g slots for
+ * this group), but a waiter stops after timeout_ns without a peer's arrival
+ * or as soon as its own abort word (aborts[rank]) is nonzero; it then
+ * writes the reason into *status (1 = timeout, 2 = aborted; atomic max),
+ * raises every participant's abort word and returns.  The caller reads
+ * *status after the phase and fails the step (no hang on a dead peer).    */
+BPX_API bpx_status_t bpx_peer_barrier(uint32_t* const* pads, uint32_t* const* aborts,
+                              uint32_t* counter, uint32_t* status, int rank, int g,
+                              unsigned long long timeout_ns, void* stream);
+
 /* ---- engine-pinned variants (tests / benchmarks): force the FFMA
  * implicit-GEMM engine regardless of shape, same semantics as above.      */
 BPX_API bpx_status_t bpx_simt_conv3x3_fwd(const float* x, const float* w,

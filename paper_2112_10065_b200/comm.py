@@ -97,136 +97,155 @@ class TorchComm:
             return
         self.dist.all_reduce(flat, op=self.dist.ReduceOp.SUM, group=self.groups[g])
 
+    def _scalar_device(self, device):
+        # gloo reduces host tensors; NCCL needs device tensors
+        return "cpu" if self.dist.get_backend() == "gloo" else device
+
     def max_scalar(self, value: float, device) -> float:
-        t = torch.tensor([value], dtype=torch.float64, device=device)
+        t = torch.tensor([value], dtype=torch.float64, device=self._scalar_device(device))
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_scalar(self, value: float, device) -> float:
-        t = torch.tensor([value], dtype=torch.float64, device=device)
+        t = torch.tensor([value], dtype=torch.float64, device=self._scalar_device(device))
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return float(t.item())
 
     def barrier(self):
         self.dist.barrier()
 
+    def allgather_object(self, obj) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def check(self) -> None:
+        pass
+
 
 class PeerComm:
     """P2P backend of the step's communication (north_star (2)-(3)): peer
     memory instead of NCCL for the data path, every op graph-capturable.
 
-    Each rank owns one device arena -- signal pads, per-group-size epoch
-    counters and a staging area -- whose CUDA IPC handle is exchanged once
-    through torch.distributed (any backend: only handles and scalars go
-    through it).  Peers map each other's arenas (NVLink peer addresses on a
-    multi-GPU box; the same device for two processes sharing one GPU).
+    * Control arena (one per rank, mapped by every peer through CUDA IPC
+      once, at construction): signal pads and an epoch counter per group
+      size, an abort word and a status word.  Barriers are
+      ``bpx_peer_barrier``: device-resident epochs (a captured step replays
+      correctly), bounded by ``BPX_BARRIER_TIMEOUT_S`` (default 60 s) and
+      by the abort words -- a dead or late peer fails the step with
+      ``CommError`` (``check``) instead of hanging it.
+    * Symmetric heaps (``make_heap``, collective): every buffer that a peer
+      reads -- the producer side of each reshard (layer outputs, data
+      gradients, shortcut gradients) and the gradient buckets -- lives in a
+      per-rank arena whose handle and per-key offsets are exchanged once,
+      so kernels pull straight out of the producer's buffer: no staging
+      copy (SymHeap.reshard / SymHeap.allreduce).
+    torch.distributed (any backend) carries only handles and scalars.  On a
+    multi-GPU box peers are NVLink addresses; in tests several processes
+    share one GPU.  Processes must load their kernels eagerly
+    (``CUDA_MODULE_LOADING=EAGER`` before CUDA initialises): with lazy
+    loading a kernel's first launch can wait on the device while a peer's
+    barrier kernel spins waiting on this process."""
 
-    * reshard (the `transfer` op, simulator.py:242-253): each source rank
-      stages its shard, a device barrier over the participants, then every
-      destination rank pulls its contiguous runs (costs.reshard_segments)
-      from the sources' staging areas with ``bpx_reshard_pull``, and a second
-      barrier before the staging areas may be reused;
-    * allreduce over ranks [0, g) (`allreduce`, :264-278): stage, barrier,
-      one-shot pull-sum in rank order (``bpx_allreduce_sum_prefix``: the
-      same bits on every rank), barrier.
-    Barriers are ``bpx_signal_barrier_dev`` (device-resident epochs), so a
-    captured step replays correctly.  Call ``prepare`` (collective) before
-    use: BurstStep does, with its largest shard and gradient bucket.
-
-    Processes must load their kernels eagerly (``CUDA_MODULE_LOADING=EAGER``
-    before CUDA initialises): with lazy loading, a kernel's first launch can
-    wait on the device while a peer's barrier kernel spins waiting on this
-    process -- a deadlock."""
-
-    def __init__(self, rank: int, world: int, group_sizes=(), device=None):
+    def __init__(self, rank: int, world: int, group_sizes=(), device=None,
+                 timeout_s: Optional[float] = None):
         import os
         import warnings
         if os.environ.get("CUDA_MODULE_LOADING", "").upper() != "EAGER":
             warnings.warn("PeerComm: set CUDA_MODULE_LOADING=EAGER before CUDA starts; "
                           "lazy kernel loading can deadlock with device barriers")
+        from . import ops
+        self._ops = ops
         self.rank, self.world = rank, world
         self.host = TorchComm(rank, world, ())   # handle exchange, scalars, host barrier
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
-        self.arena = None
+        if timeout_s is None:
+            timeout_s = float(os.environ.get("BPX_BARRIER_TIMEOUT_S", "60"))
+        self.timeout_ns = int(timeout_s * 1e9)
+        W = world
+        # uint32 words: pads [g][r] for g = 0..W, counters [g], abort, status
+        self._pad0, self._cnt0 = 0, W * (W + 1)
+        self._abort = self._cnt0 + W + 1
+        self._status = self._abort + 1
+        words = (self._status + 1 + 63) // 64 * 64
+        self.ctl = torch.zeros(words, dtype=torch.int32, device=self.device)
+        self.peer_ctl, self._ctl_maps = self._exchange(self.ctl)
+        self._heaps = []          # every heap stays mapped while this comm lives
 
-    def prepare(self, stage_bytes: int) -> None:
-        from . import ops
-        W = self.world
-        pad_bytes = 4 * W * (W + 1)               # pads for group sizes 1..W, W slots each
-        cnt_bytes = 4 * (W + 1)                   # one epoch counter per group size
-        head = (pad_bytes + cnt_bytes + 255) // 256 * 256
-        size = head + max(16, (stage_bytes + 255) // 256 * 256)
-        if self.arena is not None and self.arena.numel() >= size:
-            return
-        self.arena = torch.zeros(size, dtype=torch.uint8, device=self.device)
-        self.head = head
-        self.pad_bytes = pad_bytes
-        handle = self.arena.untyped_storage()._share_cuda_()
-        handles = [None] * W
-        self.host.dist.all_gather_object(handles, handle)
-        self.peer_storages = []
-        self.peer_base = []
-        for r in range(W):
+    def _exchange(self, t: torch.Tensor, meta=None):
+        """All ranks: share ``t``'s CUDA IPC handle (+ metadata), map every
+        peer's; returns (base addresses per rank, [storages | metadata])."""
+        handle = t.untyped_storage()._share_cuda_()
+        got = self.host.allgather_object((handle, meta))
+        bases, keep, metas = [], [], []
+        for r, (h, m) in enumerate(got):
+            metas.append(m)
             if r == self.rank:
-                self.peer_base.append(self.arena.data_ptr())
-                self.peer_storages.append(None)
+                bases.append(t.data_ptr())
+                keep.append(None)
             else:
-                st = torch.UntypedStorage._new_shared_cuda(*handles[r])
-                self.peer_storages.append(st)     # keeps the mapping alive
-                # the handle covers the caching allocator's block; the arena
-                # starts at the storage's offset inside it (handle[3])
-                self.peer_base.append(st.data_ptr())
-        self.host.dist.barrier()
-        self._ops = ops
+                st = torch.UntypedStorage._new_shared_cuda(*h)
+                keep.append(st)                  # keeps the mapping alive
+                bases.append(st.data_ptr())
+        self.host.barrier()
+        return bases, (keep if meta is None else (keep, metas))
 
-    # layout helpers (the same offsets in every rank's arena)
-    def _pads(self, g: int) -> list:
-        return [b + 4 * self.world * g for b in self.peer_base[:g]]
+    # ---- control arena
+    def _word(self, r: int, w: int) -> int:
+        return self.peer_ctl[r] + 4 * w
 
-    def _counter(self, g: int) -> int:
-        return self.arena.data_ptr() + self.pad_bytes + 4 * g
-
-    def _stage(self, r: int) -> int:
-        return self.peer_base[r] + self.head
-
-    def _barrier(self, g: int) -> None:
-        if g > 1 and self.rank < g:
-            self._ops.signal_barrier_dev(self._pads(g), self._counter(g), self.rank)
-
-    def _stage_view(self, nbytes: int) -> torch.Tensor:
-        return self.arena[self.head:self.head + nbytes]
-
-    def reshard(self, src: Optional[torch.Tensor], g: int, dst: Optional[torch.Tensor],
-                h: int, B: int, bytes_per_sample: int) -> None:
-        P = max(g, h)
-        if self.rank >= P:
-            return
-        if src is not None and self.rank < g:
-            sb = _bytes(src)
-            self._stage_view(sb.numel()).copy_(sb)
-        self._barrier(P)
-        if dst is not None and self.rank < h:
-            cg, ch = ceil_div(B, g), ceil_div(B, h)
-            srcs, soff, doff, nb = [], [], [], []
-            for p, q, s0, n in reshard_segments(B, g, h):
-                if q != self.rank:
-                    continue
-                srcs.append(self._stage(p))
-                soff.append((s0 - p * cg) * bytes_per_sample)
-                doff.append((s0 - q * ch) * bytes_per_sample)
-                nb.append(n * bytes_per_sample)
-            for k in range(0, len(nb), 64):
-                self._ops.reshard_pull(srcs[k:k + 64], soff[k:k + 64], dst, doff[k:k + 64],
-                                       nb[k:k + 64])
-        self._barrier(P)
-
-    def allreduce(self, flat: torch.Tensor, g: int) -> None:
+    def barrier_dev(self, g: int) -> None:
+        """Bounded device barrier over ranks [0, g) (stream-ordered)."""
         if g <= 1 or self.rank >= g:
             return
-        self._stage_view(flat.numel() * 4).copy_(_bytes(flat))
-        self._barrier(g)
-        self._ops.allreduce_sum_prefix([self._stage(r) for r in range(g)], flat, flat.numel())
-        self._barrier(g)
+        W = self.world
+        self._ops.peer_barrier([self._word(r, self._pad0 + g * W) for r in range(g)],
+                               [self._word(r, self._abort) for r in range(g)],
+                               self._word(self.rank, self._cnt0 + g),
+                               self._word(self.rank, self._status), self.rank, self.timeout_ns)
+
+    def status(self) -> int:
+        return int(self.ctl[self._status].item())
+
+    def check(self) -> None:
+        """Raise CommError if a device barrier of this rank timed out or was
+        aborted (synchronises with the device)."""
+        from .errors import CommError
+        st = self.status()
+        if st:
+            why = {1: "timed out waiting for a peer", 2: "was aborted by a peer"}.get(st, "failed")
+            raise CommError(f"rank {self.rank}: a P2P barrier {why} "
+                            f"(BPX_BARRIER_TIMEOUT_S={self.timeout_ns / 1e9:g})", st)
+
+    def abort(self) -> None:
+        """Raise every rank's abort word: their pending and future barriers
+        fail fast (call on a host-side error before exiting)."""
+        s = torch.cuda.Stream(device=self.device)
+        with torch.cuda.stream(s):
+            for r in range(self.world):
+                st = self._ctl_maps[r] if r != self.rank else self.ctl.untyped_storage()
+                t = torch.empty(0, dtype=torch.int32, device=self.device)
+                t.set_(st, 0, (self.ctl.numel(),), (1,))
+                t[self._abort].fill_(1)
+        s.synchronize()
+
+    # ---- symmetric heaps
+    def make_heap(self, sizes: dict) -> "SymHeap":
+        """Collective: allocate this rank's buffers ``sizes`` = {key: nbytes}
+        (keys may differ across ranks) in one IPC-shared arena and learn
+        every peer's offsets.  Returns the heap; its views are the tensors
+        the step computes into."""
+        keys = sorted(sizes, key=repr)
+        layout, off = {}, 0
+        for k in keys:
+            nb = int(sizes[k])
+            layout[k] = (off, nb)
+            off += (nb + 255) // 256 * 256
+        arena = torch.zeros(max(off, 256), dtype=torch.uint8, device=self.device)
+        bases, (keep, layouts) = self._exchange(arena, layout)
+        heap = SymHeap(self, arena, bases, layouts, keep)
+        self._heaps.append(heap)
+        return heap
 
     def max_scalar(self, value: float, device) -> float:
         return self.host.max_scalar(value, device)
@@ -236,6 +255,108 @@ class PeerComm:
 
     def barrier(self):
         self.host.barrier()
+
+    def allgather_object(self, obj) -> list:
+        return self.host.allgather_object(obj)
+
+
+class SymHeap:
+    """One BurstStep's peer-visible buffers on every rank (PeerComm.make_heap).
+
+    * ``reshard`` (the `transfer` op, simulator.py:242-253): barrier over
+      [0, max(g, h)) -- every producer has written its shard -- then each
+      consumer pulls its contiguous runs (costs.reshard_segments) straight
+      out of the producers' buffers with ``bpx_reshard_pull``, and a second
+      barrier before any producer may overwrite them;
+    * ``allreduce`` over ranks [0, g) (`allreduce`, :264-278), in place on
+      the gradient bucket: two-shot -- reduce-scatter (rank r sums chunk r
+      of all g buckets in rank order 0..g-1 into its own bucket), barrier,
+      all-gather (rank r pulls every other chunk from its owner) -- so each
+      rank reads 2(g-1)/g of the bucket over NVLink, the ring volume the
+      reference prices (costs.py:130-140); buckets below 64 floats per rank
+      take one shot (sum of all g buckets into private scratch, barrier,
+      copy back).  Every rank adds in the same order: bitwise identical
+      results on every rank, run to run."""
+
+    SMALL = 64
+
+    def __init__(self, comm: PeerComm, arena, bases, layouts, keep):
+        self.comm, self.arena, self.bases, self.layouts, self._keep = \
+            comm, arena, bases, layouts, keep
+        self.rank = comm.rank
+        self._scratch = {}
+
+    def view(self, key, shape, dtype=torch.float32) -> torch.Tensor:
+        off, nb = self.layouts[self.rank][key]
+        n = 1
+        for d in shape:
+            n *= int(d)
+        esz = torch.tensor([], dtype=dtype).element_size()
+        if n * esz > nb:
+            raise ValueError(f"heap buffer {key} holds {nb} bytes, {n * esz} requested")
+        return self.arena[off:off + n * esz].view(dtype).view(*shape)
+
+    def addr(self, r: int, key) -> int:
+        from .errors import CommError
+        ent = self.layouts[r].get(key)
+        if ent is None:
+            raise CommError(f"rank {r} has no heap buffer {key!r} (layouts disagree)")
+        return self.bases[r] + ent[0]
+
+    def reshard(self, src_key, g: int, dst: Optional[torch.Tensor], h: int, B: int,
+                bytes_per_sample: int) -> None:
+        P = max(g, h)
+        if self.rank >= P:
+            return
+        self.comm.barrier_dev(P)
+        if dst is not None and self.rank < h:
+            cg, ch = ceil_div(B, g), ceil_div(B, h)
+            srcs, soff, doff, nb = [], [], [], []
+            for p, q, s0, n in reshard_segments(B, g, h):
+                if q != self.rank:
+                    continue
+                srcs.append(self.addr(p, src_key))
+                soff.append((s0 - p * cg) * bytes_per_sample)
+                doff.append((s0 - q * ch) * bytes_per_sample)
+                nb.append(n * bytes_per_sample)
+            for k in range(0, len(nb), 64):
+                self.comm._ops.reshard_pull(srcs[k:k + 64], soff[k:k + 64], dst,
+                                            doff[k:k + 64], nb[k:k + 64])
+        self.comm.barrier_dev(P)
+
+    def allreduce(self, key, flat: torch.Tensor, g: int) -> None:
+        if g <= 1 or self.rank >= g:
+            return
+        ops, r = self.comm._ops, self.rank
+        n = flat.numel()
+        peers = [self.addr(p, key) for p in range(g)]
+        if n < self.SMALL * g:
+            buf = self._scratch.get(key)
+            if buf is None or buf.numel() < n:
+                buf = self._scratch[key] = torch.empty(n, dtype=torch.float32,
+                                                       device=flat.device)
+            self.comm.barrier_dev(g)
+            ops.allreduce_sum_prefix(peers, buf, n)
+            self.comm.barrier_dev(g)
+            flat.copy_(buf[:n])
+            return
+        c = ceil_div(ceil_div(n, g), 4) * 4            # 16-byte aligned chunks
+        lo, hi = min(n, r * c), min(n, (r + 1) * c)
+        self.comm.barrier_dev(g)
+        if hi > lo:
+            ops.allreduce_sum_prefix([a + 4 * lo for a in peers], flat[lo:hi], hi - lo)
+        self.comm.barrier_dev(g)
+        srcs, soff, doff, nb = [], [], [], []
+        for p in range(g):
+            a, b = min(n, p * c), min(n, (p + 1) * c)
+            if p != r and b > a:
+                srcs.append(peers[p])
+                soff.append(4 * a)
+                doff.append(4 * a)
+                nb.append(4 * (b - a))
+        if nb:
+            ops.reshard_pull(srcs, soff, flat, doff, nb)
+        self.comm.barrier_dev(g)
 
 
 class LocalComm:
@@ -261,4 +382,10 @@ class LocalComm:
         return value
 
     def barrier(self):
+        pass
+
+    def allgather_object(self, obj) -> list:
+        return [obj]
+
+    def check(self) -> None:
         pass

@@ -111,6 +111,61 @@ __global__ void signal_barrier_dev_kernel(PadTableDev t) {
   }
 }
 
+// Bounded barrier of the P2P backend (comm.PeerComm).  Same epoch protocol
+// as signal_barrier_dev_kernel, but a waiter gives up when a peer does not
+// arrive within timeout_ns (%globaltimer) or when any participant raised
+// its abort word: it then records the reason in this rank's status word,
+// raises every participant's abort word (so their barriers fail fast
+// instead of spinning forever) and returns.  The host reads the status
+// after the step (PeerComm.check) and raises CommError -- a dead or late
+// peer can no longer hang the job.
+struct BarrierTable {
+  unsigned int* pad[kMaxPeers];
+  unsigned int* abort_word[kMaxPeers];
+  unsigned int* counter;
+  unsigned int* status;
+  unsigned long long timeout_ns;
+  int g, rank;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void peer_barrier_kernel(BarrierTable t) {
+  __shared__ unsigned int e;
+  __shared__ int fail;
+  if (threadIdx.x == 0) {
+    e = ++(*t.counter);
+    fail = 0;
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid < t.g) {
+    __threadfence_system();
+    volatile unsigned int* slot = t.pad[tid] + t.rank;
+    *slot = e;
+    volatile unsigned int* mine = t.pad[t.rank] + tid;
+    volatile unsigned int* ab = t.abort_word[t.rank];
+    const unsigned long long t0 = global_ns();
+    unsigned int spins = 0;
+    while ((int)(*mine - e) < 0) {
+      if (*ab != 0) { atomicMax(&fail, 2); break; }
+      if ((++spins & 255u) == 0 && global_ns() - t0 > t.timeout_ns) { atomicMax(&fail, 1); break; }
+    }
+    if (*ab != 0) atomicMax(&fail, 2);         // an abort is sticky: later barriers fail too
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (fail && tid < t.g) {
+    if (tid == 0) atomicMax(t.status, (unsigned int)fail);
+    atomicExch(t.abort_word[tid], 1u);
+    __threadfence_system();
+  }
+}
+
 }  // namespace bpx
 
 using namespace bpx;
@@ -196,6 +251,25 @@ bpx_status_t bpx_signal_barrier_dev(uint32_t* const* pads, uint32_t* counter, in
   t.counter = counter;
   t.g = g; t.rank = rank;
   signal_barrier_dev_kernel<<<1, 32, 0, as_stream(stream)>>>(t);
+  return launch_status();
+}
+
+bpx_status_t bpx_peer_barrier(uint32_t* const* pads, uint32_t* const* aborts,
+                              uint32_t* counter, uint32_t* status, int rank, int g,
+                              unsigned long long timeout_ns, void* stream) {
+  BPX_CHECK_ARG(pads && aborts && counter && status && g >= 1 && g <= kMaxPeers &&
+                rank >= 0 && rank < g && timeout_ns > 0);
+  BarrierTable t{};
+  for (int r = 0; r < g; ++r) {
+    BPX_CHECK_ARG(pads[r] != nullptr && aborts[r] != nullptr);
+    t.pad[r] = pads[r];
+    t.abort_word[r] = aborts[r];
+  }
+  t.counter = counter;
+  t.status = status;
+  t.timeout_ns = timeout_ns;
+  t.g = g; t.rank = rank;
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t);
   return launch_status();
 }
 

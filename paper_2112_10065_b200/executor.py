@@ -114,9 +114,6 @@ class BurstStep:
         # parameters live in flat buffers with the same layout as the gradient
         # buckets, so the SGD update is one launch per bucket
         self.pbuckets: dict[int, torch.Tensor] = {}
-        for g, n in sizes.items():
-            self.buckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
-            self.pbuckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
         cursor = {g: 0 for g in sizes}
 
         names = {L.spec.name: i for i, L in enumerate(self.layers)}
@@ -161,6 +158,25 @@ class BurstStep:
             else:
                 L.src_i = names[sp.src] if sp.src is not None else i - 1
 
+        # P2P backend: every buffer a peer reads lives in a symmetric heap
+        # (PeerComm.make_heap, collective): the producer side of each
+        # reshard and the gradient buckets of g > 1
+        self.heap = None
+        sym = self._peer_visible(sizes) if hasattr(self.comm, "make_heap") else {}
+        if hasattr(self.comm, "make_heap"):
+            self.heap = self.comm.make_heap(sym)
+        for g, n in sizes.items():
+            if ("bucket", g) in sym:
+                self.buckets[g] = self.heap.view(("bucket", g), (n,))
+            else:
+                self.buckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
+            self.pbuckets[g] = torch.zeros(n, dtype=torch.float32, device=dev)
+
+        def _buf(key, shape):
+            if key in sym:
+                return self.heap.view(key, shape)
+            return torch.empty(shape, dtype=torch.float32, device=dev)
+
         ws_need = 0
         for i, L in enumerate(self.layers):
             sp = L.spec
@@ -175,7 +191,7 @@ class BurstStep:
                 L.x = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
             else:
                 L.x = src.y.view(sp.in_shape(L.b))
-            L.y = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+            L.y = _buf(("y", i), sp.out_shape(L.b))
             if sp.kind == "pool" and hasattr(self.k, "maxpool2x2_fwd_idx"):
                 L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
             if sp.kind == "pool3":
@@ -184,7 +200,7 @@ class BurstStep:
             if src is not None:
                 last = consumers[L.src_i][-1] == i
                 if L.reshard_in or not last:
-                    L.dx = torch.empty(sp.in_shape(L.b), dtype=torch.float32, device=dev)
+                    L.dx = _buf(("dx", i), sp.in_shape(L.b))
                     L.dx_acc = not L.reshard_in
                 else:
                     L.dx = src.dy.view(sp.in_shape(L.b))
@@ -217,7 +233,7 @@ class BurstStep:
                 else:
                     L.s = S.y
                 if L.join != "fused" and L.join != "direct":
-                    L.dskip = torch.empty(sshape, dtype=torch.float32, device=dev)
+                    L.dskip = _buf(("dskip", i), sshape)
             ps = sp.param_shapes()
             if ps:
                 w, b = params[sp.name]
@@ -265,23 +281,6 @@ class BurstStep:
                 S = self.layers[L.skip_i]
                 if S.active:
                     L.dskip_src = torch.empty_like(S.y)
-        if hasattr(self.comm, "prepare"):
-            # P2P backend: one staging area per rank, sized from the plan only
-            # (identical on every rank: the call is collective)
-            stage = 0
-            for i, L in enumerate(self.layers):
-                if self._chain_transfer(i):
-                    bps = 4 * L.spec.in_elems()
-                    stage = max(stage, ceil_div(self.B, self.layers[i - 1].g) * bps,
-                                ceil_div(self.B, L.g) * bps)
-                if L.join == "reshard":
-                    bps = 4 * self.layers[L.skip_i].spec.out_elems()
-                    stage = max(stage, ceil_div(self.B, L.g) * bps,
-                                ceil_div(self.B, self.layers[L.skip_i].g) * bps)
-            for g, n in sizes.items():
-                if g > 1:
-                    stage = max(stage, 4 * n)
-            self.comm.prepare(stage)
         self.ws = self.k.Workspace(dev)
         self.ws.reserve(ws_need)
         last = self.layers[-1]
@@ -289,6 +288,32 @@ class BurstStep:
         self.labels = torch.zeros(max(last.b, 1), dtype=torch.int32, device=dev)
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self.op_events: Optional[list] = None
+
+    def _peer_visible(self, bucket_sizes: dict) -> dict:
+        """{heap key: nbytes} of this rank's buffers that peers read: the
+        output of a layer whose consumer runs on another GPU count (forward
+        reshard source), the data gradient of such a consumer (backward
+        reshard source), a resharded shortcut's source output and gradient,
+        the gradient buckets of g > 1, and the loss partial."""
+        out = {}
+        for i, L in enumerate(self.layers):
+            if self._chain_transfer(i):
+                P = self.layers[i - 1]
+                if P.active:
+                    out[("y", i - 1)] = 4 * P.spec.out_elems() * P.b
+                if L.active:
+                    out[("dx", i)] = 4 * L.spec.in_elems() * L.b
+            if L.join == "reshard":
+                S = self.layers[L.skip_i]
+                if S.active:
+                    out[("y", L.skip_i)] = 4 * S.spec.out_elems() * S.b
+                if L.active:
+                    out[("dskip", i)] = 4 * S.spec.out_elems() * L.b
+        for g, n in bucket_sizes.items():
+            if g > 1:
+                out[("bucket", g)] = 4 * n
+        out[("loss",)] = 16
+        return out
 
     # ------------------------------------------------------------ data
     @property
@@ -371,7 +396,14 @@ class BurstStep:
         L = self.layers[i]
         S = self.layers[L.skip_i]
         bps = 4 * S.spec.out_elems()
-        if not backward:
+        if self.heap is not None:
+            if not backward:
+                self.heap.reshard(("y", L.skip_i), S.g, L.s if L.active else None, L.g,
+                                  self.B, bps)
+            else:
+                self.heap.reshard(("dskip", i), L.g, L.dskip_src if S.active else None, S.g,
+                                  self.B, bps)
+        elif not backward:
             self.comm.reshard(S.y if S.active else None, S.g,
                               L.s if L.active else None, L.g, self.B, bps)
         else:
@@ -471,7 +503,14 @@ class BurstStep:
     def _reshard(self, i: int, backward: bool) -> None:
         prev, L = self.layers[i - 1], self.layers[i]
         bps = 4 * L.spec.in_elems()
-        if not backward:
+        if self.heap is not None:
+            if not backward:
+                self.heap.reshard(("y", i - 1), prev.g, L.x if L.active else None, L.g,
+                                  self.B, bps)
+            else:
+                self.heap.reshard(("dx", i), L.g, prev.dy if prev.active else None, prev.g,
+                                  self.B, bps)
+        elif not backward:
             self.comm.reshard(prev.y if prev.active else None, prev.g,
                               L.x if L.active else None, L.g, self.B, bps)
         else:
@@ -526,10 +565,15 @@ class BurstStep:
                                      lambda j=j: self._skip_accumulate(j)))
         for g in sorted(self.buckets, reverse=True):
             if g > 1:
-                prog.append((("allreduce", g, "sync"),
-                             lambda g=g: self.comm.allreduce(self.buckets[g], g)))
+                prog.append((("allreduce", g, "sync"), lambda g=g: self._allreduce(g)))
         prog.append((("sgd", 0, "update"), self._sgd))
         return prog
+
+    def _allreduce(self, g: int) -> None:
+        if self.heap is not None:
+            self.heap.allreduce(("bucket", g), self.buckets[g], g)
+        else:
+            self.comm.allreduce(self.buckets[g], g)
 
     def _loss(self) -> None:
         last = self.layers[-1]
@@ -627,6 +671,14 @@ class BurstStep:
     def loss(self) -> float:
         """Global mean loss (sum of shard partials over the last layer's g)."""
         last = self.layers[-1]
+        if self.heap is not None:
+            part = self.heap.view(("loss",), (1,))
+            if last.active:
+                part.copy_(self.loss_buf[:1])
+            self.heap.allreduce(("loss",), part, last.g)
+            val = float(part.item())
+            self.comm.check()
+            return val
         part = self.loss_buf[:1].clone() if last.active else torch.zeros(1, device=self.device)
         if last.g > 1:
             self.comm.allreduce(part, last.g)
@@ -687,17 +739,31 @@ def _pad4(n: int) -> int:
 # reference-shaped entry points
 
 
-def _dist_comm(plan_gs):
-    """NCCL/gloo collectives by default; ``BPX_COMM=peer`` selects the P2P
-    backend (comm.PeerComm: libbpx pull kernels over IPC-mapped peer memory,
-    needs CUDA_MODULE_LOADING=EAGER)."""
+_COMMS: dict = {}
+
+
+def _dist_comm(plan_gs=()):
+    """The process's communicator for the default torch.distributed world:
+    NCCL/gloo collectives by default, ``BPX_COMM=peer`` selects the P2P
+    backend (comm.PeerComm: libbpx kernels over IPC-mapped peer memory,
+    needs CUDA_MODULE_LOADING=EAGER).  One instance per (backend, world),
+    created collectively with every prefix group [0, g), g = 2..world, and
+    reused by every run / sweep point (no per-call groups or arenas)."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        if os.environ.get("BPX_COMM", "").lower() == "peer":
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        return LocalComm()
+    world, rank = dist.get_world_size(), dist.get_rank()
+    peer = os.environ.get("BPX_COMM", "").lower() == "peer"
+    key = ("peer" if peer else "torch", world, id(dist.group.WORLD))
+    comm = _COMMS.get(key)
+    if comm is None:
+        if peer:
             from .comm import PeerComm
-            return PeerComm(dist.get_rank(), dist.get_world_size(), plan_gs)
-        return TorchComm(dist.get_rank(), dist.get_world_size(), plan_gs)
-    return LocalComm()
+            comm = PeerComm(rank, world, range(2, world + 1))
+        else:
+            comm = TorchComm(rank, world, range(2, world + 1))
+        _COMMS[key] = comm
+    return comm
 
 
 def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
@@ -733,8 +799,14 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         bg = BgJob(bg_graph, config, seed=seed + 1)
     mux = Multiplexer(st, bg, config, sensitive, measure_ops=measure_ops)
     trace = SimTrace()
-    trace = mux.run(iterations, inputs, trace, rank=comm.rank,
-                    comm=comm if comm.world > 1 else None)
+    try:
+        trace = mux.run(iterations, inputs, trace, rank=comm.rank,
+                        comm=comm if comm.world > 1 else None)
+        comm.check()
+    except BaseException:
+        if hasattr(comm, "abort"):
+            comm.abort()             # peers' barriers fail fast instead of spinning
+        raise
     base = baseline_fg_iteration_us or tl.predicted_fg_iteration_us
     metrics = metrics_from_trace(trace, n_gpus, tl.global_batch, tl.bg_batch, config,
                                  iterations, base)
@@ -771,13 +843,19 @@ def run_two_phase(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
     flags: frozenset = frozenset()
     bg = None
     trace, metrics = None, None
+    comm = st.comm
     for _ in range(feedback_rounds):
         trace, metrics = run(plan, graph, n_gpus, bg_graph, config, iterations, flags,
                              baseline_fg_iteration_us, step=st, bg=bg, measure_ops=True,
                              **kw)
         bg = trace.bg_job
         trace.op_isolated.update(isolated)
-        new = feedback_update(trace, config, flags)
+        # every rank flags from its own op durations; the union is the one
+        # global flag set the reference computes (feedback_update over all
+        # ops), so every rank protects the same ops and leaves the loop at
+        # the same round (same number of collective run() calls)
+        mine = feedback_update(trace, config, flags)
+        new = frozenset().union(*comm.allgather_object(sorted(mine)))
         if new == flags:
             break
         flags = new

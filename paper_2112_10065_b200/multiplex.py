@@ -132,6 +132,11 @@ class Multiplexer:
         qi = 0
         ends = []
         op_acc: dict[str, list] = {}
+        # busy intervals of this GPU (measure_ops only: per-op CUDA events of
+        # the foreground replays, start/end events of the background chunks);
+        # the reference's utilisation is the union of per-op busy intervals
+        busy: list = []
+        bg_spans: list = []
         # Inputs arrive end to end every iteration, pipelined: the H2D copy of
         # iteration it+1 runs on a copy stream into a staging buffer while
         # iteration it computes; the step then takes it with one D2D copy.
@@ -174,11 +179,17 @@ class Multiplexer:
                 with torch.cuda.stream(self.bg_stream):
                     if hold is not None:
                         self.bg_stream.wait_event(hold)
+                    s0 = None
+                    if self.measure:
+                        s0 = torch.cuda.Event(enable_timing=True)
+                        s0.record(self.bg_stream)
                     bg.chunks[bg_next].replay()
                     e = torch.cuda.Event(enable_timing=True)
                     e.record(self.bg_stream)
                 closes = bg_next == len(bg.chunks) - 1
                 outstanding.append((e, closes))
+                if s0 is not None:
+                    bg_spans.append((s0, e))
                 bg_next = 0 if closes else bg_next + 1
 
         while qi < len(seg_queue) or fg_pending:
@@ -216,7 +227,7 @@ class Multiplexer:
                 if last:
                     ends.append(e)
                     if self.measure:
-                        _collect(fg, self.events, op_acc)
+                        _collect(fg, self.events, op_acc, ev0, busy)
             if hold is not None and hold.query():
                 hold = None
             time.sleep(0)
@@ -228,10 +239,16 @@ class Multiplexer:
             if comm is not None:
                 t = int(comm.max_scalar(float(t), fg.device))
             tr.iteration_ticks.append(t)
-            tr.busy.setdefault(rank, []).append((prev, t))
             tr.events.append((t, rank, FG_TASK, f"iteration#{it}", "end"))
             prev = t
         tr.stop_tick = prev
+        if self.measure:
+            busy.extend((_tick(ev0, a), _tick(ev0, b)) for a, b in bg_spans)
+            if comm is not None:
+                for r, spans in enumerate(comm.allgather_object(busy)):
+                    tr.busy.setdefault(r, []).extend(spans)
+            else:
+                tr.busy.setdefault(rank, []).extend(busy)
         for name, vals in op_acc.items():
             tr.op_durations.setdefault(name, []).extend(vals)
         tr.loss = float(fg.loss_buf[0].item())
@@ -242,9 +259,10 @@ def _tick(ev0, e) -> int:
     return us_to_ticks(ev0.elapsed_time(e) * 1000.0)
 
 
-def _collect(step, events, acc) -> None:
+def _collect(step, events, acc, ev0=None, busy=None) -> None:
     """Per-op durations (ms -> us) of the last completed foreground replay,
-    fwd and bwd halves of an op summed (the reference's op granularity)."""
+    fwd and bwd halves of an op summed (the reference's op granularity);
+    with ``busy`` also the ops' (start, end) ticks relative to ``ev0``."""
     starts = {}
     per = {}
     for (key, what), ev in events:
@@ -253,5 +271,7 @@ def _collect(step, events, acc) -> None:
         elif key in starts:
             name = op_name(step, key)
             per[name] = per.get(name, 0.0) + starts[key].elapsed_time(ev) * 1000.0
+            if busy is not None:
+                busy.append((_tick(ev0, starts[key]), _tick(ev0, ev)))
     for name, us in per.items():
         acc.setdefault(name, []).append(us)

@@ -99,6 +99,9 @@ _SIGS = {
                                                 ctypes.c_void_p]),
     "bpx_signal_barrier_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                                ctypes.c_int, ctypes.c_void_p]),
+    "bpx_peer_barrier": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_ulonglong, ctypes.c_void_p]),
     "bpx_signal_barrier": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_uint32,
                                           ctypes.c_void_p]),
@@ -520,6 +523,18 @@ def allreduce_sum_prefix(peer_ptrs: Sequence[int], out: torch.Tensor, n: int):
     _check(lib.bpx_allreduce_sum_prefix(ctypes.cast(arr, ctypes.c_void_p),
                                         len(peer_ptrs), _ptr(out), int(n), _stream()),
            "bpx_allreduce_sum_prefix")
+
+
+def peer_barrier(pad_ptrs: Sequence[int], abort_ptrs: Sequence[int], counter: int,
+                 status: int, rank: int, timeout_ns: int):
+    """Bounded device barrier over len(pad_ptrs) ranks (bpx_peer_barrier)."""
+    lib = load_library()
+    g = len(pad_ptrs)
+    pads = (ctypes.c_void_p * g)(*pad_ptrs)
+    aborts = (ctypes.c_void_p * g)(*abort_ptrs)
+    _check(lib.bpx_peer_barrier(ctypes.cast(pads, ctypes.c_void_p),
+                                ctypes.cast(aborts, ctypes.c_void_p), counter, status,
+                                rank, g, int(timeout_ns), _stream()), "bpx_peer_barrier")
 
 
 def signal_barrier(pad_ptrs: Sequence[int], rank: int, epoch: int):

@@ -210,7 +210,7 @@ class SimMetrics:
     fg_throughput_samples_per_s: float
     bg_throughput_samples_per_s: float
     cluster_total_throughput_samples_per_s: float
-    per_gpu_utilization: tuple[float, ...]
+    per_gpu_utilization: Optional[tuple[float, ...]]   # None: not measured
     qos_degradation: float
 
     def to_dict(self) -> dict:
@@ -221,7 +221,8 @@ class SimMetrics:
             "bg_throughput_samples_per_s": self.bg_throughput_samples_per_s,
             "cluster_total_throughput_samples_per_s":
                 self.cluster_total_throughput_samples_per_s,
-            "per_gpu_utilization": list(self.per_gpu_utilization),
+            "per_gpu_utilization": (None if self.per_gpu_utilization is None
+                                    else list(self.per_gpu_utilization)),
             "qos_degradation": self.qos_degradation,
         }
 
@@ -257,6 +258,11 @@ def metrics_from_trace(trace: SimTrace, n_gpus: int, global_batch: int,
     fg = global_batch * len(meas) / ws
     bg_done = sum(1 for t, _ in trace.bg_completions if w0 < t <= w1)
     bg = bg_done * bg_batch / ws
+    if not trace.busy:
+        # no per-op intervals were recorded (run() without measure_ops):
+        # utilisation is unknown rather than a fabricated number
+        return SimMetrics(mean, percentile(sorted(meas), 0.99), fg, bg, fg + bg,
+                          None, mean / baseline_us if baseline_us > 0 else 1.0)
     utils = []
     for gpu in range(n_gpus):
         covered, cur = 0, None
