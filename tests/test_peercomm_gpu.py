@@ -65,6 +65,7 @@ def _step_case(comm, rank, world, gs, B, res):
     st.sync_and_update()
     torch.cuda.synchronize()
     res["loss"] = st.loss()
+    res["last_g"] = gs[-1]
     g0 = {n: (a.cpu().clone(), b.cpu().clone()) for n, (a, b) in st.grads().items()}
     st.capture(warmup=1)                  # captured step: barriers must replay
     for _ in range(2):
@@ -74,7 +75,7 @@ def _step_case(comm, rank, world, gs, B, res):
     res["replay_same"] = all(torch.equal(a.cpu(), g0[n][0]) and torch.equal(b.cpu(), g0[n][1])
                              for n, (a, b) in st.grads().items())
     # every rank of a layer's group holds the same (allreduced) gradient
-    res["grads"] = g0
+    res["grads"] = _digest(g0)
     if rank == 0:
         ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
         ref32, r32 = vgg_ref.forward_backward(net, params, x, y, torch.float32)
@@ -191,7 +192,7 @@ def _worker(rank, world, port, q, case):
                 heap.allreduce("big", big, 2)
                 heap.allreduce("small", small, 2)
                 torch.cuda.synchronize()
-                res[f"big{k}"] = big.cpu().clone()
+                res[f"big{k}"] = big.cpu().tolist()   # plain data: workers exit first
                 res[f"small{k}"] = float(small[0].item())
             # captured allreduce replays against fresh epochs
             gr = torch.cuda.CUDAGraph()
@@ -259,7 +260,7 @@ def test_peer_reshard_and_allreduce_across_processes():
     ar = torch.arange(1000, dtype=torch.float32)
     for k in range(3):
         ref = (ar * 1 + k) + (ar * 2 + k)
-        assert torch.equal(out[0][f"big{k}"], ref) and torch.equal(out[1][f"big{k}"], ref)
+        assert out[0][f"big{k}"] == ref.tolist() and out[1][f"big{k}"] == ref.tolist()
         assert out[0][f"small{k}"] == out[1][f"small{k}"] == float(1 + k + 2 + k)
     assert out[0]["graph_big"] == out[1]["graph_big"] == 2.0
 
@@ -277,9 +278,10 @@ def _check_step(out, world):
     assert r0["worst"] <= 1.0
     for r in range(world):
         assert out[r]["replay_same"]
-        assert out[r]["loss"] == r0["loss"]
-        for n, (dw, db) in out[r]["grads"].items():      # bitwise identical replicas
-            assert torch.equal(dw, r0["grads"][n][0]) and torch.equal(db, r0["grads"][n][1])
+        if r < out[0]["last_g"]:                  # ranks holding the loss layer
+            assert out[r]["loss"] == r0["loss"]
+        for n, h in out[r]["grads"].items():      # bitwise identical replicas
+            assert h == r0["grads"][n], (r, n)
 
 
 @pytest.mark.timeout(300)
@@ -299,7 +301,8 @@ def _check_vgg16(out, world):
     assert r0["worst"] <= 1.0, r0["worst"]
     for r in range(world):
         assert out[r]["replay_same"] and out[r]["replicas_same"]
-        assert out[r]["loss"] == r0["loss"]
+        if r < r0["gs"][-1]:
+            assert out[r]["loss"] == r0["loss"]
 
 
 @pytest.mark.timeout(900)
