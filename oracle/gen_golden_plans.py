@@ -27,7 +27,7 @@ sys.dont_write_bytecode = True
 from burstplan import synth                                   # noqa: E402
 from burstplan.costs import moved_samples                     # noqa: E402
 from burstplan.graph import graph_to_dict                     # noqa: E402
-from burstplan.planner import plan, plan_to_json              # noqa: E402
+from burstplan.planner import brute_force_plan, plan, plan_to_json  # noqa: E402
 from burstplan.simulator import compile_timeline, forced_plan, SimConfig  # noqa: E402
 from conftest import random_chain_graph, random_sp_graph      # noqa: E402
 
@@ -105,6 +105,19 @@ def main():
         rnd.append({"graph": graph_to_dict(g), "G": 8, "amp": amp,
                     "candidates": None, "plan_json": plan_to_json(p)})
     dump("random_plans.json", {"instances": rnd})
+
+    # --- the exhaustive oracle on the small instances (G=4, <= 6 layers):
+    # reference brute_force_plan (planner.py:592-682) per random_plans index
+    bf = []
+    for k, inst in enumerate(rnd[:150]):
+        from burstplan.graph import graph_from_dict
+        g = graph_from_dict(inst["graph"])
+        try:
+            p = brute_force_plan(g, 4, inst["amp"], candidates=(1, 2, 4))
+            bf.append({"index": k, "plan_json": plan_to_json(p)})
+        except Exception as exc:                   # guard / infeasible: record the type
+            bf.append({"index": k, "error": type(exc).__name__})
+    dump("brute_force_plans.json", {"instances": bf})
 
     # --- sample layout ------------------------------------------------------
     ms = []

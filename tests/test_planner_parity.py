@@ -105,3 +105,29 @@ def test_timeline_c1_matches_reference():
     assert got(tl.fg_ops) == want["fg"]
     assert got(tl.bg_ops) == want["bg"]
     assert tl.predicted_fg_iteration_us == want["predicted"]
+
+
+BF = _load("brute_force_plans.json")["instances"]
+
+
+@pytest.mark.parametrize("k", range(len(BF)))
+def test_brute_force_plan_matches_reference_oracle(k):
+    """brute_force_plan (the reference's exhaustive oracle, planner.py:592-682)
+    reproduces the reference's own brute-force plan JSON on every small
+    random instance, and agrees with the DP planner's optimum."""
+    from paper_2112_10065_b200 import brute_force_plan
+    case = BF[k]
+    inst = RND[case["index"]]
+    g = graph_from_dict(inst["graph"])
+    bf = brute_force_plan(g, 4, inst["amp"], candidates=(1, 2, 4))
+    assert plan_to_json(bf) == case["plan_json"]
+    dp = plan(g, 4, inst["amp"], candidates=(1, 2, 4))
+    if not dp.fallback_layers:
+        assert bf.predicted_iteration_us == pytest.approx(dp.predicted_iteration_us, rel=1e-12)
+
+
+def test_brute_force_plan_guards_large_instances():
+    from paper_2112_10065_b200 import brute_force_plan
+    from paper_2112_10065_b200.errors import InfeasiblePlanError
+    with pytest.raises(InfeasiblePlanError):
+        brute_force_plan(synth.vgg_like(seed=0), 8, 2.0)
