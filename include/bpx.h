@@ -61,6 +61,12 @@ BPX_API long long bpx_launch_count(void);
 BPX_API const char* bpx_last_engine(void);
 /* conv3x3 / linear calls this process sent to a legacy engine.            */
 BPX_API long long bpx_legacy_engine_calls(void);
+/* SM budget of the calling host thread's later launches (0 = all SMs):
+ * persistent grids and split-K factors are sized to at most n SMs, so work
+ * launched or graph-captured under a budget keeps the rest of the GPU free
+ * for other streams (the background job under multiplexing).  Returns the
+ * previous budget.                                                        */
+BPX_API int bpx_set_sm_budget(int n);
 /* 1 if the current device is sm_100 (the only supported target). */
 BPX_API int bpx_device_supported(void);
 

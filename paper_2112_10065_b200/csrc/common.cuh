@@ -28,6 +28,13 @@ inline bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
+// SM budget of the calling host thread's launches (0 = the whole GPU):
+// persistent grids and split-K choices size themselves to it, so a kernel
+// launched (or captured) under a budget of k keeps at most k SMs busy with
+// its long-lived CTAs -- the background job's share under multiplexing
+// (bpx_set_sm_budget, multiplex.BgJob).
+int& sm_budget();
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -36,7 +43,8 @@ inline int num_sms() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
-  return n;
+  const int b = sm_budget();
+  return (b > 0 && b < n) ? b : n;
 }
 
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }

@@ -348,11 +348,22 @@ __global__ void sgd_tail(float* __restrict__ w, const float* __restrict__ g,
 static long long g_launches = 0;
 void count_launches(long long k) { __atomic_add_fetch(&g_launches, k, __ATOMIC_RELAXED); }
 
+int& sm_budget() {
+  static thread_local int budget = 0;
+  return budget;
+}
+
 }  // namespace bpx
 
 using namespace bpx;
 
 extern "C" {
+
+int bpx_set_sm_budget(int n) {
+  const int prev = sm_budget();
+  sm_budget() = n > 0 ? n : 0;
+  return prev;
+}
 
 const char* bpx_status_string(bpx_status_t s) {
   switch (s) {

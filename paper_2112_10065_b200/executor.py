@@ -771,7 +771,8 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         iterations: int = 4, sensitive: Iterable[str] = (),
         baseline_fg_iteration_us: Optional[float] = None, *,
         inputs=None, seed: int = 0, lr: float = 0.01,
-        step: Optional[BurstStep] = None, bg=None, measure_ops: bool = False):
+        step: Optional[BurstStep] = None, bg=None, measure_ops: bool = False,
+        bg_sm_budget: Optional[int] = None):
     """Execute ``iterations`` training steps of ``plan`` on real GPUs.
 
     Same call shape and return types as the reference's
@@ -781,7 +782,9 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
     one process per GPU (torchrun) for n_gpus > 1.  ``inputs`` = (x NHWC
     [B,...], labels [B]) host tensors (pinned); every iteration copies its
     input shard in, end to end.  With ``bg_graph`` every GPU also trains a
-    single-GPU background job on a low-priority stream (multiplex.py);
+    single-GPU background job on a low-priority stream (multiplex.py),
+    its kernels sized to ``bg_sm_budget`` SMs (default: $BPX_BG_SM_BUDGET,
+    0 = the whole GPU);
     ``sensitive`` names foreground ops (``multiplex.op_name``) that must
     not overlap background work.  bg samples/s is summed over GPUs.
     """
@@ -796,7 +799,7 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         x, y = synthetic_batch(st.net, plan.global_batch, seed)
         inputs = (x.pin_memory(), y.pin_memory())
     if bg is None and bg_graph is not None:
-        bg = BgJob(bg_graph, config, seed=seed + 1)
+        bg = BgJob(bg_graph, config, seed=seed + 1, sm_budget=bg_sm_budget)
     mux = Multiplexer(st, bg, config, sensitive, measure_ops=measure_ops)
     trace = SimTrace()
     try:

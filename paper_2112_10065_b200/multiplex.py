@@ -68,7 +68,9 @@ class BgJob:
     chunk graphs of <= ``graph_split_size`` program ops."""
 
     def __init__(self, bg_graph: CompGraph, config: SimConfig, seed: int = 1,
-                 lr: float = 1e-3):
+                 lr: float = 1e-3, sm_budget: Optional[int] = None):
+        import os
+        from . import ops
         from .executor import BurstStep
         plan, g = single_gpu_plan(bg_graph, config.bg_batch_size)
         self.batch = config.bg_batch_size
@@ -78,7 +80,16 @@ class BgJob:
         prog = self.step.program()
         cut = set(range(0, len(prog), config.graph_split_size))
         self.pool = torch.cuda.graph_pool_handle()
-        self.chunks = [gr for _, _, gr in self.step.capture_segments(cut, pool=self.pool)]
+        # SM budget (B200 addition to the reference's knobs): the chunks are
+        # captured with persistent grids and split-K sized to <= sm_budget
+        # SMs, so the background's long-lived CTAs never occupy the whole
+        # GPU and foreground kernels always find free SMs (the device
+        # scheduler does not preempt running CTAs)
+        if sm_budget is None:
+            sm_budget = int(os.environ.get("BPX_BG_SM_BUDGET", "0"))
+        self.sm_budget = sm_budget
+        with ops.sm_budget(sm_budget):
+            self.chunks = [gr for _, _, gr in self.step.capture_segments(cut, pool=self.pool)]
         self.n_ops = len(prog)
 
 

@@ -30,6 +30,7 @@ _SIGS = {
     "bpx_launch_count": (ctypes.c_longlong, []),
     "bpx_last_engine": (ctypes.c_char_p, []),
     "bpx_legacy_engine_calls": (ctypes.c_longlong, []),
+    "bpx_set_sm_budget": (ctypes.c_int, [ctypes.c_int]),
     "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
@@ -145,6 +146,26 @@ def last_engine() -> str:
     """Engine that served this thread's last conv3x3 / linear call
     (fdt, wgt, c1, dtc, dwt, dns, tc; legacy: simt, ts, wg, small)."""
     return load_library().bpx_last_engine().decode()
+
+
+def set_sm_budget(n: int) -> int:
+    """SM budget (0 = all) for this thread's later libbpx launches; returns
+    the previous one (bpx_set_sm_budget)."""
+    return int(load_library().bpx_set_sm_budget(int(n)))
+
+
+class sm_budget:
+    """Context manager: launches (and graph captures) inside use <= n SMs."""
+
+    def __init__(self, n: int):
+        self.n = n
+
+    def __enter__(self):
+        self.prev = set_sm_budget(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        set_sm_budget(self.prev)
 
 
 def legacy_engine_calls() -> int:

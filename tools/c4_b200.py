@@ -25,15 +25,30 @@ def main():
     p = plan(g, world, 2.0)
     cfg = SimConfig(warmup_iterations=3, bg_batch_size=8)
     _, alone = run(p, g, world, None, cfg, 23)
-    _, col = run(p, g, world, synth.resnet50_like(global_batch=8), cfg, 23)
+    bg = synth.resnet50_like(global_batch=8)
+    sweep = []
+    budgets = [int(b) for b in os.environ.get("C4_BUDGETS", "0,16,32,48,64,96").split(",")]
+    paces = [int(b) for b in os.environ.get("C4_PACES", "2").split(",")]
+    for pace in paces:
+        for budget in budgets:
+            c = SimConfig(warmup_iterations=3, bg_batch_size=8, launch_pace_limit=pace)
+            _, col = run(p, g, world, bg, c, 23, bg_sm_budget=budget)
+            sweep.append({"bg_sm_budget": budget, "launch_pace_limit": pace,
+                          "fg_collocated_samples_per_s": col.fg_throughput_samples_per_s,
+                          "bg_samples_per_s": col.bg_throughput_samples_per_s,
+                          "total_samples_per_s": col.cluster_total_throughput_samples_per_s,
+                          "total_vs_fg_alone": col.cluster_total_throughput_samples_per_s
+                          / alone.fg_throughput_samples_per_s,
+                          "fg_slowdown": alone.fg_throughput_samples_per_s
+                          / col.fg_throughput_samples_per_s})
+    ok = [r for r in sweep if r["fg_slowdown"] <= 1.18]
+    best = max(ok or sweep, key=lambda r: r["total_vs_fg_alone"])
     out = {"config": "C4: inception_like fg (B=32, amp 2) + resnet50_like bg (batch 8/GPU)",
            "gpus": world, "fg_alone_samples_per_s": alone.fg_throughput_samples_per_s,
-           "fg_collocated_samples_per_s": col.fg_throughput_samples_per_s,
-           "bg_samples_per_s": col.bg_throughput_samples_per_s,
-           "total_samples_per_s": col.cluster_total_throughput_samples_per_s,
-           "total_vs_fg_alone": col.cluster_total_throughput_samples_per_s
-           / alone.fg_throughput_samples_per_s,
-           "fg_slowdown": alone.fg_throughput_samples_per_s / col.fg_throughput_samples_per_s}
+           "bar": "total >= 1.2x fg alone at fg slowdown <= 1.18x "
+                  "(reference test_acceptance.py:255-275)",
+           "best": best, "meets_bar": best["total_vs_fg_alone"] >= 1.2
+           and best["fg_slowdown"] <= 1.18, "sweep": sweep}
     if int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps(out))
         if len(sys.argv) > 1:
