@@ -25,20 +25,37 @@ struct SegTable {
   int n;
 };
 
+// VEC: every thread moves U = 4 16-byte vectors per round (all four loads
+// issued before the stores: four requests in flight per thread, which the
+// peer-read latency over NVLink needs as much as HBM does).
 template <bool VEC>
 __global__ void reshard_kernel(SegTable t) {
+  constexpr int U = VEC ? 4 : 1;
+  constexpr unsigned long long E = VEC ? 16 : 1;
   const unsigned long long total = t.start[t.n];
-  const unsigned long long step = (unsigned long long)gridDim.x * blockDim.x * (VEC ? 16 : 1);
-  unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * (VEC ? 16 : 1);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x * E;
+  unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * E;
   int seg = 0;
-  for (; i < total; i += step) {
-    while (i >= t.start[seg + 1]) ++seg;          // monotone in i
-    unsigned long long off = i - t.start[seg];
-    if (VEC) {
-      int4 v = *reinterpret_cast<const int4*>(t.src[seg] + off);
-      *reinterpret_cast<int4*>(t.dst[seg] + off) = v;
-    } else {
-      t.dst[seg][off] = t.src[seg][off];
+  for (; i < total; i += U * stride) {
+    int sg[U];
+    unsigned long long off[U];
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long j = i + u * stride;
+      sg[u] = -1;
+      if (j < total) {
+        while (j >= t.start[seg + 1]) ++seg;      // monotone in j
+        sg[u] = seg;
+        off[u] = j - t.start[seg];
+        if (VEC) v[u] = *reinterpret_cast<const int4*>(t.src[seg] + off[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (sg[u] < 0) continue;
+      if (VEC) *reinterpret_cast<int4*>(t.dst[sg[u]] + off[u]) = v[u];
+      else t.dst[sg[u]][off[u]] = t.src[sg[u]][off[u]];
     }
   }
 }
@@ -197,7 +214,7 @@ bpx_status_t bpx_reshard_pull(const void* const* src_ptrs, const size_t* src_off
   t.start[k] = acc;
   if (acc == 0) return BPX_OK;
   long long units = vec ? (long long)(acc / 16) : (long long)acc;
-  int grid = (int)std::min<long long>(cdivll(units, 256), 4LL * num_sms());
+  int grid = (int)std::min<long long>(cdivll(units, vec ? 1024 : 256), 4LL * num_sms());
   if (vec) reshard_kernel<true><<<grid, 256, 0, as_stream(stream)>>>(t);
   else reshard_kernel<false><<<grid, 256, 0, as_stream(stream)>>>(t);
   return launch_status();

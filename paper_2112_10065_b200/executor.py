@@ -772,7 +772,7 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         baseline_fg_iteration_us: Optional[float] = None, *,
         inputs=None, seed: int = 0, lr: float = 0.01,
         step: Optional[BurstStep] = None, bg=None, measure_ops: bool = False,
-        bg_sm_budget: Optional[int] = None):
+        bg_sm_budget: Optional[int] = None, fg_sm_budget: int = 0):
     """Execute ``iterations`` training steps of ``plan`` on real GPUs.
 
     Same call shape and return types as the reference's
@@ -784,7 +784,7 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
     input shard in, end to end.  With ``bg_graph`` every GPU also trains a
     single-GPU background job on a low-priority stream (multiplex.py),
     its kernels sized to ``bg_sm_budget`` SMs (default: $BPX_BG_SM_BUDGET,
-    0 = the whole GPU);
+    0 = the whole GPU), the foreground's to ``fg_sm_budget`` (0 = all);
     ``sensitive`` names foreground ops (``multiplex.op_name``) that must
     not overlap background work.  bg samples/s is summed over GPUs.
     """
@@ -800,7 +800,8 @@ def run(plan: TrainingPlan, graph: CompGraph, n_gpus: int,
         inputs = (x.pin_memory(), y.pin_memory())
     if bg is None and bg_graph is not None:
         bg = BgJob(bg_graph, config, seed=seed + 1, sm_budget=bg_sm_budget)
-    mux = Multiplexer(st, bg, config, sensitive, measure_ops=measure_ops)
+    mux = Multiplexer(st, bg, config, sensitive, measure_ops=measure_ops,
+                      fg_sm_budget=fg_sm_budget)
     trace = SimTrace()
     try:
         trace = mux.run(iterations, inputs, trace, rank=comm.rank,

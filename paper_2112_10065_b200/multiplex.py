@@ -98,7 +98,8 @@ class Multiplexer:
     stream, background chunks on the low-priority stream."""
 
     def __init__(self, fg_step, bg: Optional[BgJob], config: SimConfig,
-                 sensitive: Iterable[str] = (), measure_ops: bool = False):
+                 sensitive: Iterable[str] = (), measure_ops: bool = False,
+                 fg_sm_budget: int = 0):
         self.fg = fg_step
         self.bg = bg
         self.cfg = config
@@ -116,7 +117,8 @@ class Multiplexer:
             if n in self.sensitive:
                 cut |= {i, i + 1}
         fg_step.op_events = [] if measure_ops else None
-        with torch.cuda.stream(self.fg_stream):
+        from . import ops
+        with torch.cuda.stream(self.fg_stream), ops.sm_budget(fg_sm_budget):
             self.segments = fg_step.capture_segments(cut)
         self.events = fg_step.op_events or []
         fg_step.op_events = None

@@ -27,13 +27,16 @@ def main():
     _, alone = run(p, g, world, None, cfg, 23)
     bg = synth.resnet50_like(global_batch=8)
     sweep = []
-    budgets = [int(b) for b in os.environ.get("C4_BUDGETS", "0,16,32,48,64,96").split(",")]
+    # (fg SM budget, bg SM budget): 0 = the whole GPU
+    pairs = [tuple(int(v) for v in b.split(":")) for b in os.environ.get(
+        "C4_BUDGETS", "0:0,0:16,0:48,124:24,104:44,88:60,74:74,60:88").split(",")]
     paces = [int(b) for b in os.environ.get("C4_PACES", "2").split(",")]
     for pace in paces:
-        for budget in budgets:
+        for fgb, budget in pairs:
             c = SimConfig(warmup_iterations=3, bg_batch_size=8, launch_pace_limit=pace)
-            _, col = run(p, g, world, bg, c, 23, bg_sm_budget=budget)
-            sweep.append({"bg_sm_budget": budget, "launch_pace_limit": pace,
+            _, col = run(p, g, world, bg, c, 23, bg_sm_budget=budget, fg_sm_budget=fgb)
+            sweep.append({"fg_sm_budget": fgb, "bg_sm_budget": budget,
+                          "launch_pace_limit": pace,
                           "fg_collocated_samples_per_s": col.fg_throughput_samples_per_s,
                           "bg_samples_per_s": col.bg_throughput_samples_per_s,
                           "total_samples_per_s": col.cluster_total_throughput_samples_per_s,
