@@ -106,6 +106,8 @@ size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
   size_t c = wg_conv_ws(n, h, w_, cin, cout);
   size_t d = wgt_conv_ws(n, h, w_, cin, cout);
   size_t e = small_conv_wgrad_ws(n, h, w_, cin, cout);
+  size_t f = thin_conv_wgrad_ws(n, h, w_, cin, cout);
+  e = e > f ? e : f;
   size_t m = a > b ? a : b;
   m = m > c ? m : c;
   m = m > d ? m : d;
@@ -121,6 +123,11 @@ bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* dw, float
   if (wgt_conv_ok(cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
       (!dbias || aligned16(dbias)))
     return use("wgt"), wgt_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+  if (thin_conv_wgrad_ok(cin, cout, w_)) {
+    use("thin");
+    bpx_status_t s = thin_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (small_conv_wgrad_ok(cin, cout) && aligned16(dz))
     return legacy("small"), small_conv_wgrad(x, dz, dw, dbias, n, h, w_, cin, cout, ws, ws_bytes, st);
   if (wg_conv_ok(cin, cout))
@@ -149,7 +156,7 @@ size_t bpx_linear_dgrad_workspace(int b, int in, int out) {
 size_t bpx_linear_wgrad_workspace(int b, int in, int out) {
   size_t m = max3(simt_linear_wgrad_ws(b, in, out), tc_linear_wgrad_ws(b, in, out),
                   dns_linear_ws(b, in, out));
-  size_t d = dwt_linear_ws(b, in, out);
+  size_t d = max3(dwt_linear_ws(b, in, out), thin_linear_ws(b, in, out), 0);
   return m > d ? m : d;
 }
 
@@ -165,6 +172,12 @@ bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias, f
   }
   if (dns_linear_ok(b, in, out))
     return use("dns"), dns_linear_fwd(x, w, bias, y, b, in, out, relu, ws, ws_bytes, st);
+  // pixel-batched 1x1 convs with 32 outputs (the four-tower net's towers)
+  if (thin_linear_ok(b, in, out)) {
+    use("thin");
+    bpx_status_t s = thin_linear_fwd(x, w, bias, y, b, in, out, relu, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   // pixel-batched dense ops (the 1x1 convs of the four-tower net: b = pixels)
   // also go to the tensor-core engine: the FFMA fallback's fwd orientation
   // took ~3 ms at b = 39200, in = 128, out = 32
@@ -185,6 +198,11 @@ bpx_status_t bpx_linear_dgrad(const float* dy, const float* w, const float* mask
   }
   if (dns_linear_ok(b, in, out))
     return use("dns"), dns_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
+  if (thin_linear_ok(b, in, out)) {
+    use("thin");
+    bpx_status_t s = thin_linear_dgrad(dy, w, mask_src, dx, b, in, out, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))
     return use("tc"), tc_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
   return legacy("simt"), simt_linear_dgrad(dy, w, mask_src, dx, b, in, out, ws, ws_bytes, st);
@@ -205,6 +223,11 @@ bpx_status_t bpx_linear_wgrad(const float* x, const float* dy, float* dw, float*
   }
   if (dns_linear_ok(b, in, out))
     return use("dns"), dns_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+  if (thin_linear_ok(b, in, out)) {
+    use("thin");
+    bpx_status_t s = thin_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
+    if (s != BPX_ERR_UNSUPPORTED) return s;
+  }
   if (tc_linear_ok(b, in, out) || (b > 256 && b % 4 == 0 && in % 4 == 0 && out % 4 == 0))
     return use("tc"), tc_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);
   return legacy("simt"), simt_linear_wgrad(x, dy, dw, dbias, b, in, out, ws, ws_bytes, st);

@@ -95,3 +95,23 @@ bpx_status_t dtc_linear_dgrad(const float* dy, const float* w, const float* mask
                               int b, int in, int out, void* ws, size_t ws_bytes,
                               cudaStream_t st);
 }  // namespace bpx
+
+// FFMA thin-GEMM engine (thin.cu): pixel-batched 1x1 convs with 32 outputs.
+namespace bpx {
+bool thin_linear_ok(int b, int in, int out);
+size_t thin_linear_ws(int b, int in, int out);
+bpx_status_t thin_linear_fwd(const float* x, const float* w, const float* bias, float* y,
+                             int b, int in, int out, int relu, cudaStream_t st);
+bpx_status_t thin_linear_dgrad(const float* dy, const float* w, const float* mask, float* dx,
+                               int b, int in, int out, cudaStream_t st);
+bpx_status_t thin_linear_wgrad(const float* x, const float* dy, float* dw, float* dbias,
+                               int b, int in, int out, void* ws, size_t ws_bytes,
+                               cudaStream_t st);
+}  // namespace bpx
+namespace bpx {
+bool thin_conv_wgrad_ok(int cin, int cout, int w);
+size_t thin_conv_wgrad_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t thin_conv_wgrad(const float* x, const float* dz, float* dw, float* dbias, int n,
+                             int h, int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                             cudaStream_t st);
+}  // namespace bpx

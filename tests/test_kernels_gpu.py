@@ -41,6 +41,8 @@ CONV_SHAPES = [
     # full-size images: 2-D output tiles with 4-D TMA halos (32x4 at 224,
     # 16x8 at 112) and the 64-channel stages of 64-wide N tiles
     (1, 224, 64, 64), (1, 112, 64, 128),
+    # the four-tower net's 32 -> 32 tower convs (35 / 17 / 8 px; thin FFMA wgrad)
+    (4, 35, 32, 32), (3, 17, 32, 32), (5, 8, 32, 32),
 ]
 
 
@@ -85,6 +87,8 @@ def test_conv_wgrad(shape):
     dw = torch.empty(cout, 3, 3, cin, device=DEV)
     db = torch.empty(cout, device=DEV)
     ops.conv3x3_wgrad(x.to(DEV), dz.to(DEV), dw, db)
+    if cin == cout == 32:
+        assert ops.last_engine() == "thin"
     torch.cuda.synchronize()
     close(dw, dw_ref, dw32)
     close(db, db_ref, db32)
@@ -131,7 +135,10 @@ def test_conv_matches_ffma_engine():
                                              (32, 4096, 1000, False), (3, 64, 40, True),
                                              (1, 128, 1000, False), (17, 256, 384, True),
                                              (2, 512, 128, False), (12, 100, 36, True),
-                                             (32, 25088, 4096, True)], ids=str)
+                                             (32, 25088, 4096, True),
+                                             # pixel-batched 1x1 convs (thin FFMA engine)
+                                             (1000, 128, 32, True), (2050, 64, 32, False),
+                                             (39200, 128, 32, True)], ids=str)
 def test_linear_fwd_bwd(b, fin, fout, relu):
     x = relu_input(b, fin, seed=15)
     w = rnd(fout, fin, seed=16, scale=0.01)
@@ -151,6 +158,8 @@ def test_linear_fwd_bwd(b, fin, fout, relu):
     dw = torch.empty(fout, fin, device=DEV)
     db = torch.empty(fout, device=DEV)
     ops.linear_wgrad(X, dy.to(DEV), dw, db)
+    if b > 256 and fout == 32:
+        assert ops.last_engine() == "thin"
     torch.cuda.synchronize()
     y32 = vgg_ref.layer_fwd(spec, x, w, bias, dtype=torch.float32)
     dx32 = (dy @ w) * (x > 0)
