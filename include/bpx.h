@@ -193,6 +193,31 @@ BPX_API bpx_status_t bpx_global_avgpool_fwd(const float* x, float* y, int n, int
 BPX_API bpx_status_t bpx_global_avgpool_bwd(const float* dy, const float* mask, float* dx,
                                     int n, int h, int w_, int c, void* stream);
 
+/* ---- synchronised batch normalisation of the residual nets' convs
+ * (the reference has no BN notion).  z, y, g, dz:
+ * [npix][c] NHWC (npix = this rank's pixels, ntot = the whole layer
+ * group's); gamma_beta = [beta ; gamma] (2c, the layer's "bias" slot).
+ * stats / sums are 2c floats of LOCAL per-channel sums that the caller
+ * allreduces over the layer's group [0, g) before the apply steps, so every
+ * rank normalises with full-batch statistics whatever g is.
+ *   stats    = [sum z ; sum z^2]
+ *   y        = act(gamma * (z - mu) * rstd + beta),  mu, var from stats / ntot
+ *   sums     = [sum g ; sum g * xhat]  (= the local [dbeta ; dgamma])
+ *   dz       = gamma * rstd * (g - sums0/ntot - xhat * sums1/ntot)
+ * Fixed-order fp64 sums: bitwise reproducible.  c % 4 == 0, c <= 4096.     */
+BPX_API size_t bpx_bn_workspace(long long npix, int c);
+BPX_API bpx_status_t bpx_bn_stats(const float* z, long long npix, int c, float* stats,
+                          void* ws, size_t ws_bytes, void* stream);
+BPX_API bpx_status_t bpx_bn_apply(const float* z, const float* stats, const float* gamma_beta,
+                          long long npix, long long ntot, int c, float eps, int relu,
+                          float* y, void* stream);
+BPX_API bpx_status_t bpx_bn_bwd_sums(const float* g, const float* z, const float* stats,
+                             long long npix, long long ntot, int c, float eps, float* sums,
+                             void* ws, size_t ws_bytes, void* stream);
+BPX_API bpx_status_t bpx_bn_bwd_apply(const float* g, const float* z, const float* stats,
+                              const float* sums, const float* gamma_beta, long long npix,
+                              long long ntot, int c, float eps, float* dz, void* stream);
+
 /* Mean softmax cross-entropy over the GLOBAL batch: loss_out[0] =
  * sum_{local rows} CE / b_global (fixed order); loss_out must hold
  * b_local + 1 floats ([1..b_local] = per-row terms);

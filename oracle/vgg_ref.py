@@ -11,7 +11,9 @@ synth.py:86-123), so this is a restatement of the *paper's* step
 stride-2 input subsample, residual `add` with a ResNet option-A shortcut,
 global average pool; the four-tower net behind `inception_like`: 1x1 convs,
 3x3/s1 max pool over a channel subset, channel concat, branch inputs):
-forward layer by layer, mean softmax cross-entropy over the global batch,
+forward layer by layer (the residual nets' convs followed by BatchNorm
+over the whole global batch: the executor's SyncBN over [0, g) is plan-
+independent), mean softmax cross-entropy over the global batch,
 backward, per-layer weight gradients.  Numerics parity is therefore
 "unpinned" against the reference (no golden vectors exist there); it is
 pinned against this oracle in fp64, with the tolerance stated in
@@ -27,12 +29,22 @@ import torch
 import torch.nn.functional as F
 
 
+def _relu(h, margins):
+    if margins is not None:
+        margins.append(float(h.detach().abs().min()))
+    return F.relu(h)
+
+
 def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
-                     threads=None):
+                     threads=None, margins=None):
     """Return (loss, grads) with grads[name] = (dW, db) in product layouts.
 
     ``params``: dict name -> (w, b) CPU tensors; ``labels`` int tensor.
     The loss is the mean over the batch given (= the global batch).
+    ``margins`` (a list, optional) receives min |pre-activation| of every
+    ReLU: a value inside the fp32 error band can flip the ReLU mask between
+    two fp32-accurate implementations, and one flipped element moves every
+    upstream gradient by ~1/sqrt(elements) (tests pick inputs with a margin).
     """
     if threads:
         torch.set_num_threads(threads)
@@ -53,14 +65,22 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
             h = h[:, :, off:off + 2 * l.hw:2, off:off + 2 * l.hw:2]
         if l.kind == "conv":
             w, b = leaves[l.name]
-            h = F.conv2d(h, w.permute(0, 3, 1, 2), b, padding=1)
+            if getattr(l, "bn", False):      # conv -> BatchNorm (full batch) -> ReLU
+                h = F.conv2d(h, w.permute(0, 3, 1, 2), None, padding=1)
+                h = F.batch_norm(h, None, None, b[l.cout:], b[:l.cout], True, 0.0, 1e-5)
+            else:
+                h = F.conv2d(h, w.permute(0, 3, 1, 2), b, padding=1)
             if l.relu:
-                h = F.relu(h)
+                h = _relu(h, margins)
         elif l.kind == "conv1x1":
             w, b = leaves[l.name]
-            h = F.conv2d(h, w.permute(0, 3, 1, 2), b)
+            if getattr(l, "bn", False):
+                h = F.conv2d(h, w.permute(0, 3, 1, 2), None)
+                h = F.batch_norm(h, None, None, b[l.cout:], b[:l.cout], True, 0.0, 1e-5)
+            else:
+                h = F.conv2d(h, w.permute(0, 3, 1, 2), b)
             if l.relu:
-                h = F.relu(h)
+                h = _relu(h, margins)
         elif l.kind == "pool3":              # 3x3/s1/p1 max over the first cout channels
             h = F.max_pool2d(h[:, :l.cout], 3, 1, 1)
         elif l.kind == "concat":
@@ -75,7 +95,7 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
                 s = F.pad(s, (0, 0, 0, 0, 0, h.shape[1] - s.shape[1]))
             h = h + s
             if l.relu:
-                h = F.relu(h)
+                h = _relu(h, margins)
         elif l.kind == "gap":
             h = h.mean(dim=(2, 3))
             flat = True
@@ -86,7 +106,7 @@ def forward_backward(net, params, x_nhwc, labels, dtype=torch.float64,
             w, b = leaves[l.name]
             h = F.linear(h, w, b)
             if l.relu:
-                h = F.relu(h)
+                h = _relu(h, margins)
         outs[l.name] = h
     loss = F.cross_entropy(h, labels.to(torch.int64))
     loss.backward()

@@ -70,6 +70,10 @@ class _Layer:
     join: str = ""                         # add: shortcut-gradient path (fused|direct|reshard)
     dskip: Optional[torch.Tensor] = None   # add: shortcut gradient in the add's layout
     dskip_src: Optional[torch.Tensor] = None   # add: ... resharded to the source's layout
+    z: Optional[torch.Tensor] = None       # bn: the conv output before normalisation
+    dz: Optional[torch.Tensor] = None      # bn: gradient wrt z
+    bnf: Optional[torch.Tensor] = None     # bn: [sum z ; sum z^2], allreduced over [0, g)
+    bnb: Optional[torch.Tensor] = None     # bn: [sum g ; sum g*xhat], allreduced over [0, g)
 
 
 class BurstStep:
@@ -196,7 +200,12 @@ class BurstStep:
                 L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
             if sp.kind == "pool3":
                 L.idx = torch.empty(sp.out_shape(L.b), dtype=torch.uint8, device=dev)
-            L.dy = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+            if sp.kind == "add" and L.reshard_in:
+                # the join passes its gradient on unchanged (L.dx is L.dy
+                # below), so the backward transfer's source is L.dy itself
+                L.dy = _buf(("dx", i), sp.out_shape(L.b))
+            else:
+                L.dy = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
             if src is not None:
                 last = consumers[L.src_i][-1] == i
                 if L.reshard_in or not last:
@@ -234,6 +243,13 @@ class BurstStep:
                     L.s = S.y
                 if L.join != "fused" and L.join != "direct":
                     L.dskip = _buf(("dskip", i), sshape)
+            if sp.bn:
+                L.z = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+                L.dz = torch.empty(sp.out_shape(L.b), dtype=torch.float32, device=dev)
+                L.bnf = _buf(("bnf", i), (2 * sp.cout,))
+                L.bnb = _buf(("bnb", i), (2 * sp.cout,)) if L.g > 1 else None
+                ws_need = max(ws_need, self.k.bn_workspace_bytes(
+                    L.b * sp.hw * sp.hw, sp.cout))
             ps = sp.param_shapes()
             if ps:
                 w, b = params[sp.name]
@@ -309,6 +325,8 @@ class BurstStep:
                     out[("y", L.skip_i)] = 4 * S.spec.out_elems() * S.b
                 if L.active:
                     out[("dskip", i)] = 4 * S.spec.out_elems() * L.b
+            if L.spec.bn and L.active and L.g > 1:       # SyncBN sums over [0, g)
+                out[("bnf", i)] = out[("bnb", i)] = 8 * L.spec.cout
         for g, n in bucket_sizes.items():
             if g > 1:
                 out[("bucket", g)] = 4 * n
@@ -349,10 +367,57 @@ class BurstStep:
             dst.copy_(src, non_blocking=True)
 
     # ------------------------------------------------------------ step
+    def _bn_ntot(self, L) -> int:
+        """Pixels of the whole layer group (the global batch)."""
+        return self.B * L.spec.hw * L.spec.hw
+
+    def _bn_allreduce(self, i: int, key: str, t: torch.Tensor) -> None:
+        L = self.layers[i]
+        if L.g <= 1:
+            return
+        if self.heap is not None:
+            self.heap.allreduce((key, i), t, L.g)
+        else:
+            self.comm.allreduce(t, L.g)
+
+    def _bn_fwd(self, i: int) -> None:
+        """z -> y: local sums, allreduce over [0, g), normalise (+ReLU)."""
+        L = self.layers[i]
+        self.k.bn_stats(L.z, L.bnf, ws=self.ws)
+        self._bn_allreduce(i, "bnf", L.bnf)
+        self.k.bn_apply(L.z, L.bnf, L.bias, self._bn_ntot(L), L.y, L.spec.relu)
+
+    def _bn_bwd(self, i: int) -> torch.Tensor:
+        """dy -> dz.  The local sums are the layer's [dbeta ; dgamma] (summed
+        over [0, g) later by the gradient-bucket allreduce); a copy is
+        allreduced now for the data gradient."""
+        L = self.layers[i]
+        self.k.bn_bwd_sums(L.dy, L.z, L.bnf, self._bn_ntot(L), L.dbias, ws=self.ws)
+        sums = L.dbias
+        if L.g > 1:
+            L.bnb.copy_(L.dbias)
+            self._bn_allreduce(i, "bnb", L.bnb)
+            sums = L.bnb
+        self.k.bn_bwd_apply(L.dy, L.z, L.bnf, sums, L.bias, self._bn_ntot(L), L.dz)
+        return L.dz
+
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
         lo = {"w_lo": L.w_lo} if L.w_lo is not None else {}
+        if sp.bn:
+            # conv without bias / activation into z, then the synchronised BN
+            x = L.x
+            if sp.down:
+                x = self._sub_fwd(L)
+            if sp.kind == "conv":
+                self.k.conv3x3_fwd(x, L.w, None, L.z, relu=False, ws=self.ws, **lo)
+            else:
+                P = L.b * sp.hw * sp.hw
+                self.k.linear_fwd(x.reshape(P, sp.cin), L.w.view(sp.cout, sp.cin), None,
+                                  L.z.view(P, sp.cout), False, ws=self.ws)
+            self._bn_fwd(i)
+            return
         if sp.kind == "conv" and sp.down:
             self._sub_fwd(L)
             self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
@@ -458,11 +523,13 @@ class BurstStep:
         if sp.kind == "concat":
             self.k.concat_bwd(L.dy, list(L.cat_dst))
             return
+        dy = self._bn_bwd(i) if sp.bn else L.dy
+        dbias = None if sp.bn else L.dbias      # bn: [dbeta ; dgamma] came from _bn_bwd
         if sp.kind == "conv1x1":
             P = L.b * sp.hw * sp.hw
             x2 = (L.xs if sp.down else L.x).reshape(P, sp.cin)
-            dy2, w2 = L.dy.view(P, sp.cout), L.w.view(sp.cout, sp.cin)
-            self.k.linear_wgrad(x2, dy2, L.dw.view(sp.cout, sp.cin), L.dbias, ws=self.ws)
+            dy2, w2 = dy.view(P, sp.cout), L.w.view(sp.cout, sp.cin)
+            self.k.linear_wgrad(x2, dy2, L.dw.view(sp.cout, sp.cin), dbias, ws=self.ws)
             if L.src_i >= 0:
                 dxt = L.dxs if sp.down else L.dx
                 self.k.linear_dgrad(dy2, w2, x2 if sp.in_relu else None, dxt.view(P, sp.cin),
@@ -478,15 +545,15 @@ class BurstStep:
         if sp.kind == "gap":
             self.k.global_avgpool_bwd(L.dy, mask, L.dx)
         elif sp.kind == "conv" and sp.down:
-            self.k.conv3x3_wgrad(L.xs, L.dy, L.dw, L.dbias, ws=self.ws)
-            self.k.conv3x3_dgrad(L.dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
+            self.k.conv3x3_wgrad(L.xs, dy, L.dw, dbias, ws=self.ws)
+            self.k.conv3x3_dgrad(dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
                                  **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
             if not self._fused_down(i):
                 self._sub_bwd(L)
         elif sp.kind == "conv":
-            self.k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=self.ws)
+            self.k.conv3x3_wgrad(L.x, dy, L.dw, dbias, ws=self.ws)
             if i > 0:
-                self.k.conv3x3_dgrad(L.dy, L.w, mask, L.dx, ws=self.ws,
+                self.k.conv3x3_dgrad(dy, L.w, mask, L.dx, ws=self.ws,
                                      **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
         elif sp.kind == "pool":
             if L.idx is not None:

@@ -39,6 +39,8 @@ class LayerSpec:
     src: Optional[str] = None    # input layer (None: the previous layer)
     srcs: tuple = ()             # concat: the joined layers, in channel order
     ihw: int = 0                 # down: input size when not 2*hw (2*hw+1: odd pixels kept)
+    bn: bool = False             # conv: synchronised BatchNorm over [0, g) after the conv
+                                 # (no conv bias; the "bias" slot holds [beta ; gamma])
 
     @property
     def out_hw(self) -> int:
@@ -75,10 +77,11 @@ class LayerSpec:
         return (b, self.out_hw, self.out_hw, self.cout)
 
     def param_shapes(self) -> Optional[tuple[tuple[int, ...], tuple[int, ...]]]:
+        nb = 2 * self.cout if self.bn else self.cout
         if self.kind == "conv":
-            return (self.cout, 3, 3, self.cin), (self.cout,)
+            return (self.cout, 3, 3, self.cin), (nb,)
         if self.kind == "conv1x1":
-            return (self.cout, 1, 1, self.cin), (self.cout,)
+            return (self.cout, 1, 1, self.cin), (nb,)
         if self.kind == "dense":
             return (self.cout, self.cin), (self.cout,)
         return None
@@ -153,7 +156,7 @@ def mlp_for_chain(graph: CompGraph) -> NetSpec:
     return NetSpec(f"mlp{width}x{len(real)}", 1, width, width, layers)
 
 
-def wideresnet_net(graph: CompGraph) -> NetSpec:
+def wideresnet_net(graph: CompGraph, bn: bool = True) -> NetSpec:
     """Executable residual net behind the reference's ``wideresnet_like``
     family (synth.py:126-169), shapes read off the graph itself: channels
     from each conv's 9*cin*cout parameters, spatial size from its activation
@@ -170,7 +173,12 @@ def wideresnet_net(graph: CompGraph) -> NetSpec:
       graph has no projection layer, so the shortcut has no parameters);
     * ``pool`` = global average pool; ``fc`` = dense (channels -> 1000).
       The graph gives fc the rest of a 127 M parameter budget; the
-      executable classifier is the real 512 x 1000 layer.
+      executable classifier is the real 512 x 1000 layer;
+    * every conv is followed by batch normalisation (``bn=True``; the
+      reference has no BN notion), synchronised over the
+      layer's GPU group [0, g): statistics of the whole global batch, so
+      the numerics do not depend on the plan (``bn=False`` builds the
+      normalisation-free variant with the Fixup-style init).
     """
     real = [l for l in graph.layers if not l.is_virtual]
     ids = {l.id for l in real}
@@ -201,7 +209,8 @@ def wideresnet_net(graph: CompGraph) -> NetSpec:
             if k == 1 and ihw != hw:
                 raise GraphFormatError(f"{l.name}: strided 1x1 convs are not built")
             specs.append(LayerSpec(l.name, "conv" if k == 9 else "conv1x1", cin, cout, hw, relu,
-                                   bool(preds) and relu_out[preds[0]], down=ihw == 2 * hw))
+                                   bool(preds) and relu_out[preds[0]], down=ihw == 2 * hw,
+                                   bn=bn))
             out_c[l.id], out_hw[l.id], relu_out[l.id] = cout, hw, relu
         elif l.kind == "add":
             main = [p for p in preds if by_id[p].kind == "conv"
@@ -342,12 +351,14 @@ def init_params(net: NetSpec, seed: int = 0) -> dict[str, tuple[torch.Tensor, to
         if l.kind in ("conv", "conv1x1"):
             k = 9 if l.kind == "conv" else 1
             std = math.sqrt(2.0 / ((l.cin if fan_in else l.cout) * k))
-            if blocks and not l.relu:
+            if blocks and not l.relu and not l.bn:
                 std /= math.sqrt(blocks)
         else:
             std = 0.01
         w = torch.randn(ps[0], generator=gen, dtype=torch.float32) * std
         b = torch.zeros(ps[1], dtype=torch.float32)
+        if l.bn:                          # [beta ; gamma] = [0 ; 1]
+            b[l.cout:] = 1.0
         out[l.name] = (w, b)
     return out
 

@@ -89,6 +89,17 @@ _SIGS = {
                                + [ctypes.c_void_p]),
     "bpx_softmax_xent": (ctypes.c_int, [_c_float_p, ctypes.c_void_p]
                          + [ctypes.c_int] * 3 + [_c_float_p, _c_float_p, ctypes.c_void_p]),
+    "bpx_bn_workspace": (ctypes.c_size_t, [ctypes.c_longlong, ctypes.c_int]),
+    "bpx_bn_stats": (ctypes.c_int, [_c_float_p, ctypes.c_longlong, ctypes.c_int, _c_float_p,
+                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_bn_apply": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_longlong] * 2
+                     + [ctypes.c_int, ctypes.c_float, ctypes.c_int, _c_float_p,
+                        ctypes.c_void_p]),
+    "bpx_bn_bwd_sums": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_longlong] * 2
+                        + [ctypes.c_int, ctypes.c_float, _c_float_p, ctypes.c_void_p,
+                           ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_bn_bwd_apply": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_longlong] * 2
+                         + [ctypes.c_int, ctypes.c_float, _c_float_p, ctypes.c_void_p]),
     "bpx_sgd_update": (ctypes.c_int, [_c_float_p, _c_float_p, ctypes.c_size_t,
                                       ctypes.c_float, ctypes.c_void_p]),
     "bpx_reshard_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
@@ -513,6 +524,53 @@ def softmax_xent(logits, labels, b_global, loss_out, dlogits):
                                 _ptr(loss_out), _ptr(dlogits), _stream()),
            "bpx_softmax_xent")
     return loss_out
+
+
+BN_EPS = 1e-5
+
+
+def _npc(t):
+    """(pixels, channels) of an NHWC activation (or [rows][c])."""
+    return t.numel() // t.shape[-1], t.shape[-1]
+
+
+def bn_stats(z, stats, ws: Optional[Workspace] = None):
+    """stats[0:c] = sum z, stats[c:2c] = sum z^2 over this rank's pixels."""
+    lib = load_library()
+    _f32(z, stats)
+    npix, c = _npc(z)
+    wp, wb = _ws(ws, lib.bpx_bn_workspace(npix, c), z.device)
+    _check(lib.bpx_bn_stats(_ptr(z), npix, c, _ptr(stats), wp, wb, _stream()), "bpx_bn_stats")
+
+
+def bn_apply(z, stats, gamma_beta, ntot, y, relu, eps=BN_EPS):
+    lib = load_library()
+    _f32(z, stats, gamma_beta, y)
+    npix, c = _npc(z)
+    _check(lib.bpx_bn_apply(_ptr(z), _ptr(stats), _ptr(gamma_beta), npix, int(ntot), c,
+                            float(eps), int(relu), _ptr(y), _stream()), "bpx_bn_apply")
+
+
+def bn_bwd_sums(g, z, stats, ntot, sums, ws: Optional[Workspace] = None, eps=BN_EPS):
+    lib = load_library()
+    _f32(g, z, stats, sums)
+    npix, c = _npc(z)
+    wp, wb = _ws(ws, lib.bpx_bn_workspace(npix, c), z.device)
+    _check(lib.bpx_bn_bwd_sums(_ptr(g), _ptr(z), _ptr(stats), npix, int(ntot), c, float(eps),
+                               _ptr(sums), wp, wb, _stream()), "bpx_bn_bwd_sums")
+
+
+def bn_bwd_apply(g, z, stats, sums, gamma_beta, ntot, dz, eps=BN_EPS):
+    lib = load_library()
+    _f32(g, z, stats, sums, gamma_beta, dz)
+    npix, c = _npc(z)
+    _check(lib.bpx_bn_bwd_apply(_ptr(g), _ptr(z), _ptr(stats), _ptr(sums), _ptr(gamma_beta),
+                                npix, int(ntot), c, float(eps), _ptr(dz), _stream()),
+           "bpx_bn_bwd_apply")
+
+
+def bn_workspace_bytes(npix, c) -> int:
+    return int(load_library().bpx_bn_workspace(int(npix), int(c)))
 
 
 def sgd_update(w, g, lr):

@@ -36,7 +36,8 @@ def _nhwc(t):
 def conv3x3_fwd(x, w, bias, y, relu=True, ws=None):
     if x.shape[0] == 0:
         return y
-    o = F.conv2d(_nchw(x), w.double().permute(0, 3, 1, 2), bias.double(), padding=1)
+    o = F.conv2d(_nchw(x), w.double().permute(0, 3, 1, 2),
+                 None if bias is None else bias.double(), padding=1)
     y.copy_(_nhwc(F.relu(o) if relu else o))
     return y
 
@@ -57,17 +58,21 @@ def conv3x3_dgrad(dz, w, mask, dx, ws=None):
 def conv3x3_wgrad(x, dz, dw, dbias, ws=None):
     if x.shape[0] == 0:
         dw.zero_()
-        dbias.zero_()
+        if dbias is not None:
+            dbias.zero_()
         return dw
     g = torch.nn.grad.conv2d_weight(_nchw(x), (dw.shape[0], dw.shape[3], 3, 3), _nchw(dz),
                                     padding=1)
     dw.copy_(g.permute(0, 2, 3, 1))
-    dbias.copy_(dz.double().sum(dim=(0, 1, 2)))
+    if dbias is not None:
+        dbias.copy_(dz.double().sum(dim=(0, 1, 2)))
     return dw
 
 
 def linear_fwd(x, w, bias, y, relu, ws=None):
-    o = x.double() @ w.double().t() + bias.double()
+    o = x.double() @ w.double().t()
+    if bias is not None:
+        o = o + bias.double()
     y.copy_(F.relu(o) if relu else o)
     return y
 
@@ -82,8 +87,52 @@ def linear_dgrad(dy, w, mask, dx, ws=None):
 
 def linear_wgrad(x, dy, dw, dbias, ws=None):
     dw.copy_(dy.double().t() @ x.double())
-    dbias.copy_(dy.double().sum(0))
+    if dbias is not None:
+        dbias.copy_(dy.double().sum(0))
     return dw
+
+
+# synchronised BN (libbpx bn_*: local sums, the executor allreduces them)
+def bn_workspace_bytes(*a):
+    return 0
+
+
+def _pc(t):
+    return t.double().reshape(-1, t.shape[-1])
+
+
+def _coef(stats, ntot, eps):
+    c = stats.numel() // 2
+    m = stats[:c].double() / ntot
+    v = (stats[c:].double() / ntot - m * m).clamp_min(0)
+    return m, 1.0 / torch.sqrt(v + eps)
+
+
+def bn_stats(z, stats, ws=None):
+    zz = _pc(z)
+    stats.copy_(torch.cat([zz.sum(0), (zz * zz).sum(0)]))
+
+
+def bn_apply(z, stats, gb, ntot, y, relu, eps=1e-5):
+    c = z.shape[-1]
+    m, r = _coef(stats, ntot, eps)
+    o = (_pc(z) - m) * r * gb[c:].double() + gb[:c].double()
+    y.copy_((F.relu(o) if relu else o).reshape(y.shape))
+
+
+def bn_bwd_sums(g, z, stats, ntot, sums, ws=None, eps=1e-5):
+    m, r = _coef(stats, ntot, eps)
+    gg, xh = _pc(g), (_pc(z) - m) * r
+    sums.copy_(torch.cat([gg.sum(0), (gg * xh).sum(0)]))
+
+
+def bn_bwd_apply(g, z, stats, sums, gb, ntot, dz, eps=1e-5):
+    c = z.shape[-1]
+    m, r = _coef(stats, ntot, eps)
+    xh = (_pc(z) - m) * r
+    t0, t1 = sums[:c].double() / ntot, sums[c:].double() / ntot
+    d = gb[c:].double() * r * (_pc(g) - t0 - xh * t1)
+    dz.copy_(d.reshape(dz.shape))
 
 
 def maxpool2x2_fwd(x, y):

@@ -319,3 +319,38 @@ def test_vgg16_ops_take_tensor_core_engines(b):
             assert eng in ALLOWED[sp.kind][op], (b, sp.name, op, eng)
         torch.cuda.synchronize()
     assert len(seen) == 3 * 16 - 1
+
+
+# ---- synchronised batch norm (bn_*): one rank holding the whole batch, so
+# the local sums are the global ones; against torch's fp64 batch_norm
+@pytest.mark.parametrize("n,h,c", [(4, 13, 64), (2, 7, 128), (3, 5, 2048), (1, 35, 32)])
+def test_batchnorm_fwd_bwd(n, h, c):
+    z = rnd(n, h, h, c, seed=40, scale=2.0) + 0.5
+    g = rnd(n, h, h, c, seed=41)
+    gb = torch.cat([rnd(c, seed=42, scale=0.1), 1.0 + rnd(c, seed=43, scale=0.1)])
+    zz = z.double().permute(0, 3, 1, 2).requires_grad_(True)
+    beta = gb[:c].double().requires_grad_(True)
+    gamma = gb[c:].double().requires_grad_(True)
+    yr = torch.nn.functional.batch_norm(zz, None, None, gamma, beta, True, 0.0, 1e-5)
+    yr.backward(g.double().permute(0, 3, 1, 2))
+    Z, G, GB = z.to(DEV), g.to(DEV), gb.to(DEV)
+    st = torch.empty(2 * c, device=DEV)
+    y = torch.empty_like(Z)
+    ops.bn_stats(Z, st)
+    ops.bn_apply(Z, st, GB, n * h * h, y, relu=False)
+    sums = torch.empty(2 * c, device=DEV)
+    ops.bn_bwd_sums(G, Z, st, n * h * h, sums)
+    dz = torch.empty_like(Z)
+    ops.bn_bwd_apply(G, Z, st, sums, GB, n * h * h, dz)
+    torch.cuda.synchronize()
+    assert vgg_ref.normwise_rel(y, yr.detach().permute(0, 2, 3, 1)) < 1e-6
+    assert vgg_ref.normwise_rel(dz, zz.grad.permute(0, 2, 3, 1)) < 1e-5
+    assert vgg_ref.normwise_rel(sums[:c], beta.grad) < 1e-6
+    assert vgg_ref.normwise_rel(sums[c:], gamma.grad) < 1e-5
+    # relu variant and bitwise reproducibility
+    y2 = torch.empty_like(Z)
+    ops.bn_apply(Z, st, GB, n * h * h, y2, relu=True)
+    st2 = torch.empty_like(st)
+    ops.bn_stats(Z, st2)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, torch.relu(y)) and torch.equal(st, st2)

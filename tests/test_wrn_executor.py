@@ -6,6 +6,8 @@ fan-in, stride-2 stage transitions with option-A shortcuts, global average
 pool -- with the test-only torch op set (tests/cpu_kernels.py) and checks
 loss and every weight gradient against the fp64 oracle (oracle/vgg_ref.py)."""
 
+import math
+
 import pytest
 import torch
 
@@ -55,7 +57,7 @@ def test_wideresnet_like_net_structure():
     # conv FLOPs of the graph's own pricing (2*9*cin*cout*hw^2 per conv)
     g = synth.wideresnet_like(seed=0, global_batch=32)
     convs = [l for l in net.layers if l.kind == "conv"]
-    assert sum(c.n_params() - c.cout for c in convs) == sum(
+    assert sum(math.prod(c.param_shapes()[0]) for c in convs) == sum(
         l.params_bytes // 4 for l in g.layers if l.kind == "conv")
 
 

@@ -64,13 +64,29 @@ def test_subsample_and_global_avgpool(n, h, c):
         _same(got, ref)
 
 
+def margin_seed(net, B, margin=3e-6, tries=20):
+    """First init/data seed whose fp64 pre-activations all sit at least
+    ``margin`` away from the ReLU kink: the gate compares two fp32-accurate
+    computations, and a pre-activation inside their ~1e-6 error band can
+    flip one ReLU mask element, which moves every upstream gradient by
+    ~1/sqrt(elements) (a single flip at the last join of this net gave
+    ~7e-3) -- a property of the input, not of either implementation."""
+    for seed in range(tries):
+        params = init_params(net, seed=seed)
+        x, y = synthetic_batch(net, B, seed=seed)
+        m = []
+        vgg_ref.forward_backward(net, params, x, y, torch.float64, margins=m)
+        if min(m) > margin:
+            return params, x, y
+    raise AssertionError("no seed with a ReLU margin")
+
+
 @pytest.mark.timeout(600)
 def test_residual_net_step_matches_fp64():
     B = 2
     graph = tiny_wrn_graph(B, stem_c=64, stages=((128, 2, 16), (256, 2, 8)), classes=16)
     net = net_for_graph(graph)
-    params = init_params(net, seed=0)
-    x, y = synthetic_batch(net, B, seed=0)
+    params, x, y = margin_seed(net, B)
     loss64, g64 = vgg_ref.forward_backward(net, params, x, y, torch.float64)
     loss32, g32 = vgg_ref.forward_backward(net, params, x, y, torch.float32)
     st = BurstStep(one_gpu_plan(graph), graph, params=params, lr=0.0)
