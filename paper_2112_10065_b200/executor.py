@@ -61,6 +61,9 @@ class _Layer:
     dx_acc: bool = False                   # dx is private: accumulate into the source's dy
     cat_dst: tuple = ()                    # concat bwd targets (source dy or private)
     cat_acc: tuple = ()                    # concat: (source index, private buffer) pairs
+    cat_in: tuple = ()                     # concat fwd parts (source y, or a resharded copy)
+    xedges: tuple = ()                     # input edges (src, part) crossing a GPU-count change
+    xdy: dict = field(default_factory=dict)    # source side: (consumer, part) -> landing buffer
     idx: Optional[torch.Tensor] = None     # pool: first-max position per output
     reshard_in: bool = False               # input arrives through a reshard
     xs: Optional[torch.Tensor] = None      # down conv: stride-2 subsample of x
@@ -148,19 +151,28 @@ class BurstStep:
                 L.join = "direct"
             self.join_after[c1] = i
 
-        # input edges: the previous layer (a chain edge, resharded when g
-        # changes), a named earlier layer (a branch edge), or several
-        # (concat).  Branch edges stay on one GPU set.  A layer feeding
-        # several consumers gets its gradient from all of them: the consumer
-        # whose backward runs first (the highest index) writes the source's
-        # dy, the others write private buffers that are accumulated into it.
+        # input edges: the previous layer (a chain edge), a named earlier
+        # layer (a branch edge), or several (concat).  Any edge may cross a
+        # GPU-count change: its source's output is resharded into the
+        # consumer's layout before the consumer runs, and the consumer's
+        # input gradient is resharded back (the reference's `transfer`,
+        # simulator.py:242-253).  A layer feeding several consumers gets its
+        # gradient from all of them: the consumer whose backward runs first
+        # (the highest index) writes the source's dy -- through the backward
+        # transfer when the edge crosses g -- the others land in private
+        # buffers (in the source's layout) that are accumulated into it.
         consumers = branch_topology([L.spec for L in self.layers], [L.g for L in self.layers])
         for i, L in enumerate(self.layers):
             sp = L.spec
             if sp.kind == "concat":
                 L.srcs_i = tuple(names[n] for n in sp.srcs)
+                L.xedges = tuple((j, k) for k, j in enumerate(L.srcs_i)
+                                 if self.layers[j].g != L.g)
             else:
                 L.src_i = names[sp.src] if sp.src is not None else i - 1
+                if L.src_i >= 0 and self.layers[L.src_i].g != L.g:
+                    L.xedges = ((L.src_i, -1),)
+        self.consumers = consumers
 
         # P2P backend: every buffer a peer reads lives in a symmetric heap
         # (PeerComm.make_heap, collective): the producer side of each
@@ -214,16 +226,22 @@ class BurstStep:
                 else:
                     L.dx = src.dy.view(sp.in_shape(L.b))
             if sp.kind == "concat":
-                dst, acc = [], []
-                for j in L.srcs_i:
+                dst, acc, cin = [], [], []
+                for k, j in enumerate(L.srcs_i):
                     S = self.layers[j]
-                    if consumers[j][-1] == i:
+                    pshape = (L.b,) + tuple(S.spec.out_shape(1)[1:])
+                    if S.g != L.g:            # part arrives / leaves by reshard
+                        cin.append(torch.empty(pshape, dtype=torch.float32, device=dev))
+                        dst.append(_buf(("cdy", i, k), pshape))
+                    elif consumers[j][-1] == i:
+                        cin.append(S.y)
                         dst.append(S.dy)
                     else:
+                        cin.append(S.y)
                         buf = torch.empty_like(S.dy)
                         dst.append(buf)
                         acc.append((j, buf))
-                L.cat_dst, L.cat_acc = tuple(dst), tuple(acc)
+                L.cat_dst, L.cat_acc, L.cat_in = tuple(dst), tuple(acc), tuple(cin)
             if sp.down:
                 low = (L.b, sp.hw, sp.hw, sp.cin)
                 L.xs = torch.empty(low, dtype=torch.float32, device=dev)
@@ -271,6 +289,14 @@ class BurstStep:
                         L.b * sp.hw * sp.hw, sp.cin, sp.cout))
                 else:
                     ws_need = max(ws_need, self.k.linear_workspace_bytes(L.b, sp.cin, sp.cout))
+        # cross-g edges, source side: the backward transfer lands in the
+        # source's dy when this consumer writes it first, else in a private
+        # buffer (source layout) accumulated into dy afterwards
+        for i, L in enumerate(self.layers):
+            for j, k in L.xedges:
+                S = self.layers[j]
+                if S.active and consumers[j][-1] != i:
+                    S.xdy[(i, k)] = torch.empty_like(S.dy)
         # conv weights' 3xTF32 low parts: one split launch per bucket over
         # its contiguous conv span, after every update (fwd and dgrad then
         # reuse it instead of splitting per call)
@@ -313,12 +339,13 @@ class BurstStep:
         the gradient buckets of g > 1, and the loss partial."""
         out = {}
         for i, L in enumerate(self.layers):
-            if self._chain_transfer(i):
-                P = self.layers[i - 1]
+            for j, k in L.xedges:
+                P = self.layers[j]
                 if P.active:
-                    out[("y", i - 1)] = 4 * P.spec.out_elems() * P.b
+                    out[("y", j)] = 4 * P.spec.out_elems() * P.b
                 if L.active:
-                    out[("dx", i)] = 4 * L.spec.in_elems() * L.b
+                    key = ("cdy", i, k) if k >= 0 else ("dx", i)
+                    out[key] = 4 * P.spec.out_elems() * L.b
             if L.join == "reshard":
                 S = self.layers[L.skip_i]
                 if S.active:
@@ -429,7 +456,7 @@ class BurstStep:
         elif sp.kind == "pool3":
             self.k.maxpool3x3_fwd_idx(self._sub_fwd(L) if sp.down else L.x, L.y, L.idx)
         elif sp.kind == "concat":
-            self.k.concat_fwd([self.layers[j].y for j in L.srcs_i], L.y)
+            self.k.concat_fwd(list(L.cat_in), L.y)
         elif sp.kind == "conv":
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
         elif sp.kind == "add":
@@ -567,22 +594,32 @@ class BurstStep:
                 self.k.linear_dgrad(L.dy, L.w, None if mask is None else x2,
                                  L.dx.view(L.b, sp.cin), ws=self.ws)
 
-    def _reshard(self, i: int, backward: bool) -> None:
-        prev, L = self.layers[i - 1], self.layers[i]
-        bps = 4 * L.spec.in_elems()
-        if self.heap is not None:
-            if not backward:
-                self.heap.reshard(("y", i - 1), prev.g, L.x if L.active else None, L.g,
-                                  self.B, bps)
+    def _edge_reshard(self, i: int, j: int, k: int, backward: bool) -> None:
+        """The transfer of input edge j -> i (part k of a concat, -1
+        otherwise): forward j.y (g_j layout) -> i's input (g_i layout);
+        backward i's input gradient -> j.dy, or j's landing buffer."""
+        L, S = self.layers[i], self.layers[j]
+        bps = 4 * S.spec.out_elems()
+        if not backward:
+            dst = (L.cat_in[k] if k >= 0 else L.x) if L.active else None
+            if self.heap is not None:
+                self.heap.reshard(("y", j), S.g, dst, L.g, self.B, bps)
             else:
-                self.heap.reshard(("dx", i), L.g, prev.dy if prev.active else None, prev.g,
-                                  self.B, bps)
-        elif not backward:
-            self.comm.reshard(prev.y if prev.active else None, prev.g,
-                              L.x if L.active else None, L.g, self.B, bps)
+                self.comm.reshard(S.y if S.active else None, S.g, dst, L.g, self.B, bps)
+            return
+        dst = None
+        if S.active:
+            dst = S.xdy.get((i, k), S.dy)
+        if self.heap is not None:
+            key = ("cdy", i, k) if k >= 0 else ("dx", i)
+            self.heap.reshard(key, L.g, dst, S.g, self.B, bps)
         else:
-            self.comm.reshard(L.dx if L.active else None, L.g,
-                              prev.dy if prev.active else None, prev.g, self.B, bps)
+            src = (L.cat_dst[k] if k >= 0 else L.dx) if L.active else None
+            self.comm.reshard(src, L.g, dst, S.g, self.B, bps)
+
+    def _edge_accumulate(self, i: int, j: int, k: int) -> None:
+        S = self.layers[j]
+        self.k.accumulate(S.dy, S.xdy[(i, k)])
 
     def _mark(self, tag):
         if self.op_events is not None and self.device.type == "cuda":
@@ -601,8 +638,9 @@ class BurstStep:
         prog = []
         n = len(self.layers)
         for i in range(n):
-            if self._chain_transfer(i):
-                prog.append((("transfer", i, "fwd"), lambda i=i: self._reshard(i, False)))
+            for j, k in self.layers[i].xedges:
+                prog.append((("transfer", i, "fwd" if k < 0 else f"fwd{k}"),
+                             lambda i=i, j=j, k=k: self._edge_reshard(i, j, k, False)))
             if self.layers[i].join == "reshard":
                 prog.append((("transfer", i, "skip_fwd"),
                              lambda i=i: self._skip_reshard(i, False)))
@@ -615,8 +653,12 @@ class BurstStep:
                 prog.append((("compute", i, "bwd"), lambda i=i: self._bwd(i)))
                 if self.layers[i].dx_acc or self.layers[i].cat_acc:
                     prog.append((("compute", i, "fanin"), lambda i=i: self._fanin(i)))
-            if self._chain_transfer(i):
-                prog.append((("transfer", i, "bwd"), lambda i=i: self._reshard(i, True)))
+            for j, k in self.layers[i].xedges:
+                prog.append((("transfer", i, "bwd" if k < 0 else f"bwd{k}"),
+                             lambda i=i, j=j, k=k: self._edge_reshard(i, j, k, True)))
+                if self.layers[j].active and (i, k) in self.layers[j].xdy:
+                    prog.append((("compute", i, "xacc" if k < 0 else f"xacc{k}"),
+                                 lambda i=i, j=j, k=k: self._edge_accumulate(i, j, k)))
             if i in self.join_after:
                 # the join's backward = its shortcut gradient, after conv1's
                 # data gradient (and its transfer) wrote the source's dy
@@ -771,13 +813,10 @@ class _EagerReplay:
 
 
 def branch_topology(specs, gs) -> dict:
-    """Input edges of every layer -> {source index: [consumer indices]}.
-
-    Raises UnsupportedTopologyError unless every branch edge (an input that
-    is not the previous layer, or a concat part) and every fan-out stays on
-    one GPU count; chain edges may change g (they reshard).  The
-    reference's own plans for the branch/join families (C3, C4 at G=8,
-    amp 2..8) satisfy this (tests/test_inception_executor.py)."""
+    """Input edges of every layer -> {source index: [consumer indices]}, in
+    consumer order.  Every edge may cross a GPU-count change (a reshard);
+    raises UnsupportedTopologyError for an input that is not an earlier
+    layer."""
     names = {sp.name: i for i, sp in enumerate(specs)}
     consumers: dict[int, list] = {}
     for i, sp in enumerate(specs):
@@ -787,14 +826,9 @@ def branch_topology(specs, gs) -> dict:
             j = names[sp.src] if sp.src is not None else i - 1
             edges = (j,) if j >= 0 else ()
         for j in edges:
-            if (j != i - 1 or sp.kind == "concat") and gs[j] != gs[i]:
-                raise UnsupportedTopologyError(
-                    f"{sp.name}: branch edge from {specs[j].name} crosses GPU counts "
-                    f"{gs[j]} -> {gs[i]}")
+            if j >= i:
+                raise UnsupportedTopologyError(f"{sp.name}: input {specs[j].name} is not earlier")
             consumers.setdefault(j, []).append(i)
-    for j, cs in consumers.items():
-        if len(cs) > 1 and any(gs[c] != gs[j] for c in cs):
-            raise UnsupportedTopologyError(f"{specs[j].name}: fan-out across GPU counts")
     return consumers
 
 

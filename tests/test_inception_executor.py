@@ -104,7 +104,23 @@ def test_reference_plans_of_branch_join_families_are_executable():
 # world 2, ragged B=5: the amp-2 plan's shape (stem on 2 GPUs, modules on 1)
 # plus the classifier back on 2 -- chain transfers into and out of the
 # branch/join section
-def _worker(rank, port, q):
+# mixed: every kind of edge crossing g -- the module input fans out to
+# towers on 1 and 2 GPUs, towers change g inside, concat parts arrive from
+# both GPU counts and the concat itself alternates
+MIXED = {"m1_t1_1x1": 2, "m1_t2_1x1": 1, "m1_t2_3x3": 2, "m1_t3_1x1": 2, "m1_t3_3x3": 1,
+         "m1_t3_3x3b": 2, "m1_pool_proj": 1, "m1_concat": 2, "m2_t1_1x1": 1,
+         "m2_t2_1x1": 2, "m2_t2_3x3": 2, "m2_t3_1x1": 1, "m2_t3_3x3": 1, "m2_t3_3x3b": 2,
+         "m2_pool_proj": 2, "m2_concat": 1, "stem_conv5": 1}
+
+
+def _gs(net, mode):
+    if mode == "mixed":
+        return [MIXED.get(l.name, 2) for l in net.layers]
+    return [2 if (l.name.startswith("stem") and l.name != "stem_conv5") or l.name == "fc"
+            else 1 for l in net.layers]
+
+
+def _worker(rank, port, q, mode="amp2"):
     try:
         import os
         import torch.distributed as dist
@@ -119,8 +135,7 @@ def _worker(rank, port, q):
         graph = tiny_inception_graph(B, modules=2)
         net = net_for_graph(graph)
         ids = [l.id for l in graph.layers if not l.is_virtual]
-        gs = [2 if (l.name.startswith("stem") and l.name != "stem_conv5") or l.name == "fc"
-              else 1 for l in net.layers]
+        gs = _gs(net, mode)
         params = init_params(net, seed=5)
         x, y = synthetic_batch(net, B, seed=6)
         p = TrainingPlan(graph.name, 2, 2.0, B, tuple(zip(ids, gs)), 0.0, (), ())
@@ -144,7 +159,7 @@ def _worker(rank, port, q):
         q.put((rank, {"error": traceback.format_exc()}))
 
 
-def test_world2_four_tower_net_matches_oracle():
+def _run_world2(mode):
     import socket
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
@@ -153,7 +168,7 @@ def test_world2_four_tower_net_matches_oracle():
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    ps = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, port, q, mode)) for r in range(2)]
     for p in ps:
         p.start()
     out = dict(q.get(timeout=300) for _ in ps)
@@ -166,3 +181,13 @@ def test_world2_four_tower_net_matches_oracle():
     assert len(r0["errs"]) == 3 + 2 * 6 + 1
     for name, e in r0["errs"].items():
         assert e < 1e-6, (name, e)
+
+
+def test_world2_four_tower_net_matches_oracle():
+    _run_world2("amp2")
+
+
+def test_world2_branch_edges_across_gpu_counts_match_oracle():
+    """Fan-outs, concat parts and tower chains crossing 1 <-> 2 GPUs."""
+    from paper_2112_10065_b200.executor import BurstStep  # noqa: F401
+    _run_world2("mixed")

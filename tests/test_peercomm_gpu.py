@@ -190,6 +190,51 @@ def _wrn_case(comm, rank, world, res):
         res["errs"] = errs
 
 
+def _incep_case(comm, rank, world, res):
+    """Four-tower net on 2 ranks with every kind of edge crossing 1 <-> 2
+    GPUs (test_inception_executor.MIXED): fan-outs, concat parts and tower
+    chains reshard through the symmetric heap."""
+    from oracle import vgg_ref
+    from paper_2112_10065_b200.executor import BurstStep
+    from paper_2112_10065_b200.network import net_for_graph
+    from paper_2112_10065_b200.planner import TrainingPlan
+    from test_inception_executor import _gs, tiny_inception_graph
+    from test_wrn_gpu import margin_seed
+    B = 5
+    graph = tiny_inception_graph(B, modules=2)
+    net = net_for_graph(graph)
+    params, x, y = margin_seed(net, B)
+    gs = _gs(net, "mixed")
+    ids = [l.id for l in graph.layers if not l.is_virtual]
+    p = TrainingPlan(graph.name, world, 2.0, B, tuple(zip(ids, gs)), 0.0, (), ())
+    st = BurstStep(p, graph, comm=comm, params=params, lr=0.0)
+    st.load(x, y)
+    st.forward_backward()
+    st.sync_and_update()
+    torch.cuda.synchronize()
+    res["loss"] = st.loss()
+    res["last_g"] = gs[-1]
+    g0 = {n: (a.cpu().clone(), b.cpu().clone()) for n, (a, b) in st.grads().items()}
+    st.capture(warmup=1)
+    st.step()
+    torch.cuda.synchronize()
+    comm.check()
+    res["replay_same"] = _digest(st.grads()) == _digest(g0)
+    res["grads"] = _digest(g0)
+    if rank == 0:
+        ref_loss, ref = vgg_ref.forward_backward(net, params, x, y, torch.float64)
+        _, r32 = vgg_ref.forward_backward(net, params, x, y, torch.float32)
+        res["ref_loss"] = ref_loss
+        worst, errs = 0.0, {}
+        for n, (dw, db) in g0.items():
+            for k, (got, rf, rf32) in enumerate(((dw, ref[n][0], r32[n][0]),
+                                                 (db, ref[n][1], r32[n][1]))):
+                gate = max(1e-3, 2 * vgg_ref.normwise_rel(rf32, rf))
+                errs[(n, k)] = vgg_ref.normwise_rel(got, rf) / gate
+                worst = max(worst, errs[(n, k)])
+        res["worst"], res["errs"] = worst, errs
+
+
 def _worker(rank, world, port, q, case):
     if os.environ.get("BPX_PC_DEBUG"):
         import faulthandler
@@ -272,6 +317,8 @@ def _worker(rank, world, port, q, case):
             _vgg16_b32_case(comm, rank, world, case, res)
         elif case == "wrn":
             _wrn_case(comm, rank, world, res)
+        elif case == "incep":
+            _incep_case(comm, rank, world, res)
         elif case == "step":
             from test_executor_dist import GS
             _step_case(comm, rank, world, GS, 5, res)
@@ -370,3 +417,8 @@ def test_peer_backend_uniform_dp8_vgg16_b32():
 @pytest.mark.timeout(400)
 def test_peer_backend_residual_net_syncbn_two_ranks():
     _check_step(_run("wrn", 2), 2)
+
+
+@pytest.mark.timeout(400)
+def test_peer_backend_branch_edges_across_gpu_counts():
+    _check_step(_run("incep", 2), 2)
