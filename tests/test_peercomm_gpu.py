@@ -201,7 +201,7 @@ def _incep_case(comm, rank, world, res):
     from test_inception_executor import _gs, tiny_inception_graph
     from test_wrn_gpu import margin_seed
     B = 5
-    graph = tiny_inception_graph(B, modules=2)
+    graph = tiny_inception_graph(B, modules=2, classes=16)   # dense ops: out % 4 == 0
     net = net_for_graph(graph)
     params, x, y = margin_seed(net, B)
     gs = _gs(net, "mixed")
