@@ -79,16 +79,26 @@ BPX_API bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float
                              float* y, int n, int h, int w_, int cin, int cout,
                              int relu, void* ws, size_t ws_bytes, void* stream);
 BPX_API size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout);
-/* Same op with the weights' 3xTF32 low part supplied by the caller
- * (w_lo = w - tf32(w), from bpx_tf32_split_lo; NULL = split here): a
- * training step splits every weight once per update instead of once per
- * call.  bpx_conv3x3_dgrad_presplit likewise.                              */
+/* Same op with its fp16x3 operands prepared by the caller (DESIGN.md,
+ * "fp16x3"): w_hi / w_lo / w_amax = the weights split by bpx_f16_split
+ * (fp16 [cout][3][3][cin] each, and the split span's max |w| bits), made
+ * once per update instead of once per call; x_amax = max |x| as bits
+ * (bpx_absmax, or written by the producer of x).  Each may be NULL (the
+ * call then prepares it in its workspace).  bpx_conv3x3_dgrad_presplit
+ * likewise, with dz_amax for dz.                                          */
 BPX_API bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w,
-                                      const float* w_lo, const float* bias, float* y,
+                                      const void* w_hi, const void* w_lo,
+                                      const unsigned* w_amax, const unsigned* x_amax,
+                                      const float* bias, float* y,
                                       int n, int h, int w_, int cin, int cout, int relu,
                                       void* ws, size_t ws_bytes, void* stream);
-/* lo[i] = w[i] - tf32(w[i]) (truncated tf32: the value the tensor core reads), n % 4 == 0 */
-BPX_API bpx_status_t bpx_tf32_split_lo(const float* w, float* lo, size_t n, void* stream);
+/* *amax = max |x[i]| as its fp32 bit pattern (x 16-B aligned).           */
+BPX_API bpx_status_t bpx_absmax(const float* x, size_t n, unsigned* amax, void* stream);
+/* fp16x3 weight split: *amax = max |w|, s = 14 - floor(log2 *amax) (so
+ * |w 2^s| < 2^15), hi = fp16(w 2^s), lo = fp16(w 2^s - hi); hi, lo hold n
+ * fp16 each (8-B aligned), in w's layout.                                  */
+BPX_API bpx_status_t bpx_f16_split(const float* w, size_t n, void* hi, void* lo,
+                                   unsigned* amax, void* stream);
 
 /* dx = conv3x3_transpose(dz, w) [* (mask_src > 0) if mask_src != NULL].
  * dz:[n,h,w,cout] dx,mask_src:[n,h,w,cin].  mask_src is the layer input
@@ -99,7 +109,9 @@ BPX_API bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w,
                                size_t ws_bytes, void* stream);
 BPX_API size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout);
 BPX_API bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w,
-                                        const float* w_lo, const float* mask_src, float* dx,
+                                        const void* w_hi, const void* w_lo,
+                                        const unsigned* w_amax, const unsigned* dz_amax,
+                                        const float* mask_src, float* dx,
                                         int n, int h, int w_, int cin, int cout, void* ws,
                                         size_t ws_bytes, void* stream);
 

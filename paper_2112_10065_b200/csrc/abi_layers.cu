@@ -35,16 +35,26 @@ size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
 bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, float* y,
                              int n, int h, int w_, int cin, int cout, int relu, void* ws,
                              size_t ws_bytes, void* stream) {
-  return bpx_conv3x3_fwd_presplit(x, w, nullptr, bias, y, n, h, w_, cin, cout, relu, ws,
-                                  ws_bytes, stream);
+  return bpx_conv3x3_fwd_presplit(x, w, nullptr, nullptr, nullptr, nullptr, bias, y, n, h, w_,
+                                  cin, cout, relu, ws, ws_bytes, stream);
 }
 
-bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const float* w_lo,
-                                      const float* bias, float* y, int n, int h, int w_,
-                                      int cin, int cout, int relu, void* ws, size_t ws_bytes,
-                                      void* stream) {
+static bool split_args(const void* hi, const void* lo, const unsigned* amax, F16Weights& wt) {
+  if (!hi && !lo && !amax) return true;
+  if (!hi || !lo || !amax || !aligned16(hi) || !aligned16(lo)) return false;
+  wt.hi = hi; wt.lo = lo; wt.amax = amax;
+  return true;
+}
+
+bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const void* w_hi,
+                                      const void* w_lo, const unsigned* w_amax,
+                                      const unsigned* x_amax, const float* bias, float* y,
+                                      int n, int h, int w_, int cin, int cout, int relu,
+                                      void* ws, size_t ws_bytes, void* stream) {
   BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
-  BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w) && aligned16(w_lo));
+  BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
+  F16Weights wt;
+  BPX_CHECK_ARG(split_args(w_hi, w_lo, w_amax, wt));
   cudaStream_t st = as_stream(stream);
   if (c1_conv_fwd_ok(cin, cout)) {
     use("c1");
@@ -55,8 +65,8 @@ bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const floa
     return legacy("small"), small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(x)) {
     use("fdt");
-    bpx_status_t s = fdt_conv_fwd(x, w, w_lo, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes,
-                                  st);
+    bpx_status_t s = fdt_conv_fwd(x, w, wt.hi ? &wt : nullptr, x_amax, bias, y, n, h, w_, cin,
+                                  cout, relu, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (ts_conv_ok(cin, cout))
@@ -76,21 +86,24 @@ size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
 bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mask_src,
                                float* dx, int n, int h, int w_, int cin, int cout,
                                void* ws, size_t ws_bytes, void* stream) {
-  return bpx_conv3x3_dgrad_presplit(dz, w, nullptr, mask_src, dx, n, h, w_, cin, cout, ws,
-                                    ws_bytes, stream);
+  return bpx_conv3x3_dgrad_presplit(dz, w, nullptr, nullptr, nullptr, nullptr, mask_src, dx, n,
+                                    h, w_, cin, cout, ws, ws_bytes, stream);
 }
 
-bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w, const float* w_lo,
-                                        const float* mask_src, float* dx, int n, int h, int w_,
-                                        int cin, int cout, void* ws, size_t ws_bytes,
-                                        void* stream) {
+bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w, const void* w_hi,
+                                        const void* w_lo, const unsigned* w_amax,
+                                        const unsigned* dz_amax, const float* mask_src,
+                                        float* dx, int n, int h, int w_, int cin, int cout,
+                                        void* ws, size_t ws_bytes, void* stream) {
   BPX_CHECK_ARG(dz && w && dx && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
-  BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w) && aligned16(w_lo));
+  BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w));
+  F16Weights wt;
+  BPX_CHECK_ARG(split_args(w_hi, w_lo, w_amax, wt));
   cudaStream_t st = as_stream(stream);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(dz) && (!mask_src || aligned16(mask_src))) {
     use("fdt");
-    bpx_status_t s = fdt_conv_dgrad(dz, w, w_lo, mask_src, dx, n, h, w_, cin, cout, ws,
-                                    ws_bytes, st);
+    bpx_status_t s = fdt_conv_dgrad(dz, w, wt.hi ? &wt : nullptr, dz_amax, mask_src, dx, n, h,
+                                    w_, cin, cout, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (ts_conv_ok(cin, cout))

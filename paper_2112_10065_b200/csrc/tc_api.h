@@ -67,17 +67,33 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
                             cudaStream_t st);
 }  // namespace bpx
 
-// TMA-fed persistent forward / data-gradient engine (tc_fdt.cu).
+// fp16x3 operand preparation (f16split.cu): *amax = max |x| as bits (memset +
+// one launch); f16_split = absmax of the span, then hi/lo fp16 arrays of
+// w * 2^s in w's layout (two launches + memset).
+namespace bpx {
+struct F16Weights {
+  const void* hi = nullptr;          // fp16 [cout][3][3][cin]
+  const void* lo = nullptr;
+  const uint32_t* amax = nullptr;    // max |w| bits of the split span (sets the scale)
+};
+void absmax(const float* x, size_t n, uint32_t* amax, cudaStream_t st);
+void f16_split(const float* w, size_t n, void* hi, void* lo, uint32_t* amax, cudaStream_t st);
+}  // namespace bpx
+
+// TMA-fed persistent forward / data-gradient engine, fp16x3 (tc_fdt.cu).
 namespace bpx {
 bool fdt_conv_ok(int cin, int cout, int w);
 size_t fdt_conv_ws(int n, int h, int w, int cin, int cout);
-// w_lo (nullable): w - tf32(w) split by the caller (bpx_tf32_split_lo)
-bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* w_lo, const float* bias,
-                          float* y, int n, int h, int w_, int cin, int cout, int relu,
-                          void* ws, size_t ws_bytes, cudaStream_t st);
-bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* w_lo,
-                            const float* mask, float* dx, int n, int h, int w_, int cin,
-                            int cout, void* ws, size_t ws_bytes, cudaStream_t st);
+// wsplit (nullable): the weights split by the caller (bpx_f16_split);
+// amax_x / amax_dz (nullable): the A operand's max |v| bits (bpx_absmax)
+bpx_status_t fdt_conv_fwd(const float* x, const float* w, const F16Weights* wsplit,
+                          const uint32_t* amax_x, const float* bias, float* y, int n, int h,
+                          int w_, int cin, int cout, int relu, void* ws, size_t ws_bytes,
+                          cudaStream_t st);
+bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const F16Weights* wsplit,
+                            const uint32_t* amax_dz, const float* mask, float* dx, int n, int h,
+                            int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
 }  // namespace bpx
 
 // TMA-fed tcgen05 dense fwd / dgrad for batches <= 32 (tc_dense.cu).

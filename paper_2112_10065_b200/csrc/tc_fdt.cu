@@ -6,36 +6,41 @@
 //   s_tap = dy*W + dx  (flattened-pixel shift of the tap)
 //
 // M = 128 output pixels per tile, N = output channels, K = (channel chunk,
-// tap) stages.  Per channel chunk the CTA loads ONE halo of the activations
-// by TMA and all nine taps read their shifted 128-row window out of it, so
-// activation traffic is the halo/tile ratio instead of 9x the tile:
+// tap) stages of 64 channels.  Per channel chunk the CTA loads ONE halo of
+// the activations by TMA and all nine taps read their shifted 128-row window
+// out of it, so activation traffic is the halo/tile ratio instead of 9x the
+// tile:
 //   * 2-D tiles (W, H divisible by a TW x TH = 128 block, e.g. 32 x 4 at
-//     224x224): the halo is one 4-D box (TW+2) x (TH+2) x 32 channels whose
-//     out-of-bounds rows TMA zero-fills -- the conv's padding for free;
+//     224x224): the halo is one 4-D box (TW+2) x (TH+2) x 32 channels per
+//     32-channel half whose out-of-bounds rows TMA zero-fills -- the conv's
+//     padding for free;
 //   * otherwise 128 consecutive flattened pixels: the halo is the flattened
 //     rows [m0 - W - 1, m0 + 128 + W + 1), and rows whose source pixel wraps
 //     across an image row/edge are zeroed by the A converters from a 9-bit
 //     per-pixel tap mask computed once per tile.
-// A stage carries 32 channels (N = 128 tiles) or 64 (N = 64 tiles), so every
-// stage holds the same 768 MMA cycles and pays one converter/MMA handshake.
-// The B tile is the raw weight tile, straight from w by TMA:
-//   fwd   B(co, k) = w[co][tap][ci]: K-major, 128-B swizzle (one box)
-//   dgrad B(ci, k) = w[co][tap][ci]: MN-major, SWIZZLE_128B_ATOM_32B, one
-//                    box per 32 input channels (w viewed [Cout][9][Cin]).
 //
-// fp32 accuracy by 3xTF32 (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi); the raw tile
-// is b_hi.  A converters split A into TMEM (TS form).  b_lo = w - tf32(w) is
-// a pre-split copy of the (small) weight tensor made by one elementwise
-// kernel per call, loaded by TMA next to b_hi: shared memory then carries
-// only the MMA's B reads, the TMA fills and one LDS pass over A -- a
-// converter pass over B in shared memory made this kernel smem-bound.
-// TMEM chunk promotion into RN fp32 registers as in the other engines.  The kernel is persistent: the stage ring and the
-// accumulator ping-pong run straight across tiles, so a tile's epilogue
-// (drain warps: bias + ReLU or ReLU mask, stores) overlaps the next tile's
-// main loop.
+// fp32 accuracy by fp16x3 (tc_ptx.cuh): the activations are scaled by a
+// power of two from their absolute maximum (one word written by a reduction
+// before the launch) and split by the A converters into fp16 hi/lo pairs
+// stored in TMEM (TS form); the weights come pre-split by bpx_conv3x3_wsplit
+// (fp16 hi and lo in the layout of w, one power-of-two scale per weight
+// span) and are loaded by TMA:
+//   fwd   B(co, k) = w16[co][tap][ci]: K-major, 128-B swizzle
+//   dgrad B(ci, k) = w16[co][tap][ci]: MN-major, 128-B swizzle, one box per
+//                    64 input channels (w viewed [Cout][9][Cin]).
+// Each k-step (16 channels) issues a_lo*b_hi + a_hi*b_lo + a_hi*b_hi as
+// kind::f16 MMAs: twice the tf32 rate and, at 64-wide N tiles, half the
+// TMEM A reads per product.  Partial sums accumulate in 128-K chunks in
+// ping-pong TMEM and are promoted into round-to-nearest fp32 registers by
+// the drain warps (the tensor core's fp32 accumulation truncates), which
+// undo both scales (exact powers of two) before the epilogue.  The kernel is
+// persistent: the stage ring and the accumulator ping-pong run straight
+// across tiles, so a tile's epilogue (bias + ReLU or ReLU mask, stores)
+// overlaps the next tile's main loop.
 //
-// CTA: 14 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters,
-// 6-13 drain + epilogue.
+// CTA: 2 + 8 + BN/16 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-9 A
+// converters (two per TMEM lane quadrant, one 32-channel half each), then
+// the drain + epilogue warps.
 #include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "tc_api.h"
@@ -43,32 +48,26 @@
 namespace bpx {
 namespace fdt {
 using namespace tcx;
-#ifdef FDT_PROF
-void* fdt_prof_ptr = nullptr;
-#endif
 
 constexpr int TMA_WARP = 0, MMA_WARP = 1, CV0 = 2;   // A converters from warp 2
-#ifndef FDT_NCONV
-#define FDT_NCONV 8
-#endif
+constexpr int KS = 64;                               // channels per stage
+constexpr int NCH = 2;                               // 32-channel halo halves per stage
+constexpr int PCH = 128 / KS;                        // stages per promotion chunk (K = 128)
 
-// BN output channels per tile, KS channels per stage, NS stages.
-template <int BN, int KS, int NS>
+// BN output channels per tile, S stages.
+template <int BN, int S_>
 struct Cfg {
-  static_assert((BN == 128 && KS == 32) || (BN == 64 && KS == 64), "tile");
-  static constexpr int S = NS;
-  static constexpr int NCH = KS / 32;                     // 32-channel halves per stage
-  static constexpr int PCH = 128 / KS;                    // stages per promotion chunk (K = 128)
-  // A converter warps (two per TMEM lane quadrant split the channels) and
-  // drain warps (64 accumulator columns per thread)
-  static constexpr int NCONV = FDT_NCONV;
-  static constexpr int NDRAIN = BN / 16;
+  static_assert(BN == 128 || BN == 64, "tile");
+  static constexpr int S = S_;
+  static constexpr int NCONV = 8;
+  static constexpr int NDRAIN = BN / 16;                  // 64 accumulator columns per thread
   static constexpr int DR0 = CV0 + NCONV;
   static constexpr int NTHREADS = 32 * (2 + NCONV + NDRAIN);
-  static constexpr int B_BYTES = BN * KS * 4;
-  static constexpr int STAGE = 2 * B_BYTES;               // B raw | B lo
+  static constexpr int B_BYTES = BN * KS * 2;             // one fp16 tile (hi or lo)
+  static constexpr int STAGE = 2 * B_BYTES;               // B hi | B lo
   static constexpr int A_COL = 2 * BN;                    // accumulators: 2 x BN columns
-  static_assert(A_COL + S * 2 * KS <= 512, "TMEM budget");
+  static constexpr int A_STAGE = KS;                      // TMEM columns per stage: hi | lo
+  static_assert(A_COL + S * A_STAGE <= 512, "TMEM budget");
   // dynamic smem = 1024 (align) + S*STAGE + 2 halo slots + 512 (barriers)
   static int smem(int halo_bytes) { return 1024 + S * STAGE + 2 * halo_bytes + 512; }
 };
@@ -82,9 +81,10 @@ struct Geo {
   int half_bytes;            // smem stride of one 32-channel halo (1 KB aligned)
   int halo_bytes;            // one halo slot (NCH halves)
   int halo_tx;               // bytes TMA delivers per halo slot
-  int ksplit, units;         // K halves per tile (1 or 2) and work units = tiles * ksplit
-  float* part;               // ksplit > 1: raw partial sums [ksplit][npix][N]
-  void* prof;                // FDT_PROF builds: MMA-issuer cycle counters
+  int ksplit, units;         // K parts per tile and work units = tiles * ksplit
+  float* part;               // ksplit > 1: partial sums [ksplit][npix][N]
+  const uint32_t* amax_a;    // max |A| bits (activations / output gradient)
+  const uint32_t* amax_w;    // max |w| bits of the weights' span
 };
 
 struct EBiasAct {
@@ -140,12 +140,12 @@ __device__ __forceinline__ Tile tile_of(const Geo& g, int mi) {
   return t;
 }
 
-template <int BN, int KS, int NS, bool DG, class EPI>
-__global__ void __launch_bounds__(Cfg<BN, KS, NS>::NTHREADS, 1)
+template <int BN, int S_, bool DG, class EPI>
+__global__ void __launch_bounds__(Cfg<BN, S_>::NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
-  using Cf = Cfg<BN, KS, NS>;
-  constexpr int S = Cf::S, NCH = Cf::NCH, PCH = Cf::PCH;
+  using Cf = Cfg<BN, S_>;
+  constexpr int S = Cf::S;
   constexpr int NCONV = Cf::NCONV, NDRAIN = Cf::NDRAIN, DR0 = Cf::DR0;
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
@@ -183,6 +183,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int sa = f16_scale_exp(*g.amax_a), sw = f16_scale_exp(*g.amax_w);
 
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
@@ -217,18 +218,17 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
             char* st = smem + s * Cf::STAGE;
             mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
-            if (DG) {        // BN/32 boxes of 32 ci x KS co rows (MN-major)
-              for (int j = 0; j < BN / 32; ++j) {
-                tma_load_3d(st + j * KS * 128, &tb, n0 + 32 * j, tap, cc * KS, &bfull[s]);
-                tma_load_3d(st + Cf::B_BYTES + j * KS * 128, &tbl, n0 + 32 * j, tap, cc * KS,
+            if (DG) {        // BN/64 boxes of 64 ci x KS co rows (MN-major)
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) {
+                tma_load_3d(st + j * KS * 128, &tb, n0 + 64 * j, tap, cc * KS, &bfull[s]);
+                tma_load_3d(st + Cf::B_BYTES + j * KS * 128, &tbl, n0 + 64 * j, tap, cc * KS,
                             &bfull[s]);
               }
-            } else {         // NCH boxes of 32 k x BN rows (K-major)
-              for (int h = 0; h < NCH; ++h) {
-                const int k0 = tap * g.C + cc * KS + 32 * h;
-                tma_load_2d(st + h * BN * 128, &tb, k0, n0, &bfull[s]);
-                tma_load_2d(st + Cf::B_BYTES + h * BN * 128, &tbl, k0, n0, &bfull[s]);
-              }
+            } else {         // one box of 64 k x BN rows (K-major)
+              const int k0 = tap * g.C + cc * KS;
+              tma_load_2d(st, &tb, k0, n0, &bfull[s]);
+              tma_load_2d(st + Cf::B_BYTES, &tbl, k0, n0, &bfull[s]);
             }
           }
         }
@@ -237,84 +237,54 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     // (the whole warp runs the loop; elect.sync picks the issuing lane)
-    {
-      // M=128, N=BN, tf32 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
-      constexpr uint32_t idesc = make_idesc(BN) | (DG ? (1u << 16) : 0u);
-      int i = 0, c = 0;
-#ifdef FDT_PROF
-      long long t_acc = 0, t_a = 0, t_issue = 0, t0 = clock64();
-#endif
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        for (int kb = 0; kb < nk; ++kb, ++i) {
-          const int s = i % S;
-          const uint32_t ph = (i / S) & 1;
-          const int b = c & 1;
-          if (kb % PCH == 0 && c >= 2) {
-#ifdef FDT_PROF
-            long long q0 = clock64();
-#endif
-            mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
-            tc_fence_after();
-#ifdef FDT_PROF
-            t_acc += clock64() - q0;
-#endif
-          }
-#ifdef FDT_PROF
-          long long q1 = clock64();
-#endif
-          // aready[s] also covers the stage's B tiles: the converters wait for
-          // them before arriving, so the issuer makes one barrier check per
-          // stage (its checks come straight out of MMA issue time: the tensor
-          // pipe's queue is only a few instructions deep)
-          mbar_wait(&aready[s], ph);
+    // M=128, N=BN, f16 x f16 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
+    constexpr uint32_t idesc = make_idesc_f16(BN) | (DG ? (1u << 16) : 0u);
+    int i = 0, c = 0;
+    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        const int b = c & 1;
+        if (kb % PCH == 0 && c >= 2) {
+          mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
           tc_fence_after();
-#ifdef FDT_PROF
-          long long q3 = clock64();
-          t_a += q3 - q1;
-#endif
-          const uint32_t d = tmem + b * BN;
-          const uint32_t ah = tmem + Cf::A_COL + s * 2 * KS, al = ah + KS;
-          const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
-          const uint64_t dbh0 = DG ? make_desc_mn32(bh, KS * 128, 512) : make_desc_sw128(bh, 16, 1024);
-          const uint64_t dbl0 = dbh0 + (Cf::B_BYTES >> 4);
+        }
+        // aready[s] also covers the stage's B tiles: the converters wait for
+        // them before arriving, so the issuer makes one barrier check per
+        // stage (its checks come straight out of MMA issue time)
+        mbar_wait(&aready[s], ph);
+        tc_fence_after();
+        const uint32_t d = tmem + b * BN;
+        const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + KS / 2;
+        const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
+        const uint64_t dbh0 = DG ? make_desc_sw128(bh, KS * 128, 1024) : make_desc_sw128(bh, 16, 1024);
+        const uint64_t dbl0 = dbh0 + (Cf::B_BYTES >> 4);
 #pragma unroll
-          for (int ks = 0; ks < KS / 8; ++ks) {
-            // descriptor start address is (addr >> 4) in bits [0,14)
-            const uint32_t off = DG ? ks * 1024 : (ks >> 2) * BN * 128 + (ks & 3) * 32;
-            const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
-            const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
-            mma_ts_elect(d, al + 8 * ks, dbh, idesc, acc);
-            mma_ts_elect(d, ah + 8 * ks, dbl, idesc, 1u);
-            mma_ts_elect(d, ah + 8 * ks, dbh, idesc, 1u);
-          }
-          tc_commit_elect(&empty[s]);
-#ifdef FDT_PROF
-          t_issue += clock64() - q3;
-#endif
-          if (kb % PCH == PCH - 1 || kb == nk - 1) {
-            tc_commit_elect(&accfull[b]);
-            ++c;
-          }
+        for (int ks = 0; ks < KS / 16; ++ks) {
+          // descriptor start address is (addr >> 4) in bits [0,14): dgrad
+          // steps 16 k-rows (2 KB), fwd 16 fp16 of the 128-B K row (32 B)
+          const uint32_t off = DG ? ks * 2048 : ks * 32;
+          const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
+          const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
+          mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+        }
+        tc_commit_elect(&empty[s]);
+        if (kb % PCH == PCH - 1 || kb == nk - 1) {
+          tc_commit_elect(&accfull[b]);
+          ++c;
         }
       }
-#ifdef FDT_PROF
-      unsigned long long* pst = reinterpret_cast<unsigned long long*>(g.prof);
-      if (lane == 0) {
-      atomicAdd(pst + 0, (unsigned long long)(clock64() - t0));
-      atomicAdd(pst + 1, (unsigned long long)t_acc);
-      atomicAdd(pst + 2, (unsigned long long)t_a);
-      atomicAdd(pst + 3, 0ull);
-      atomicAdd(pst + 4, (unsigned long long)t_issue);
-      atomicAdd(pst + 5, (unsigned long long)i);
-      }
-#endif
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ A converters
-    // thread = TMEM lane = output pixel r of the tile; stage (cc, tap) reads
-    // the halo row of its source pixel
-    const int q = warp & 3, r = q * 32 + lane;
+    // thread = TMEM lane = output pixel r of the tile; warp half c2 converts
+    // channels [32 c2, 32 c2 + 32) of each stage, i.e. TMEM columns
+    // [16 c2, +16) of the hi half and of the lo half
+    const int q = warp & 3, c2 = (warp - CV0) >> 2, r = q * 32 + lane;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
+    const float scale = exp2i(sa);
     const int hw = g.H * g.W;
     const int rr = g.tw ? r / g.tw : 0, rc = g.tw ? r % g.tw : 0;
     int i = 0, hc = 0;
@@ -335,39 +305,36 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
         }
       }
-      for (int cc = 0; cc < cpu; ++cc, ++hc) {
+      for (int cc = 0; cc < g.C / KS / g.ksplit; ++cc, ++hc) {
         const int hs = hc & 1;
         mbar_wait(&hfull[hs], (hc >> 1) & 1);
-        const char* hbase = halo + hs * g.halo_bytes;
+        const char* hbase = halo + hs * g.halo_bytes + c2 * g.half_bytes;
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
-          if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
           const int dy = DG ? 1 - tap / 3 : tap / 3 - 1, dx = DG ? 1 - tap % 3 : tap % 3 - 1;
           const int hr = g.tw ? (rr + 1 + dy) * (g.tw + 2) + rc + 1 + dx
                               : r + g.W + 1 + dy * g.W + dx;
           const bool ok = (tmask >> tap) & 1u;
-          tc_fence_after();
-          const uint32_t a = lanebase + s * 2 * KS;
+          const char* row = hbase + hr * 128;
+          const uint32_t a = lanebase + s * Cf::A_STAGE + 16 * c2;
+          // two 16-channel passes (8 TMEM columns of hi and of lo each)
 #pragma unroll
-          // this warp's 16-channel units: part, part + NCONV/4, ...
-#pragma unroll
-          for (int k = 0; k < KS / 16 / (NCONV / 4); ++k) {
-            const int u16 = ((warp - CV0) >> 2) + k * (NCONV / 4);
-            const int c2 = u16 >> 1, j0 = (u16 & 1) * 4;
-            const char* row = hbase + c2 * g.half_bytes + hr * 128;
-            float hi[16], lo[16];
+          for (int h = 0; h < 2; ++h) {
+            uint32_t hi[8], lo[8];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              const int j = j0 + jj;
+              const int j = 4 * h + jj;
               float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
               if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
-              split(v.x, hi[4 * jj + 0], lo[4 * jj + 0]);
-              split(v.y, hi[4 * jj + 1], lo[4 * jj + 1]);
-              split(v.z, hi[4 * jj + 2], lo[4 * jj + 2]);
-              split(v.w, hi[4 * jj + 3], lo[4 * jj + 3]);
+              split_f16x2(v.x * scale, v.y * scale, hi[2 * jj], lo[2 * jj]);
+              split_f16x2(v.z * scale, v.w * scale, hi[2 * jj + 1], lo[2 * jj + 1]);
             }
-            tmem_st16(a + 16 * u16, hi);
-            tmem_st16(a + KS + 16 * u16, lo);
+            if (h == 0) {
+              if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
+              tc_fence_after();
+            }
+            tmem_st8u(a + 8 * h, hi);
+            tmem_st8u(a + KS / 2 + 8 * h, lo);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
@@ -388,6 +355,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + hf * CW;
     const int nch = (nk + PCH - 1) / PCH;
     const int r = q * 32 + lane;
+    const float unscale = exp2i(-sa) * exp2i(-sw);
     int c = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int t = u / g.ksplit, kh = u % g.ksplit;
@@ -416,18 +384,19 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                                : (long long)T.m0 + r;
       const int n0 = (t % g.nt) * BN + hf * CW;
       if (p < g.npix) {
-        if (g.ksplit > 1) {               // raw partial; fdt_finish applies the epilogue
+        if (g.ksplit > 1) {               // partial; fdt_finish applies the epilogue
           float* o = g.part + ((long long)kh * g.npix + p) * g.N + n0;
 #pragma unroll
           for (int j = 0; j < CW; j += 4)
             *reinterpret_cast<float4*>(o + j) =
-                make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                make_float4(acc[j] * unscale, acc[j + 1] * unscale, acc[j + 2] * unscale,
+                            acc[j + 3] * unscale);
         } else {
 #pragma unroll
           for (int j = 0; j < CW; j += 8) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = acc[j + e];
+            for (int e = 0; e < 8; ++e) v[e] = acc[j + e] * unscale;
             epi(p, n0 + j, g.N, v);
           }
         }
@@ -468,31 +437,19 @@ __global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long
 // Work units: output tiles, split along K (2, 4 or 8 ways) while the tiles
 // alone would leave the persistent grid under two waves -- conv5 at 14x14
 // (196 tiles on 148 SMs), or any layer at the small per-GPU batches of a
-// wide burst plan; the parts' raw sums meet in fdt_finish.
+// wide burst plan; the parts' sums meet in fdt_finish.
 inline int ksplit_for(long long tiles, int chunks) {
   int k = 1;
   while (k < 8 && tiles * k < 2LL * num_sms() && chunks % (2 * k) == 0) k *= 2;
   return k;
 }
 
-__global__ void split_lo_kernel(const float4* __restrict__ w, float4* __restrict__ lo,
-                                long long n4) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 v = w[i];
-    float4 h, l;
-    split(v.x, h.x, l.x); split(v.y, h.y, l.y);
-    split(v.z, h.z, l.z); split(v.w, h.w, l.w);
-    lo[i] = l;
-  }
-}
-
-inline bool encode(CUtensorMap* m, const float* p, int rank, const cuuint64_t* dims,
-                   const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
+inline bool encode(CUtensorMap* m, const void* p, CUtensorMapDataType dt, int rank,
+                   const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                   CUtensorMapSwizzle sw) {
   const cuuint32_t es[4] = {1, 1, 1, 1};
-  return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(p), dims,
-                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  return encode_tiled(m, dt, rank, const_cast<void*>(p), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -503,12 +460,14 @@ inline void tile2d(int H, int W, int& tw, int& th) {
     if (W % w == 0 && H % (128 / w) == 0) { tw = w; th = 128 / w; return; }
 }
 
-// wlo_ready: `wlo` already holds w - tf32(w) (the caller split the weights
-// once per update); otherwise the split runs here into the workspace.
-template <int BN, int KS, int NS, bool DG, class EPI>
-bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, float* part,
+// Workspace: [amax word of A (16 B)] [weights: hi | lo fp16 + amax word when
+// the caller did not split them] [split-K partials].
+inline size_t wsplit_bytes(long long nw) { return (size_t)(4 * nw + 16 + 15) / 16 * 16; }
+
+template <int BN, int S, bool DG, class EPI>
+bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32_t* amax_a,
                  int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
-  using Cf = Cfg<BN, KS, NS>;
+  using Cf = Cfg<BN, S>;
   Geo g;
   g.H = H; g.W = W;
   g.C = DG ? Cout : Cin;
@@ -516,22 +475,14 @@ bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, flo
   if (g.C % KS || g.N % BN) return BPX_ERR_UNSUPPORTED;
   g.npix = n * H * W;
   tile2d(H, W, g.tw, g.th);
-  if (BN == 64 && !g.tw) return BPX_ERR_UNSUPPORTED;      // halo ring would not fit
   g.mt = g.tw ? n * (H / g.th) * (W / g.tw) : cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;
   g.ksplit = ksplit_for(g.tiles, g.C / KS);
   g.units = g.tiles * g.ksplit;
   g.part = part;
-#ifdef FDT_PROF
-  static void* prof = nullptr;
-  if (!prof) cudaMalloc(&prof, 64);
-  cudaMemsetAsync(prof, 0, 64, st);
-  g.prof = prof;
-  fdt_prof_ptr = prof;
-#else
-  g.prof = nullptr;
-#endif
+  g.amax_a = amax_a;
+  g.amax_w = wt.amax;
   if (g.tw) {
     g.nhbox = 1;
     g.hbox = cdiv((g.tw + 2) * (g.th + 2), 8) * 8;
@@ -541,8 +492,8 @@ bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, flo
     g.hbox = cdiv(cdiv(hrows, g.nhbox), 8) * 8;
   }
   g.half_bytes = g.nhbox * g.hbox * 128;
-  g.halo_bytes = Cf::NCH * g.half_bytes;
-  g.halo_tx = Cf::NCH * (g.tw ? (g.tw + 2) * (g.th + 2) * 128 : g.half_bytes);
+  g.halo_bytes = NCH * g.half_bytes;
+  g.halo_tx = NCH * (g.tw ? (g.tw + 2) * (g.th + 2) * 128 : g.half_bytes);
   const int smem = Cf::smem(g.halo_bytes);
   if (smem > 227 * 1024) return BPX_ERR_UNSUPPORTED;
   CUtensorMap ta, tb, tbl;
@@ -551,42 +502,37 @@ bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, flo
     const cuuint64_t strides[3] = {(cuuint64_t)g.C * 4, (cuuint64_t)W * g.C * 4,
                                    (cuuint64_t)H * W * g.C * 4};
     const cuuint32_t box[4] = {32, (cuuint32_t)g.tw + 2, (cuuint32_t)g.th + 2, 1};
-    if (!encode(&ta, a, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!encode(&ta, a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dims, strides, box,
+                CU_TENSOR_MAP_SWIZZLE_128B))
       return BPX_ERR_INVALID_ARGUMENT;
   } else {           // activations [pixels][C]: box 32 ch x hbox rows
     const cuuint64_t dims[2] = {(cuuint64_t)g.C, (cuuint64_t)g.npix};
     const cuuint64_t strides[1] = {(cuuint64_t)g.C * 4};
     const cuuint32_t box[2] = {32, (cuuint32_t)g.hbox};
-    if (!encode(&ta, a, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!encode(&ta, a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dims, strides, box,
+                CU_TENSOR_MAP_SWIZZLE_128B))
       return BPX_ERR_INVALID_ARGUMENT;
   }
   for (int v = 0; v < 2; ++v) {
-    const float* src = v ? wlo : w;
+    const void* src = v ? wt.lo : wt.hi;
     CUtensorMap* m = v ? &tbl : &tb;
-    if (DG) {       // w as [Cout][9][Cin]: box 32 ci x 1 tap x KS co, MN-major
+    if (DG) {       // w16 as [Cout][9][Cin]: box 64 ci x 1 tap x KS co, MN-major
       const cuuint64_t dims[3] = {(cuuint64_t)Cin, 9, (cuuint64_t)Cout};
-      const cuuint64_t strides[2] = {(cuuint64_t)Cin * 4, (cuuint64_t)9 * Cin * 4};
-      const cuuint32_t box[3] = {32, 1, (cuuint32_t)KS};
-      if (!encode(m, src, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      const cuuint64_t strides[2] = {(cuuint64_t)Cin * 2, (cuuint64_t)9 * Cin * 2};
+      const cuuint32_t box[3] = {64, 1, (cuuint32_t)KS};
+      if (!encode(m, src, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
-    } else {        // w as [Cout][9*Cin]: box 32 k x BN rows, K-major
+    } else {        // w16 as [Cout][9*Cin]: box 64 k x BN rows, K-major
       const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
-      const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 4};
-      const cuuint32_t box[2] = {32, (cuuint32_t)BN};
-      if (!encode(m, src, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 2};
+      const cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)BN};
+      if (!encode(m, src, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
-  int nk = 1;
-  if (!wlo_ready) {
-    const long long n4 = (long long)Cout * 9 * Cin / 4;
-    int sgrid = (int)cdivll(n4, 256);
-    if (sgrid > 4 * num_sms()) sgrid = 4 * num_sms();
-    split_lo_kernel<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(w),
-                                           reinterpret_cast<float4*>(wlo), n4);
-    ++nk;
-  }
-  auto kern = fdt_kernel<BN, KS, NS, DG, EPI>;
+  auto kern = fdt_kernel<BN, S, DG, EPI>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -594,21 +540,56 @@ bpx_status_t run(const float* a, const float* w, float* wlo, bool wlo_ready, flo
   }
   const int grid = g.units < num_sms() ? g.units : num_sms();
   kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
-  if (g.ksplit == 1) return launch_status(nk);
+  if (g.ksplit == 1) return launch_status(1);
   const long long groups = (long long)g.npix * (g.N / 8);
   int fg = (int)cdivll(groups, 256);
   if (fg > 8 * num_sms()) fg = 8 * num_sms();
   fdt_finish<<<fg, 256, 0, st>>>(part, g.ksplit, g.npix, g.N, epi);
-  return launch_status(nk + 1);
+  return launch_status(2);
 }
 
+#ifndef FDT_S128
+#define FDT_S128 3
+#endif
+#ifndef FDT_S64
+#define FDT_S64 5
+#endif
+
 template <bool DG, class EPI>
-bpx_status_t dispatch(const float* a, const float* w, float* wlo, bool ready, float* part,
+bpx_status_t dispatch(const float* a, const F16Weights& wt, float* part, const uint32_t* amax_a,
                       int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
   const int N = DG ? Cin : Cout;
   if (N % 128 == 0)
-    return run<128, 32, 4, DG>(a, w, wlo, ready, part, n, H, W, Cin, Cout, epi, st);
-  return run<64, 64, 3, DG>(a, w, wlo, ready, part, n, H, W, Cin, Cout, epi, st);
+    return run<128, FDT_S128, DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+  return run<64, FDT_S64, DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+}
+
+// The call's operands in fp16x3 form: A's amax (from the caller or reduced
+// here into the workspace) and the weights' split (from the caller or made
+// here).  Returns the kernel launches issued.
+inline int prepare(const float* a, long long na, const uint32_t* amax_a_in, const float* w,
+                   long long nw, const F16Weights* wsplit, char* ws, const uint32_t*& amax_a,
+                   F16Weights& wt, cudaStream_t st) {
+  int k = 0;
+  uint32_t* aw = reinterpret_cast<uint32_t*>(ws);
+  amax_a = amax_a_in;
+  if (!amax_a) {
+    absmax(a, (size_t)na, aw, st);
+    amax_a = aw;
+    ++k;
+  }
+  if (wsplit && wsplit->hi) {
+    wt = *wsplit;
+  } else {
+    char* wb = ws + 16;
+    wt.hi = wb;
+    wt.lo = wb + 2 * nw;
+    wt.amax = reinterpret_cast<uint32_t*>(wb + 4 * nw);
+    f16_split(w, (size_t)nw, const_cast<void*>(wt.hi), const_cast<void*>(wt.lo),
+              const_cast<uint32_t*>(wt.amax), st);
+    k += 2;
+  }
+  return k;
 }
 
 }  // namespace fdt
@@ -616,81 +597,69 @@ bpx_status_t dispatch(const float* a, const float* w, float* wlo, bool ready, fl
 // ============================================================ entry points
 
 // Channel counts in multiples of 64, W <= 224 (two halo slots + the B stages
-// fit in 227 KB of smem).  64-wide N tiles also need a 2-D output tile.
+// fit in 227 KB of smem).
 bool fdt_conv_ok(int cin, int cout, int w) {
   if (cin % 64 || cout % 64 || w > 224) return false;
   return true;
 }
 
-// workspace: the weights' lo split, then (split-K) raw partials [ksplit][pixels][N]
+// workspace: A's amax word, the weights' split (when not supplied), then
+// split-K partials [ksplit][pixels][N]
 size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
-  const size_t wlo = (size_t)cout * 9 * cin;
+  const long long nw = (long long)cout * 9 * cin;
   const long long npix = (long long)n * h * w;
   size_t part = 0;
   for (int dg = 0; dg < 2; ++dg) {        // fwd (N = cout) and dgrad (N = cin)
     const int N = dg ? cin : cout, C = dg ? cout : cin;
-    const int ks = N % 128 == 0 ? 32 : 64;
     const long long tiles = cdivll(npix, 128) * (N / (N % 128 == 0 ? 128 : 64));
-    const int k = C % ks == 0 ? fdt::ksplit_for(tiles, C / ks) : 1;
+    const int k = C % fdt::KS == 0 ? fdt::ksplit_for(tiles, C / fdt::KS) : 1;
     if (k > 1) {
       const size_t need = (size_t)k * npix * N;
       part = part > need ? part : need;
     }
   }
-  return (wlo + part) * sizeof(float);
+  return 16 + fdt::wsplit_bytes(nw) + part * sizeof(float);
 }
 
-bpx_status_t fdt_conv_fwd(const float* x, const float* w, const float* w_lo, const float* bias,
-                          float* y, int n, int h, int w_, int cin, int cout, int relu,
-                          void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y) ||
-      !aligned16(w_lo))
+bpx_status_t fdt_conv_fwd(const float* x, const float* w, const F16Weights* wsplit,
+                          const uint32_t* amax_x, const float* bias, float* y, int n, int h,
+                          int w_, int cin, int cout, int relu, void* ws, size_t ws_bytes,
+                          cudaStream_t st) {
+  if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EBiasAct epi{y, bias, relu};
-  float* scratch = static_cast<float*>(ws);
-  float* wlo = w_lo ? const_cast<float*>(w_lo) : scratch;
-  return fdt::dispatch<false>(x, w, wlo, w_lo != nullptr, scratch + (size_t)cout * 9 * cin, n,
-                              h, w_, cin, cout, epi, st);
+  const long long nw = (long long)cout * 9 * cin;
+  char* scratch = static_cast<char*>(ws);
+  const uint32_t* amax_a;
+  F16Weights wt;
+  const int k = fdt::prepare(x, (long long)n * h * w_ * cin, amax_x, w, nw, wsplit, scratch,
+                             amax_a, wt, st);
+  count_launches(k);
+  float* part = reinterpret_cast<float*>(scratch + 16 + fdt::wsplit_bytes(nw));
+  return fdt::dispatch<false>(x, wt, part, amax_a, n, h, w_, cin, cout, epi, st);
 }
 
-bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const float* w_lo,
-                            const float* mask, float* dx, int n, int h, int w_, int cin,
-                            int cout, void* ws, size_t ws_bytes, cudaStream_t st) {
+bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const F16Weights* wsplit,
+                            const uint32_t* amax_dz, const float* mask, float* dx, int n, int h,
+                            int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
   if (!fdt_conv_ok(cin, cout, w_) || !aligned16(dz) || !aligned16(w) || !aligned16(dx) ||
-      (mask && !aligned16(mask)) || !aligned16(w_lo))
+      (mask && !aligned16(mask)))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
   fdt::EMask epi{dx, mask};
-  float* scratch = static_cast<float*>(ws);
-  float* wlo = w_lo ? const_cast<float*>(w_lo) : scratch;
-  return fdt::dispatch<true>(dz, w, wlo, w_lo != nullptr, scratch + (size_t)cout * 9 * cin, n,
-                             h, w_, cin, cout, epi, st);
+  const long long nw = (long long)cout * 9 * cin;
+  char* scratch = static_cast<char*>(ws);
+  const uint32_t* amax_a;
+  F16Weights wt;
+  const int k = fdt::prepare(dz, (long long)n * h * w_ * cout, amax_dz, w, nw, wsplit, scratch,
+                             amax_a, wt, st);
+  count_launches(k);
+  float* part = reinterpret_cast<float*>(scratch + 16 + fdt::wsplit_bytes(nw));
+  return fdt::dispatch<true>(dz, wt, part, amax_a, n, h, w_, cin, cout, epi, st);
 }
 
 }  // namespace bpx
-
-extern "C" bpx_status_t bpx_tf32_split_lo(const float* w, float* lo, size_t n, void* stream) {
-  using namespace bpx;
-  BPX_CHECK_ARG(n % 4 == 0);
-  if (n == 0) return BPX_OK;
-  BPX_CHECK_ARG(w && lo && aligned16(w) && aligned16(lo));
-  const long long n4 = (long long)(n / 4);
-  int grid = (int)cdivll(n4, 256);
-  if (grid > 4 * num_sms()) grid = 4 * num_sms();
-  fdt::split_lo_kernel<<<grid, 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float4*>(w), reinterpret_cast<float4*>(lo), n4);
-  return launch_status();
-}
-
-#ifdef FDT_PROF
-// Profiling builds only (BPX_NVCC_EXTRA=-DFDT_PROF): MMA-issuer cycles of the
-// last fdt launch -- {total, wait accfree, wait aready, 0, issue, stages}
-// summed over CTAs (tools/fdt_prof.py).
-extern "C" __attribute__((visibility("default"))) void bpx_fdt_prof(unsigned long long* out) {
-  cudaDeviceSynchronize();
-  if (bpx::fdt::fdt_prof_ptr) cudaMemcpy(out, bpx::fdt::fdt_prof_ptr, 48, cudaMemcpyDeviceToHost);
-}
-#endif

@@ -245,6 +245,68 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- fp32-accurate products on the fp16 tensor-core path ("fp16x3") ------
+// A fp32 operand tensor is scaled by a power of two 2^s chosen from its
+// absolute maximum (so every scaled |v| < 2^15) and split into two fp16
+// halves, hi = rn16(v 2^s), lo = rn16(v 2^s - hi): 22 significant bits
+// (error <= 2^-24 |v| above fp16's subnormal range, <= 2^-25 2^-s absolute
+// below it).  a.b = (a_hi b_hi + a_hi b_lo + a_lo b_hi) / (2^sa 2^sb) with
+// the dropped a_lo b_lo <= 2^-24 |a b|; kind::f16 runs at twice the tf32
+// MMA rate (K = 16 per instruction, same cycles as K = 8 tf32).
+//
+// scale exponent s for a tensor whose max |v| has bit pattern `amax_bits`
+// (max |v| < 2^(e-126) with e its biased exponent -> max |v| 2^s < 2^15)
+__host__ __device__ __forceinline__ int f16_scale_exp(uint32_t amax_bits) {
+  const int e = (int)((amax_bits >> 23) & 0xffu);
+  if (amax_bits == 0u || e == 255) return 0;
+  int s = 141 - e;
+  return s < -126 ? -126 : (s > 126 ? 126 : s);
+}
+__host__ __device__ __forceinline__ float exp2i(int s) {
+  union { uint32_t u; float f; } c;
+  c.u = (uint32_t)(s + 127) << 23;
+  return c.f;
+}
+// (a, b) already scaled -> packed fp16 hi pair and lo pair (a in the low half)
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  uint32_t h, l;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+  float ha, hb;
+  asm("{\n\t.reg .f16 x, y;\n\tmov.b32 {x, y}, %2;\n\tcvt.f32.f16 %0, x;\n\tcvt.f32.f16 %1, y;\n\t}"
+      : "=f"(ha), "=f"(hb) : "r"(h));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+  hi = h;
+  lo = l;
+}
+__host__ __device__ constexpr uint32_t make_idesc_f16(int n) {
+  // D f32 (bits 4-5 = 1), A = B = f16 (format 0), K-major A, N >> 3, M >> 4
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16, warp-converged elect issue
+__device__ __forceinline__ void mma_ts_f16_elect(uint32_t d, uint32_t a, uint64_t b_desc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d), "r"(a), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st8u(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+        "r"(v[6]), "r"(v[7]) : "memory");
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+        "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+        "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+}
+
 }  // namespace tcx
 }  // namespace bpx
 

@@ -55,7 +55,7 @@ class _Layer:
     bias: Optional[torch.Tensor] = None
     dw: Optional[torch.Tensor] = None
     dbias: Optional[torch.Tensor] = None
-    w_lo: Optional[torch.Tensor] = None    # conv: w - tf32(w), refreshed after each update
+    wsplit: Optional[object] = None        # conv: fp16x3 split of w (ops.F16Split), per update
     src_i: int = -1                        # input layer (-1: the network input / concat)
     srcs_i: tuple = ()                     # concat: joined layers
     dx_acc: bool = False                   # dx is private: accumulate into the source's dy
@@ -297,27 +297,15 @@ class BurstStep:
                 S = self.layers[j]
                 if S.active and consumers[j][-1] != i:
                     S.xdy[(i, k)] = torch.empty_like(S.dy)
-        # conv weights' 3xTF32 low parts: one split launch per bucket over
-        # its contiguous conv span, after every update (fwd and dgrad then
-        # reuse it instead of splitting per call)
-        self.lo_spans: list = []
-        if hasattr(self.k, "tf32_split_lo"):
-            spans: dict[int, list] = {}
+        # conv weights in fp16x3 form (fp16 hi/lo + scale word): split once
+        # per update (after SGD), then fwd and dgrad load them by TMA
+        self.wsplits: list = []
+        if hasattr(self.k, "F16Split"):
             for L in self.layers:
                 if L.active and L.spec.kind == "conv":
-                    off = L.w.data_ptr() - self.pbuckets[L.g].data_ptr()
-                    a, b = off // 4, off // 4 + L.w.numel()
-                    sp = spans.setdefault(L.g, [a, b])
-                    sp[0], sp[1] = min(sp[0], a), max(sp[1], b)
-            for g, (a, b) in spans.items():
-                a, b = a // 4 * 4, (b + 3) // 4 * 4
-                lo = torch.empty(b - a, dtype=torch.float32, device=dev)
-                self.lo_spans.append((self.pbuckets[g][a:b], lo))
-                for L in self.layers:
-                    if L.active and L.spec.kind == "conv" and L.g == g:
-                        o = (L.w.data_ptr() - self.pbuckets[g].data_ptr()) // 4 - a
-                        L.w_lo = lo[o:o + L.w.numel()].view(L.w.shape)
-            self._split_lo()
+                    L.wsplit = self.k.F16Split(L.w)
+                    self.wsplits.append((L.w, L.wsplit))
+            self._split_w()
         for L in self.layers:
             if L.join == "reshard":
                 S = self.layers[L.skip_i]
@@ -431,7 +419,7 @@ class BurstStep:
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
-        lo = {"w_lo": L.w_lo} if L.w_lo is not None else {}
+        lo = {"wsplit": L.wsplit} if L.wsplit is not None else {}
         if sp.bn:
             # conv without bias / activation into z, then the synchronised BN
             x = L.x
@@ -574,14 +562,14 @@ class BurstStep:
         elif sp.kind == "conv" and sp.down:
             self.k.conv3x3_wgrad(L.xs, dy, L.dw, dbias, ws=self.ws)
             self.k.conv3x3_dgrad(dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
-                                 **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
+                                 **({"wsplit": L.wsplit} if L.wsplit is not None else {}))
             if not self._fused_down(i):
                 self._sub_bwd(L)
         elif sp.kind == "conv":
             self.k.conv3x3_wgrad(L.x, dy, L.dw, dbias, ws=self.ws)
             if i > 0:
                 self.k.conv3x3_dgrad(dy, L.w, mask, L.dx, ws=self.ws,
-                                     **({"w_lo": L.w_lo} if L.w_lo is not None else {}))
+                                     **({"wsplit": L.wsplit} if L.wsplit is not None else {}))
         elif sp.kind == "pool":
             if L.idx is not None:
                 self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx)
@@ -691,11 +679,11 @@ class BurstStep:
     def _sgd(self) -> None:
         for g in sorted(self.buckets):
             self.k.sgd_update(self.pbuckets[g], self.buckets[g], self.lr)
-        self._split_lo()
+        self._split_w()
 
-    def _split_lo(self) -> None:
-        for w, lo in self.lo_spans:
-            self.k.tf32_split_lo(w, lo)
+    def _split_w(self) -> None:
+        for w, sp in self.wsplits:
+            sp.refresh(w)
 
     def run_ops(self, prog) -> None:
         for key, fn in prog:

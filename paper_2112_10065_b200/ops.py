@@ -34,11 +34,12 @@ _SIGS = {
     "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
-    "bpx_conv3x3_fwd_presplit": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_int] * 6
+    "bpx_conv3x3_fwd_presplit": (ctypes.c_int, [_c_float_p] * 8 + [ctypes.c_int] * 6
                                  + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
-    "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_int] * 5
+    "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 8 + [ctypes.c_int] * 5
                                    + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
-    "bpx_tf32_split_lo": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_absmax": (ctypes.c_int, [_c_float_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
+    "bpx_f16_split": (ctypes.c_int, [_c_float_p, ctypes.c_size_t] + [ctypes.c_void_p] * 4),
     "bpx_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
                           + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_dgrad_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
@@ -236,42 +237,92 @@ def _ws(ws: Optional[Workspace], nbytes: int, device):
 
 # ---------------------------------------------------------------- layers
 
-def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None, w_lo=None):
-    """``w_lo`` (optional): w - tf32(w) from ``tf32_split_lo``, reused across
-    calls until the weights change."""
+class F16Split:
+    """A weight tensor in fp16x3 form (bpx_f16_split): fp16 hi and lo arrays
+    in the weights' layout and the max |w| word that sets their power-of-two
+    scale.  ``refresh(w)`` re-splits after an update."""
+
+    def __init__(self, w: torch.Tensor):
+        n = w.numel()
+        self.n = n
+        self.hi = torch.empty(n, dtype=torch.float16, device=w.device)
+        self.lo = torch.empty(n, dtype=torch.float16, device=w.device)
+        self.amax = torch.zeros(4, dtype=torch.int32, device=w.device)
+
+    def refresh(self, w: torch.Tensor) -> "F16Split":
+        f16_split(w, self)
+        return self
+
+    def dequant(self) -> torch.Tensor:
+        """(hi + lo) / 2^s in fp64: what the tensor core multiplies (tests)."""
+        s = f16_scale_exp(int(self.amax[0].item()) & 0xFFFFFFFF)
+        return (self.hi.double() + self.lo.double()) * 2.0 ** (-s)
+
+
+def f16_scale_exp(amax_bits: int) -> int:
+    """Scale exponent s of a tensor whose max |v| has fp32 bits ``amax_bits``:
+    max |v| 2^s < 2^15 (tc_ptx.cuh f16_scale_exp)."""
+    e = (amax_bits >> 23) & 0xFF
+    if amax_bits == 0 or e == 255:
+        return 0
+    return max(-126, min(126, 141 - e))
+
+
+def f16_split(w, sp: F16Split):
     lib = load_library()
-    _f32(x, w, bias, y, w_lo)
+    _f32(w)
+    if w.numel() != sp.n:
+        raise KernelError("f16_split: size mismatch")
+    _check(lib.bpx_f16_split(_ptr(w), w.numel(), _ptr(sp.hi), _ptr(sp.lo), _ptr(sp.amax),
+                             _stream()), "bpx_f16_split")
+    return sp
+
+
+def absmax(x, out):
+    """out[0] (int32 tensor) = max |x| as fp32 bits."""
+    lib = load_library()
+    _f32(x)
+    _check(lib.bpx_absmax(_ptr(x), x.numel(), _ptr(out), _stream()), "bpx_absmax")
+    return out
+
+
+def _split_ptrs(wsplit):
+    if wsplit is None:
+        return None, None, None
+    return _ptr(wsplit.hi), _ptr(wsplit.lo), _ptr(wsplit.amax)
+
+
+def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None, wsplit=None,
+                x_amax=None):
+    """``wsplit`` (optional F16Split of w) and ``x_amax`` (optional int32 word
+    with max |x|, from ``absmax``) are the fp16x3 operand forms the call
+    otherwise prepares itself."""
+    lib = load_library()
+    _f32(x, w, bias, y)
     n, h, wd, cin = x.shape
     cout = w.shape[0]
     need = lib.bpx_conv3x3_fwd_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, x.device)
-    _check(lib.bpx_conv3x3_fwd_presplit(_ptr(x), _ptr(w), _ptr(w_lo), _ptr(bias), _ptr(y), n,
-                                        h, wd, cin, cout, int(relu), wp, wb, _stream()),
+    _check(lib.bpx_conv3x3_fwd_presplit(_ptr(x), _ptr(w), *_split_ptrs(wsplit), _ptr(x_amax),
+                                        _ptr(bias), _ptr(y), n, h, wd, cin, cout, int(relu),
+                                        wp, wb, _stream()),
            "bpx_conv3x3_fwd")
     return y
 
 
-def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, w_lo=None):
+def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, wsplit=None,
+                  dz_amax=None):
     lib = load_library()
-    _f32(dz, w, mask_src, dx, w_lo)
+    _f32(dz, w, mask_src, dx)
     n, h, wd, cout = dz.shape
     cin = w.shape[3]
     need = lib.bpx_conv3x3_dgrad_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, dz.device)
-    _check(lib.bpx_conv3x3_dgrad_presplit(_ptr(dz), _ptr(w), _ptr(w_lo), _ptr(mask_src),
-                                          _ptr(dx), n, h, wd, cin, cout, wp, wb, _stream()),
+    _check(lib.bpx_conv3x3_dgrad_presplit(_ptr(dz), _ptr(w), *_split_ptrs(wsplit),
+                                          _ptr(dz_amax), _ptr(mask_src), _ptr(dx), n, h, wd,
+                                          cin, cout, wp, wb, _stream()),
            "bpx_conv3x3_dgrad")
     return dx
-
-
-def tf32_split_lo(w, lo):
-    """lo = w - tf32(w) elementwise (same number of floats, multiple of 4)."""
-    lib = load_library()
-    _f32(w, lo)
-    if w.numel() != lo.numel() or w.numel() % 4:
-        raise KernelError("tf32_split_lo: sizes must match and be a multiple of 4")
-    _check(lib.bpx_tf32_split_lo(_ptr(w), _ptr(lo), w.numel(), _stream()), "bpx_tf32_split_lo")
-    return lo
 
 
 def conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):

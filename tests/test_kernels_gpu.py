@@ -354,3 +354,48 @@ def test_batchnorm_fwd_bwd(n, h, c):
     ops.bn_stats(Z, st2)
     torch.cuda.synchronize()
     assert torch.equal(y2, torch.relu(y)) and torch.equal(st, st2)
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-7, 1e5, 1e30], ids=str)
+def test_conv_fp16x3_scaling(scale):
+    # fp16x3 operands carry a power-of-two scale from each tensor's max |v|:
+    # the result is scale-invariant far outside fp16's own range, and
+    # elements ~2^-20 below the max keep their share of the norm
+    n, h, cin, cout = 2, 12, 64, 128
+    x = rnd(n, h, h, cin, seed=21) * scale
+    x[0, :3] *= 2.0 ** -20
+    w = rnd(cout, 3, 3, cin, seed=22, scale=0.05 / scale ** 0.5)
+    w[:7] *= 2.0 ** -18
+    b = torch.zeros(cout)
+    spec = LayerSpec("c", "conv", cin, cout, h, False, False)
+    ref = vgg_ref.layer_fwd(spec, x, w, b)
+    ref32 = vgg_ref.layer_fwd(spec, x, w, b, dtype=torch.float32)
+    y = torch.empty(n, h, h, cout, device=DEV)
+    ops.conv3x3_fwd(x.to(DEV), w.to(DEV), b.to(DEV), y, relu=False)
+    dz = rnd(n, h, h, cout, seed=23) * scale
+    dx_ref = vgg_ref.conv_grads(x, w, dz)[0]
+    dx32 = vgg_ref.conv_grads(x, w, dz, torch.float32)[0]
+    dx = torch.empty(n, h, h, cin, device=DEV)
+    ops.conv3x3_dgrad(dz.to(DEV), w.to(DEV), None, dx)
+    torch.cuda.synchronize()
+    close(y, ref, ref32)
+    close(dx, dx_ref, dx32)
+    # the rescaled rows too (normwise over them alone)
+    close(y[0, :3], ref[0, :3], ref32[0, :3])
+
+
+def test_f16_split_roundtrip():
+    # hi + lo reproduces w to 2^-22 relative (RN halves), scale from max |w|
+    w = rnd(4096, seed=24) * 3.0
+    w[:16] *= 2.0 ** -30
+    sp = ops.F16Split(w.to(DEV)).refresh(w.to(DEV))
+    torch.cuda.synchronize()
+    back = sp.dequant().cpu()
+    amax = int(sp.amax[0].item()) & 0xFFFFFFFF
+    assert amax == int(w.abs().max().view(torch.int32).item())
+    err = (back - w.double()).abs()
+    rel = (err[16:] / w.double()[16:].abs()).max().item()
+    assert rel < 2.0 ** -21, rel
+    # below fp16's normal range the split is exact to 2^-25 in scaled units
+    s = ops.f16_scale_exp(amax)
+    assert err[:16].max().item() <= 2.0 ** (-24 - s), err[:16].max().item()

@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--op", default=None, choices=(None, "fwd", "dgrad", "wgrad"))
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--engine", default="auto", choices=("auto", "simt"))
+    ap.add_argument("--inline-prep", action="store_true",
+                    help="conv fwd/dgrad prepare their fp16x3 operands per call "
+                         "(default: weights split and amax words made once, as the executor)")
     a = ap.parse_args()
     net = vgg16()
     dev = "cuda"
@@ -40,8 +43,13 @@ def main():
         db = torch.empty_like(bias)
         flops = l.fwd_flops() * b
         if l.kind == "conv":
-            fns = {"fwd": lambda: ops.conv3x3_fwd(x, w, bias, y, True, ws),
-                   "dgrad": lambda: ops.conv3x3_dgrad(dy, w, x, dx, ws),
+            sp = xa = dya = None
+            if not a.inline_prep and hasattr(ops, "F16Split") and l.cin % 64 == 0:
+                sp = ops.F16Split(w).refresh(w)
+                xa = ops.absmax(x, torch.zeros(4, dtype=torch.int32, device=dev))
+                dya = ops.absmax(dy, torch.zeros(4, dtype=torch.int32, device=dev))
+            fns = {"fwd": lambda: ops.conv3x3_fwd(x, w, bias, y, True, ws, wsplit=sp, x_amax=xa),
+                   "dgrad": lambda: ops.conv3x3_dgrad(dy, w, x, dx, ws, wsplit=sp, dz_amax=dya),
                    "wgrad": lambda: ops.conv3x3_wgrad(x, dy, dw, db, ws)}
             if a.engine == "simt":
                 fns = {"fwd": lambda: ops.simt_conv3x3_fwd(x, w, bias, y, True),
