@@ -54,7 +54,8 @@ BPX_API int bpx_abi_version(void);
  * a CUDA-graph replay re-runs the captured launches without counting). */
 BPX_API long long bpx_launch_count(void);
 /* Engine that served the calling thread's last conv3x3 / linear call:
- * "fdt" (TMA fwd/dgrad), "wgt" (TMA wgrad), "c1" (conv1_1 fwd), "dtc"
+ * "fdt" (TMA fwd/dgrad), "wgh" (TMA wgrad), "wgt" (conv1_1 wgrad), "c1"
+ * (conv1_1 fwd), "dtc"
  * (dense fwd/dgrad), "dwt" (dense wgrad), "dns" (dense FFMA, <= 8 rows or
  * 1000 outputs), "tc" (pixel-batched 1x1 convs); legacy: "simt", "ts",
  * "wg", "small".  Static storage.                                         */
@@ -121,6 +122,13 @@ BPX_API bpx_status_t bpx_conv3x3_wgrad(const float* x, const float* dz, float* d
                                int cout, void* ws, size_t ws_bytes,
                                void* stream);
 BPX_API size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout);
+/* Same op with the operands' max |v| words supplied (bpx_absmax; each
+ * nullable): the fp16x3 engine scales x and dz by powers of two from them. */
+BPX_API bpx_status_t bpx_conv3x3_wgrad_presplit(const float* x, const float* dz,
+                                        const unsigned* x_amax, const unsigned* dz_amax,
+                                        float* dw, float* dbias, int n, int h, int w_,
+                                        int cin, int cout, void* ws, size_t ws_bytes,
+                                        void* stream);
 
 /* y[b,out] = relu?(x[b,in] . w[out,in]^T + bias)                           */
 BPX_API bpx_status_t bpx_linear_fwd(const float* x, const float* w, const float* bias,

@@ -80,6 +80,17 @@ void absmax(const float* x, size_t n, uint32_t* amax, cudaStream_t st);
 void f16_split(const float* w, size_t n, void* hi, void* lo, uint32_t* amax, cudaStream_t st);
 }  // namespace bpx
 
+// TMA-fed weight-gradient engine, fp16x3 (tc_wgh.cu): Cin % 32, Cout % 64.
+// amax_x / amax_dz (nullable): the operands' max |v| bits (bpx_absmax).
+namespace bpx {
+bool wgh_conv_ok(int cin, int cout);
+size_t wgh_conv_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t wgh_conv_wgrad(const float* x, const float* dz, const uint32_t* amax_x,
+                            const uint32_t* amax_dz, float* dw, float* dbias, int n, int h,
+                            int w_, int cin, int cout, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
+}  // namespace bpx
+
 // TMA-fed persistent forward / data-gradient engine, fp16x3 (tc_fdt.cu).
 namespace bpx {
 bool fdt_conv_ok(int cin, int cout, int w);

@@ -56,6 +56,7 @@ class _Layer:
     dw: Optional[torch.Tensor] = None
     dbias: Optional[torch.Tensor] = None
     wsplit: Optional[object] = None        # conv: fp16x3 split of w (ops.F16Split), per update
+    amax: Optional[torch.Tensor] = None    # conv: [0] max |x| bits, [4] max |dz| bits
     src_i: int = -1                        # input layer (-1: the network input / concat)
     srcs_i: tuple = ()                     # concat: joined layers
     dx_acc: bool = False                   # dx is private: accumulate into the source's dy
@@ -299,12 +300,16 @@ class BurstStep:
                     S.xdy[(i, k)] = torch.empty_like(S.dy)
         # conv weights in fp16x3 form (fp16 hi/lo + scale word): split once
         # per update (after SGD), then fwd and dgrad load them by TMA
+        # and one max |v| word per conv operand (x for fwd + wgrad, dz for
+        # dgrad + wgrad), reduced once per step and shared by the engines
         self.wsplits: list = []
         if hasattr(self.k, "F16Split"):
-            for L in self.layers:
-                if L.active and L.spec.kind == "conv":
-                    L.wsplit = self.k.F16Split(L.w)
-                    self.wsplits.append((L.w, L.wsplit))
+            convs = [L for L in self.layers if L.active and L.spec.kind == "conv"]
+            words = torch.zeros(max(1, len(convs)) * 8, dtype=torch.int32, device=dev)
+            for j, L in enumerate(convs):
+                L.wsplit = self.k.F16Split(L.w)
+                self.wsplits.append((L.w, L.wsplit))
+                L.amax = words[8 * j:8 * j + 8]
             self._split_w()
         for L in self.layers:
             if L.join == "reshard":
@@ -416,6 +421,26 @@ class BurstStep:
         self.k.bn_bwd_apply(L.dy, L.z, L.bnf, sums, L.bias, self._bn_ntot(L), L.dz)
         return L.dz
 
+    def _xa(self, L, x) -> dict:
+        """fp16x3: max |x| word of conv L's input, reduced here (one launch)
+        and reused by the layer's weight gradient."""
+        if L.amax is None or L.spec.cin % 32:      # Cin = 3: the tf32 engines
+            return {}
+        self.k.absmax(x, L.amax[0:1])
+        return {"x_amax": L.amax[0:1]}
+
+    def _dza(self, L, dz) -> tuple:
+        """fp16x3 keyword arguments of conv L's wgrad and dgrad: the stored
+        max |x| word and max |dz| reduced here."""
+        if L.amax is None:
+            return {}, {}
+        if L.spec.cin % 32:                        # Cin = 3: the tf32 engines
+            return {}, {"wsplit": L.wsplit}
+        self.k.absmax(dz, L.amax[4:5])
+        da = {"wsplit": L.wsplit, "dz_amax": L.amax[4:5]}
+        wa = {"x_amax": L.amax[0:1], "dz_amax": L.amax[4:5]}
+        return wa, da
+
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
@@ -426,7 +451,8 @@ class BurstStep:
             if sp.down:
                 x = self._sub_fwd(L)
             if sp.kind == "conv":
-                self.k.conv3x3_fwd(x, L.w, None, L.z, relu=False, ws=self.ws, **lo)
+                self.k.conv3x3_fwd(x, L.w, None, L.z, relu=False, ws=self.ws, **lo,
+                                   **self._xa(L, x))
             else:
                 P = L.b * sp.hw * sp.hw
                 self.k.linear_fwd(x.reshape(P, sp.cin), L.w.view(sp.cout, sp.cin), None,
@@ -435,7 +461,8 @@ class BurstStep:
             return
         if sp.kind == "conv" and sp.down:
             self._sub_fwd(L)
-            self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
+            self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo,
+                               **self._xa(L, L.xs))
         elif sp.kind == "conv1x1":
             x = self._sub_fwd(L) if sp.down else L.x
             P = L.b * sp.hw * sp.hw
@@ -446,7 +473,8 @@ class BurstStep:
         elif sp.kind == "concat":
             self.k.concat_fwd(list(L.cat_in), L.y)
         elif sp.kind == "conv":
-            self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo)
+            self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo,
+                               **self._xa(L, L.x))
         elif sp.kind == "add":
             self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu)
         elif sp.kind == "gap":
@@ -560,16 +588,16 @@ class BurstStep:
         if sp.kind == "gap":
             self.k.global_avgpool_bwd(L.dy, mask, L.dx)
         elif sp.kind == "conv" and sp.down:
-            self.k.conv3x3_wgrad(L.xs, dy, L.dw, dbias, ws=self.ws)
-            self.k.conv3x3_dgrad(dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws,
-                                 **({"wsplit": L.wsplit} if L.wsplit is not None else {}))
+            wa, da = self._dza(L, dy)
+            self.k.conv3x3_wgrad(L.xs, dy, L.dw, dbias, ws=self.ws, **wa)
+            self.k.conv3x3_dgrad(dy, L.w, L.xs if sp.in_relu else None, L.dxs, ws=self.ws, **da)
             if not self._fused_down(i):
                 self._sub_bwd(L)
         elif sp.kind == "conv":
-            self.k.conv3x3_wgrad(L.x, dy, L.dw, dbias, ws=self.ws)
+            wa, da = self._dza(L, dy)
+            self.k.conv3x3_wgrad(L.x, dy, L.dw, dbias, ws=self.ws, **wa)
             if i > 0:
-                self.k.conv3x3_dgrad(dy, L.w, mask, L.dx, ws=self.ws,
-                                     **({"wsplit": L.wsplit} if L.wsplit is not None else {}))
+                self.k.conv3x3_dgrad(dy, L.w, mask, L.dx, ws=self.ws, **da)
         elif sp.kind == "pool":
             if L.idx is not None:
                 self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx)

@@ -38,6 +38,8 @@ _SIGS = {
                                  + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 8 + [ctypes.c_int] * 5
                                    + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_conv3x3_wgrad_presplit": (ctypes.c_int, [_c_float_p] * 6 + [ctypes.c_int] * 5
+                                   + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_absmax": (ctypes.c_int, [_c_float_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_f16_split": (ctypes.c_int, [_c_float_p, ctypes.c_size_t] + [ctypes.c_void_p] * 4),
     "bpx_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
@@ -325,15 +327,17 @@ def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, wsplit=No
     return dx
 
 
-def conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None):
+def conv3x3_wgrad(x, dz, dw, dbias, ws: Optional[Workspace] = None, x_amax=None,
+                  dz_amax=None):
     lib = load_library()
     _f32(x, dz, dw, dbias)
     n, h, wd, cin = x.shape
     cout = dz.shape[3]
     need = lib.bpx_conv3x3_wgrad_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, x.device)
-    _check(lib.bpx_conv3x3_wgrad(_ptr(x), _ptr(dz), _ptr(dw), _ptr(dbias), n, h,
-                                 wd, cin, cout, wp, wb, _stream()),
+    _check(lib.bpx_conv3x3_wgrad_presplit(_ptr(x), _ptr(dz), _ptr(x_amax), _ptr(dz_amax),
+                                          _ptr(dw), _ptr(dbias), n, h, wd, cin, cout, wp, wb,
+                                          _stream()),
            "bpx_conv3x3_wgrad")
     return dw
 

@@ -277,7 +277,7 @@ def test_signal_barrier_single_rank():
 # dense FFMA kernels chosen for them by measurement) -- never by a legacy
 # engine (simt / ts / tc / wg / small).
 ALLOWED = {
-    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgt"}},
+    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgh", "wgt"}},
     "dense": {"fwd": {"dtc", "dns"}, "dgrad": {"dtc", "dns"}, "wgrad": {"dwt", "dns"}},
 }
 

@@ -44,13 +44,13 @@ def main():
         flops = l.fwd_flops() * b
         if l.kind == "conv":
             sp = xa = dya = None
-            if not a.inline_prep and hasattr(ops, "F16Split") and l.cin % 64 == 0:
+            if not a.inline_prep and hasattr(ops, "F16Split") and l.cin % 32 == 0:
                 sp = ops.F16Split(w).refresh(w)
                 xa = ops.absmax(x, torch.zeros(4, dtype=torch.int32, device=dev))
                 dya = ops.absmax(dy, torch.zeros(4, dtype=torch.int32, device=dev))
             fns = {"fwd": lambda: ops.conv3x3_fwd(x, w, bias, y, True, ws, wsplit=sp, x_amax=xa),
                    "dgrad": lambda: ops.conv3x3_dgrad(dy, w, x, dx, ws, wsplit=sp, dz_amax=dya),
-                   "wgrad": lambda: ops.conv3x3_wgrad(x, dy, dw, db, ws)}
+                   "wgrad": lambda: ops.conv3x3_wgrad(x, dy, dw, db, ws, x_amax=xa, dz_amax=dya)}
             if a.engine == "simt":
                 fns = {"fwd": lambda: ops.simt_conv3x3_fwd(x, w, bias, y, True),
                        "dgrad": lambda: ops.simt_conv3x3_dgrad(dy, w, x, dx),
