@@ -85,12 +85,14 @@ BPX_API size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout
  * (fp16 [cout][3][3][cin] each, and the split span's max |w| bits), made
  * once per update instead of once per call; x_amax = max |x| as bits
  * (bpx_absmax, or written by the producer of x).  Each may be NULL (the
- * call then prepares it in its workspace).  bpx_conv3x3_dgrad_presplit
- * likewise, with dz_amax for dz.                                          */
+ * call then prepares it in its workspace).  y_amax (nullable): atomicMax'ed
+ * with the max |y| bits -- the next conv's x_amax, fused into this
+ * producer (zero it first).  bpx_conv3x3_dgrad_presplit likewise, with
+ * dz_amax for dz and dx_amax for dx.                                       */
 BPX_API bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w,
                                       const void* w_hi, const void* w_lo,
                                       const unsigned* w_amax, const unsigned* x_amax,
-                                      const float* bias, float* y,
+                                      unsigned* y_amax, const float* bias, float* y,
                                       int n, int h, int w_, int cin, int cout, int relu,
                                       void* ws, size_t ws_bytes, void* stream);
 /* *amax = max |x[i]| as its fp32 bit pattern (x 16-B aligned).           */
@@ -100,6 +102,15 @@ BPX_API bpx_status_t bpx_absmax(const float* x, size_t n, unsigned* amax, void* 
  * fp16 each (8-B aligned), in w's layout.                                  */
 BPX_API bpx_status_t bpx_f16_split(const float* w, size_t n, void* hi, void* lo,
                                    unsigned* amax, void* stream);
+/* Batched bpx_f16_split of nseg weight tensors in three graph nodes (a
+ * memset of the nwords amax words, one max launch, one split launch): segs
+ * is a DEVICE array of records {const float* w; void* hi; void* lo;
+ * unsigned* amax; int64 n4; int64 blk0}, n4 = floats / 4 (w 16-B aligned,
+ * hi/lo 8-B aligned), blk0 = the segment's first block with
+ * bpx_f16_split_batch_chunk() float4 per block; blocks = the total.        */
+BPX_API bpx_status_t bpx_f16_split_batch(const void* segs, int nseg, long long blocks,
+                                         unsigned* words, size_t nwords, void* stream);
+BPX_API int bpx_f16_split_batch_chunk(void);
 
 /* dx = conv3x3_transpose(dz, w) [* (mask_src > 0) if mask_src != NULL].
  * dz:[n,h,w,cout] dx,mask_src:[n,h,w,cin].  mask_src is the layer input
@@ -112,7 +123,7 @@ BPX_API size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int co
 BPX_API bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w,
                                         const void* w_hi, const void* w_lo,
                                         const unsigned* w_amax, const unsigned* dz_amax,
-                                        const float* mask_src, float* dx,
+                                        unsigned* dx_amax, const float* mask_src, float* dx,
                                         int n, int h, int w_, int cin, int cout, void* ws,
                                         size_t ws_bytes, void* stream);
 
@@ -154,11 +165,14 @@ BPX_API bpx_status_t bpx_maxpool2x2_bwd(const float* x, const float* dy, float* 
                                 int n, int h, int w_, int c, void* stream);
 /* Same pool, keeping each window's first-max position (idx: one byte per
  * output element, values 0..3 in (row, col) order) for a backward that
- * reads idx + dy instead of x + dy.                                        */
+ * reads idx + dy instead of x + dy.  y_amax / dx_amax (nullable):
+ * atomicMax'ed with the max |v| bits of the output (the consumer conv's
+ * fp16x3 scale word; zero it before the step).                             */
 BPX_API bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* idx, int n,
-                                    int h, int w_, int c, void* stream);
+                                    int h, int w_, int c, unsigned* y_amax, void* stream);
 BPX_API bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* dx,
-                                    int n, int h, int w_, int c, void* stream);
+                                    int n, int h, int w_, int c, unsigned* dx_amax,
+                                    void* stream);
 
 /* ---- branch/join elements of the residual net behind `wideresnet_like`
  * (synth.py:126-169; the `add` layers of its residual diamonds, the stage

@@ -35,8 +35,19 @@ size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout) {
 bpx_status_t bpx_conv3x3_fwd(const float* x, const float* w, const float* bias, float* y,
                              int n, int h, int w_, int cin, int cout, int relu, void* ws,
                              size_t ws_bytes, void* stream) {
-  return bpx_conv3x3_fwd_presplit(x, w, nullptr, nullptr, nullptr, nullptr, bias, y, n, h, w_,
-                                  cin, cout, relu, ws, ws_bytes, stream);
+  return bpx_conv3x3_fwd_presplit(x, w, nullptr, nullptr, nullptr, nullptr, nullptr, bias, y, n,
+                                  h, w_, cin, cout, relu, ws, ws_bytes, stream);
+}
+
+// The fdt / c1 epilogues reduce max |out| into the caller's word; the
+// legacy engines do not, so the call does it after them.
+static bpx_status_t with_amax(bpx_status_t s, const float* out, size_t n, unsigned* amax,
+                              cudaStream_t st) {
+  if (s == BPX_OK && amax && n) {
+    absmax_into(out, n, amax, st);
+    count_launches(1);
+  }
+  return s;
 }
 
 static bool split_args(const void* hi, const void* lo, const unsigned* amax, F16Weights& wt) {
@@ -48,9 +59,10 @@ static bool split_args(const void* hi, const void* lo, const unsigned* amax, F16
 
 bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const void* w_hi,
                                       const void* w_lo, const unsigned* w_amax,
-                                      const unsigned* x_amax, const float* bias, float* y,
-                                      int n, int h, int w_, int cin, int cout, int relu,
-                                      void* ws, size_t ws_bytes, void* stream) {
+                                      const unsigned* x_amax, unsigned* y_amax,
+                                      const float* bias, float* y, int n, int h, int w_,
+                                      int cin, int cout, int relu, void* ws, size_t ws_bytes,
+                                      void* stream) {
   BPX_CHECK_ARG(x && w && y && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cout % 4 == 0 && aligned16(y) && aligned16(w));
   F16Weights wt;
@@ -58,22 +70,31 @@ bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const void
   cudaStream_t st = as_stream(stream);
   if (c1_conv_fwd_ok(cin, cout)) {
     use("c1");
-    bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, st);
+    bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, y_amax, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
+  const size_t ny = (size_t)n * h * w_ * cout;
   if (small_conv_fwd_ok(cin, cout))
-    return legacy("small"), small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
+    return legacy("small"),
+           with_amax(small_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st), y, ny, y_amax,
+                     st);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(x)) {
     use("fdt");
-    bpx_status_t s = fdt_conv_fwd(x, w, wt.hi ? &wt : nullptr, x_amax, bias, y, n, h, w_, cin,
-                                  cout, relu, ws, ws_bytes, st);
+    bpx_status_t s = fdt_conv_fwd(x, w, wt.hi ? &wt : nullptr, x_amax, y_amax, bias, y, n, h,
+                                  w_, cin, cout, relu, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
   if (ts_conv_ok(cin, cout))
-    return legacy("ts"), ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
+    return legacy("ts"),
+           with_amax(ts_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st), y,
+                     ny, y_amax, st);
   if (tc_conv_fwd_ok(n, h, w_, cin, cout))
-    return legacy("tc"), tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st);
-  return legacy("simt"), simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st);
+    return legacy("tc"),
+           with_amax(tc_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, ws, ws_bytes, st), y,
+                     ny, y_amax, st);
+  return legacy("simt"),
+         with_amax(simt_conv_fwd(x, w, bias, y, n, h, w_, cin, cout, relu, st), y, ny, y_amax,
+                   st);
 }
 
 size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
@@ -86,15 +107,16 @@ size_t bpx_conv3x3_dgrad_workspace(int n, int h, int w_, int cin, int cout) {
 bpx_status_t bpx_conv3x3_dgrad(const float* dz, const float* w, const float* mask_src,
                                float* dx, int n, int h, int w_, int cin, int cout,
                                void* ws, size_t ws_bytes, void* stream) {
-  return bpx_conv3x3_dgrad_presplit(dz, w, nullptr, nullptr, nullptr, nullptr, mask_src, dx, n,
-                                    h, w_, cin, cout, ws, ws_bytes, stream);
+  return bpx_conv3x3_dgrad_presplit(dz, w, nullptr, nullptr, nullptr, nullptr, nullptr, mask_src,
+                                    dx, n, h, w_, cin, cout, ws, ws_bytes, stream);
 }
 
 bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w, const void* w_hi,
                                         const void* w_lo, const unsigned* w_amax,
-                                        const unsigned* dz_amax, const float* mask_src,
-                                        float* dx, int n, int h, int w_, int cin, int cout,
-                                        void* ws, size_t ws_bytes, void* stream) {
+                                        const unsigned* dz_amax, unsigned* dx_amax,
+                                        const float* mask_src, float* dx, int n, int h, int w_,
+                                        int cin, int cout, void* ws, size_t ws_bytes,
+                                        void* stream) {
   BPX_CHECK_ARG(dz && w && dx && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(cin % 4 == 0 && aligned16(dx) && aligned16(w));
   F16Weights wt;
@@ -102,15 +124,22 @@ bpx_status_t bpx_conv3x3_dgrad_presplit(const float* dz, const float* w, const v
   cudaStream_t st = as_stream(stream);
   if (fdt_conv_ok(cin, cout, w_) && aligned16(dz) && (!mask_src || aligned16(mask_src))) {
     use("fdt");
-    bpx_status_t s = fdt_conv_dgrad(dz, w, wt.hi ? &wt : nullptr, dz_amax, mask_src, dx, n, h,
-                                    w_, cin, cout, ws, ws_bytes, st);
+    bpx_status_t s = fdt_conv_dgrad(dz, w, wt.hi ? &wt : nullptr, dz_amax, dx_amax, mask_src, dx,
+                                    n, h, w_, cin, cout, ws, ws_bytes, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
   }
+  const size_t nx = (size_t)n * h * w_ * cin;
   if (ts_conv_ok(cin, cout))
-    return legacy("ts"), ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
+    return legacy("ts"),
+           with_amax(ts_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st),
+                     dx, nx, dx_amax, st);
   if (tc_conv_dgrad_ok(n, h, w_, cin, cout))
-    return legacy("tc"), tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st);
-  return legacy("simt"), simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st);
+    return legacy("tc"),
+           with_amax(tc_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, ws, ws_bytes, st),
+                     dx, nx, dx_amax, st);
+  return legacy("simt"),
+         with_amax(simt_conv_dgrad(dz, w, mask_src, dx, n, h, w_, cin, cout, st), dx, nx,
+                   dx_amax, st);
 }
 
 size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {

@@ -44,7 +44,7 @@ constexpr int SMEM = 1024 + 2 * COUT * KP * 4 + 2 * STAGE_OUT + 128;
 __global__ void __launch_bounds__(NTHREADS, CPS)
 c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
               const float* __restrict__ bias, const __grid_constant__ CUtensorMap ty, int H,
-              int W, long long npix, int relu) {
+              int W, long long npix, int relu, uint32_t* __restrict__ amax) {
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -152,6 +152,7 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
 #pragma unroll
     for (int j = 0; j < COUT; ++j) bv[j] = bias ? __ldg(bias + j) : 0.f;
     if (dtid == 0) tma_prefetch_desc(&ty);
+    uint32_t mx = 0;                      // max |y| bits of this thread's valid rows
     int it = 0;
     for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int b = it & 1;
@@ -172,6 +173,7 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
         for (int u = 0; u < 8; ++u) {
           const float s = __uint_as_float(rr[u]) + bv[j + u];
           o[u] = relu ? fmaxf(s, 0.f) : s;
+          if (t * 128 + r < npix) mx = max(mx, __float_as_uint(o[u]) & 0x7fffffffu);
         }
         // box j/32, row r, 16-B granule (j%32)/4 (+1), 128-B swizzle
         char* row = st + (j >> 5) * (STAGE_OUT / 2) + r * 128;
@@ -193,6 +195,10 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
       }
     }
     if (dtid == 0) bulk_wait_all();
+    if (amax) {
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (lane == 0 && mx) atomicMax(amax, mx);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -207,7 +213,7 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
 bool c1_conv_fwd_ok(int cin, int cout) { return cin == 3 && cout == c1::COUT; }
 
 bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                         int h, int w_, int relu, cudaStream_t st) {
+                         int h, int w_, int relu, uint32_t* y_amax, cudaStream_t st) {
   const long long npix = (long long)n * h * w_;
   if (npix == 0) return launch_status(0);
   if (!aligned16(y) || npix > 0x7fffffffLL) return BPX_ERR_UNSUPPORTED;
@@ -231,7 +237,8 @@ bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, floa
   }
   const long long tiles = (npix + 127) / 128;
   const int grid = (int)(tiles < c1::CPS * num_sms() ? tiles : c1::CPS * num_sms());
-  c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, ty, h, w_, npix, relu);
+  c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, ty, h, w_, npix, relu,
+                                                               y_amax);
   return launch_status();
 }
 

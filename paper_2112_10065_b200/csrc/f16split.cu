@@ -60,6 +60,55 @@ __global__ void split_kernel(const float4* __restrict__ w, long long n4,
   }
 }
 
+// Batched split of several weight tensors (one launch each for the maxima
+// and the split, whatever the layer count): block b serves segment k with
+// blk0[k] <= b < blk0[k+1], CHUNK float4 per block.
+struct Seg {
+  const float4* w; uint2* hi; uint2* lo; uint32_t* amax; long long n4, blk0;
+};
+constexpr int CHUNK = 2048;          // float4 per block: 8 per thread
+
+__device__ __forceinline__ int seg_of(const Seg* segs, int nseg, long long b) {
+  int k = 0;
+  while (k + 1 < nseg && segs[k + 1].blk0 <= b) ++k;
+  return k;
+}
+
+__global__ void absmax_batch_kernel(const Seg* __restrict__ segs, int nseg) {
+  const int k = seg_of(segs, nseg, blockIdx.x);
+  const Seg sg = segs[k];
+  const long long i0 = (blockIdx.x - sg.blk0) * (long long)CHUNK;
+  uint32_t m = 0;
+#pragma unroll 4
+  for (int j = threadIdx.x; j < CHUNK; j += blockDim.x) {
+    if (i0 + j < sg.n4) {
+      const float4 v = __ldg(sg.w + i0 + j);
+      m = max(m, max(max(absbits(v.x), absbits(v.y)), max(absbits(v.z), absbits(v.w))));
+    }
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(sg.amax, m);
+}
+
+__global__ void split_batch_kernel(const Seg* __restrict__ segs, int nseg) {
+  const int k = seg_of(segs, nseg, blockIdx.x);
+  const Seg sg = segs[k];
+  const float s = exp2i(f16_scale_exp(*sg.amax));
+  const long long i0 = (blockIdx.x - sg.blk0) * (long long)CHUNK;
+#pragma unroll 4
+  for (int j = threadIdx.x; j < CHUNK; j += blockDim.x) {
+    const long long i = i0 + j;
+    if (i < sg.n4) {
+      const float4 v = __ldg(sg.w + i);
+      uint2 h, l;
+      split_f16x2(v.x * s, v.y * s, h.x, l.x);
+      split_f16x2(v.z * s, v.w * s, h.y, l.y);
+      sg.hi[i] = h;
+      sg.lo[i] = l;
+    }
+  }
+}
+
 inline int grid_for(long long n4) {
   long long g = cdivll(n4 > 0 ? n4 : 1, 256);
   const long long cap = 4LL * num_sms();
@@ -67,6 +116,13 @@ inline int grid_for(long long n4) {
 }
 
 }  // namespace f16s
+
+// *amax = max(*amax, max |x[i]| as bits): one reduction launch
+void absmax_into(const float* x, size_t n, uint32_t* amax, cudaStream_t st) {
+  const long long n4 = (long long)(n / 4);
+  f16s::absmax_kernel<<<f16s::grid_for(n4), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(x), n4, x + 4 * n4, (int)(n % 4), amax);
+}
 
 // *amax = max |x[i]| as bits (a memset and one reduction launch)
 void absmax(const float* x, size_t n, uint32_t* amax, cudaStream_t st) {
@@ -86,6 +142,24 @@ void f16_split(const float* w, size_t n, void* hi, void* lo, uint32_t* amax, cud
 }
 
 }  // namespace bpx
+
+// segs: a DEVICE array of nseg {w, hi, lo, amax, n4, blk0} records (each
+// n = 4 n4 floats, blk0 = the first block of the segment, blocks = the
+// total); words/nwords: every amax word of the batch (zeroed here).
+extern "C" bpx_status_t bpx_f16_split_batch(const void* segs, int nseg, long long blocks,
+                                            unsigned* words, size_t nwords, void* stream) {
+  using namespace bpx;
+  BPX_CHECK_ARG(nseg >= 0 && blocks >= 0 && (nseg == 0 || (segs && words)));
+  if (nseg == 0 || blocks == 0) return BPX_OK;
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(words, 0, nwords * sizeof(unsigned), st);
+  const f16s::Seg* sg = static_cast<const f16s::Seg*>(segs);
+  f16s::absmax_batch_kernel<<<(unsigned)blocks, 256, 0, st>>>(sg, nseg);
+  f16s::split_batch_kernel<<<(unsigned)blocks, 256, 0, st>>>(sg, nseg);
+  return launch_status(2);
+}
+
+extern "C" int bpx_f16_split_batch_chunk(void) { return bpx::f16s::CHUNK; }
 
 extern "C" bpx_status_t bpx_absmax(const float* x, size_t n, unsigned* amax, void* stream) {
   using namespace bpx;

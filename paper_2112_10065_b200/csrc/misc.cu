@@ -218,10 +218,24 @@ __device__ __forceinline__ unsigned char argmax4(float a, float b, float c, floa
   return k;
 }
 
+__device__ __forceinline__ uint32_t abs4(float4 v) {
+  const uint32_t m = 0x7fffffffu;
+  return max(max(__float_as_uint(v.x) & m, __float_as_uint(v.y) & m),
+             max(__float_as_uint(v.z) & m, __float_as_uint(v.w) & m));
+}
+// amax (nullable): atomicMax'ed with the max |v| bits written (fp16x3 scale)
+__device__ __forceinline__ void commit_amax(uint32_t* amax, uint32_t mx) {
+  if (!amax) return;
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(amax, mx);
+}
+
 __global__ void maxpool_fwd_idx_kernel(const float4* __restrict__ x, float4* __restrict__ y,
-                                       uchar4* __restrict__ idx, int n, int h, int w, int c4) {
+                                       uchar4* __restrict__ idx, int n, int h, int w, int c4,
+                                       uint32_t* amax) {
   const int oh = h / 2, ow = w / 2;
   const long long total = (long long)n * oh * ow * c4;
+  uint32_t mx = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % c4); long long p = i / c4;
@@ -238,14 +252,17 @@ __global__ void maxpool_fwd_idx_kernel(const float4* __restrict__ x, float4* __r
     k.w = argmax4(a.w, bb.w, cc.w, d.w, r.w);
     y[i] = r;
     idx[i] = k;
+    mx = max(mx, abs4(r));
   }
+  commit_amax(amax, mx);
 }
 
 __global__ void maxpool_bwd_idx_kernel(const uchar4* __restrict__ idx,
                                        const float4* __restrict__ dy, float4* __restrict__ dx,
-                                       int n, int h, int w, int c4) {
+                                       int n, int h, int w, int c4, uint32_t* amax) {
   const int oh = h / 2, ow = w / 2;
   const long long total = (long long)n * oh * ow * c4;
+  uint32_t mx = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % c4); long long p = i / c4;
@@ -264,7 +281,9 @@ __global__ void maxpool_bwd_idx_kernel(const uchar4* __restrict__ idx,
       r[j].w = k.w == j ? g.w : 0.f;
     }
     dx[o] = r[0]; dx[o + c4] = r[1]; dx[o + rs] = r[2]; dx[o + rs + c4] = r[3];
+    mx = max(mx, max(max(abs4(r[0]), abs4(r[1])), max(abs4(r[2]), abs4(r[3]))));
   }
+  commit_amax(amax, mx);
 }
 
 static int ew_grid(long long work) {
@@ -413,26 +432,26 @@ bpx_status_t bpx_maxpool2x2_bwd(const float* x, const float* dy, float* dx, int 
 }
 
 bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* idx, int n, int h,
-                                    int w_, int c, void* stream) {
+                                    int w_, int c, unsigned* y_amax, void* stream) {
   BPX_CHECK_ARG(x && y && idx && n >= 0 && h % 2 == 0 && w_ % 2 == 0 && c % 4 == 0);
   BPX_CHECK_ARG(aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
   long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
   if (total == 0) return BPX_OK;
   maxpool_fwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
-      reinterpret_cast<uchar4*>(idx), n, h, w_, c / 4);
+      reinterpret_cast<uchar4*>(idx), n, h, w_, c / 4, y_amax);
   return launch_status();
 }
 
 bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* dx, int n,
-                                    int h, int w_, int c, void* stream) {
+                                    int h, int w_, int c, unsigned* dx_amax, void* stream) {
   BPX_CHECK_ARG(idx && dy && dx && n >= 0 && h % 2 == 0 && w_ % 2 == 0 && c % 4 == 0);
   BPX_CHECK_ARG(aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
   long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
   if (total == 0) return BPX_OK;
   maxpool_bwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const uchar4*>(idx), reinterpret_cast<const float4*>(dy),
-      reinterpret_cast<float4*>(dx), n, h, w_, c / 4);
+      reinterpret_cast<float4*>(dx), n, h, w_, c / 4, dx_amax);
   return launch_status();
 }
 

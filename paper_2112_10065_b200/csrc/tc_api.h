@@ -77,6 +77,7 @@ struct F16Weights {
   const uint32_t* amax = nullptr;    // max |w| bits of the split span (sets the scale)
 };
 void absmax(const float* x, size_t n, uint32_t* amax, cudaStream_t st);
+void absmax_into(const float* x, size_t n, uint32_t* amax, cudaStream_t st);   // no reset
 void f16_split(const float* w, size_t n, void* hi, void* lo, uint32_t* amax, cudaStream_t st);
 }  // namespace bpx
 
@@ -97,14 +98,15 @@ bool fdt_conv_ok(int cin, int cout, int w);
 size_t fdt_conv_ws(int n, int h, int w, int cin, int cout);
 // wsplit (nullable): the weights split by the caller (bpx_f16_split);
 // amax_x / amax_dz (nullable): the A operand's max |v| bits (bpx_absmax)
+// amax_y / amax_dx (nullable): atomicMax'ed with the output's max |v| bits
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const F16Weights* wsplit,
-                          const uint32_t* amax_x, const float* bias, float* y, int n, int h,
-                          int w_, int cin, int cout, int relu, void* ws, size_t ws_bytes,
-                          cudaStream_t st);
+                          const uint32_t* amax_x, uint32_t* amax_y, const float* bias, float* y,
+                          int n, int h, int w_, int cin, int cout, int relu, void* ws,
+                          size_t ws_bytes, cudaStream_t st);
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const F16Weights* wsplit,
-                            const uint32_t* amax_dz, const float* mask, float* dx, int n, int h,
-                            int w_, int cin, int cout, void* ws, size_t ws_bytes,
-                            cudaStream_t st);
+                            const uint32_t* amax_dz, uint32_t* amax_dx, const float* mask,
+                            float* dx, int n, int h, int w_, int cin, int cout, void* ws,
+                            size_t ws_bytes, cudaStream_t st);
 }  // namespace bpx
 
 // TMA-fed tcgen05 dense fwd / dgrad for batches <= 32 (tc_dense.cu).

@@ -87,23 +87,30 @@ struct Geo {
   const uint32_t* amax_w;    // max |w| bits of the weights' span
 };
 
+// Epilogues return the max |v| bits of what they stored: the drain reduces
+// them into *amax (the output's fp16x3 scale word for its consumers).
+__device__ __forceinline__ uint32_t absbits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+
 struct EBiasAct {
-  float* out; const float* bias; int relu;
-  __device__ void operator()(long long m, int n0, int N, const float (&v)[8]) const {
+  float* out; const float* bias; int relu; uint32_t* amax;
+  __device__ uint32_t operator()(long long m, int n0, int N, const float (&v)[8]) const {
     float* o = out + m * N + n0;
     float r[8];
+    uint32_t mx = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float t = v[j] + (bias ? __ldg(bias + n0 + j) : 0.f);
       r[j] = relu ? fmaxf(t, 0.f) : t;
+      mx = max(mx, absbits(r[j]));
     }
     *reinterpret_cast<float4*>(o) = make_float4(r[0], r[1], r[2], r[3]);
     *reinterpret_cast<float4*>(o + 4) = make_float4(r[4], r[5], r[6], r[7]);
+    return mx;
   }
 };
 struct EMask {
-  float* out; const float* mask;
-  __device__ void operator()(long long m, int n0, int N, const float (&v)[8]) const {
+  float* out; const float* mask; uint32_t* amax;
+  __device__ uint32_t operator()(long long m, int n0, int N, const float (&v)[8]) const {
     float* o = out + m * N + n0;
     float4 a = make_float4(v[0], v[1], v[2], v[3]);
     float4 b = make_float4(v[4], v[5], v[6], v[7]);
@@ -118,8 +125,15 @@ struct EMask {
     }
     *reinterpret_cast<float4*>(o) = a;
     *reinterpret_cast<float4*>(o + 4) = b;
+    return max(max(max(absbits(a.x), absbits(a.y)), max(absbits(a.z), absbits(a.w))),
+               max(max(absbits(b.x), absbits(b.y)), max(absbits(b.z), absbits(b.w))));
   }
 };
+__device__ __forceinline__ void amax_commit(uint32_t* amax, uint32_t mx) {
+  if (!amax) return;
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(amax, mx);
+}
 
 // Output-tile geometry shared by the producer, converters and epilogue.
 struct Tile {
@@ -356,6 +370,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int nch = (nk + PCH - 1) / PCH;
     const int r = q * 32 + lane;
     const float unscale = exp2i(-sa) * exp2i(-sw);
+    uint32_t mx = 0;
     int c = 0;
     for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
       const int t = u / g.ksplit, kh = u % g.ksplit;
@@ -397,11 +412,12 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = acc[j + e] * unscale;
-            epi(p, n0 + j, g.N, v);
+            mx = max(mx, epi(p, n0 + j, g.N, v));
           }
         }
       }
     }
+    if (g.ksplit == 1) amax_commit(epi.amax, mx);
   }
 
   tc_fence_before();
@@ -419,6 +435,7 @@ template <class EPI>
 __global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long npix, int N,
                            EPI epi) {
   const long long groups = npix * (N / 8);
+  uint32_t mx = 0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < groups;
        e += (long long)gridDim.x * blockDim.x) {
     const long long p = e / (N / 8);
@@ -430,8 +447,9 @@ __global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long
       v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
       v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
     }
-    epi(p, n0, N, v);
+    mx = max(mx, epi(p, n0, N, v));
   }
+  amax_commit(epi.amax, mx);
 }
 
 // Work units: output tiles, split along K (2, 4 or 8 ways) while the tiles
@@ -622,14 +640,14 @@ size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
 }
 
 bpx_status_t fdt_conv_fwd(const float* x, const float* w, const F16Weights* wsplit,
-                          const uint32_t* amax_x, const float* bias, float* y, int n, int h,
-                          int w_, int cin, int cout, int relu, void* ws, size_t ws_bytes,
-                          cudaStream_t st) {
+                          const uint32_t* amax_x, uint32_t* amax_y, const float* bias, float* y,
+                          int n, int h, int w_, int cin, int cout, int relu, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
   if (!fdt_conv_ok(cin, cout, w_) || !aligned16(x) || !aligned16(w) || !aligned16(y))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
-  fdt::EBiasAct epi{y, bias, relu};
+  fdt::EBiasAct epi{y, bias, relu, amax_y};
   const long long nw = (long long)cout * 9 * cin;
   char* scratch = static_cast<char*>(ws);
   const uint32_t* amax_a;
@@ -642,15 +660,15 @@ bpx_status_t fdt_conv_fwd(const float* x, const float* w, const F16Weights* wspl
 }
 
 bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const F16Weights* wsplit,
-                            const uint32_t* amax_dz, const float* mask, float* dx, int n, int h,
-                            int w_, int cin, int cout, void* ws, size_t ws_bytes,
-                            cudaStream_t st) {
+                            const uint32_t* amax_dz, uint32_t* amax_dx, const float* mask,
+                            float* dx, int n, int h, int w_, int cin, int cout, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
   if (!fdt_conv_ok(cin, cout, w_) || !aligned16(dz) || !aligned16(w) || !aligned16(dx) ||
       (mask && !aligned16(mask)))
     return BPX_ERR_INVALID_ARGUMENT;
   if ((long long)n * h * w_ == 0) return launch_status(0);
   if (ws_bytes < fdt_conv_ws(n, h, w_, cin, cout) || !aligned16(ws)) return BPX_ERR_WORKSPACE;
-  fdt::EMask epi{dx, mask};
+  fdt::EMask epi{dx, mask, amax_dx};
   const long long nw = (long long)cout * 9 * cin;
   char* scratch = static_cast<char*>(ws);
   const uint32_t* amax_a;

@@ -57,6 +57,10 @@ class _Layer:
     dbias: Optional[torch.Tensor] = None
     wsplit: Optional[object] = None        # conv: fp16x3 split of w (ops.F16Split), per update
     amax: Optional[torch.Tensor] = None    # conv: [0] max |x| bits, [4] max |dz| bits
+    x_fused: bool = False                  # amax[0] written by the producer of x
+    dz_fused: bool = False                 # amax[4] written by the writer of dy
+    y_amax: Optional[torch.Tensor] = None  # word this layer's fwd kernel max-reduces y into
+    dx_amax: Optional[torch.Tensor] = None  # word this layer's bwd kernel reduces dx into
     src_i: int = -1                        # input layer (-1: the network input / concat)
     srcs_i: tuple = ()                     # concat: joined layers
     dx_acc: bool = False                   # dx is private: accumulate into the source's dy
@@ -302,15 +306,18 @@ class BurstStep:
         # per update (after SGD), then fwd and dgrad load them by TMA
         # and one max |v| word per conv operand (x for fwd + wgrad, dz for
         # dgrad + wgrad), reduced once per step and shared by the engines
-        self.wsplits: list = []
+        self.wbatch = None
+        self.amax_words = None
         if hasattr(self.k, "F16Split"):
             convs = [L for L in self.layers if L.active and L.spec.kind == "conv"]
             words = torch.zeros(max(1, len(convs)) * 8, dtype=torch.int32, device=dev)
+            self.wbatch = self.k.F16SplitBatch([L.w for L in convs]) if convs else None
             for j, L in enumerate(convs):
-                L.wsplit = self.k.F16Split(L.w)
-                self.wsplits.append((L.w, L.wsplit))
+                L.wsplit = self.wbatch.splits[j]
                 L.amax = words[8 * j:8 * j + 8]
             self._split_w()
+            self.amax_words = words
+            self._fuse_amax(consumers)
         for L in self.layers:
             if L.join == "reshard":
                 S = self.layers[L.skip_i]
@@ -421,12 +428,48 @@ class BurstStep:
         self.k.bn_bwd_apply(L.dy, L.z, L.bnf, sums, L.bias, self._bn_ntot(L), L.dz)
         return L.dz
 
+    def _fuse_amax(self, consumers) -> None:
+        """Fuse each conv's fp16x3 scale words into the kernels that write its
+        operands where that kernel writes the operand buffer itself: x from
+        a conv forward (fdt / c1 epilogue) or a 2x2 max pool on the same g
+        (a chain edge, no reshard), dz from the dgrad of its only consumer
+        (a conv or a pool) on the same g.  Every other operand gets one
+        bpx_absmax launch.  The words are zeroed at the start of the step's
+        forward (first active layer)."""
+        self.first_active = min((i for i, L in enumerate(self.layers) if L.active), default=-1)
+        if os.environ.get("BPX_FUSE_AMAX", "1") == "0":
+            return
+        for i, L in enumerate(self.layers):
+            sp = L.spec
+            if L.amax is None or sp.cin % 32 or sp.bn or sp.down:
+                continue
+            if L.src_i >= 0 and not L.reshard_in and self.layers[L.src_i].g == L.g:
+                S = self.layers[L.src_i]
+                if ((S.spec.kind == "conv" and not S.spec.bn) or
+                        (S.spec.kind == "pool" and S.idx is not None)):
+                    S.y_amax = L.amax[0:1]
+                    L.x_fused = True
+            cons = consumers[i]
+            if len(cons) == 1:
+                C = self.layers[cons[0]]
+                # (an inactive consumer's flags are never set: compare g)
+                if (C.active and C.g == L.g and not C.reshard_in and not C.dx_acc and
+                        not C.spec.bn and
+                        ((C.spec.kind == "conv" and not C.spec.down and C.spec.cin % 32 == 0) or
+                         (C.spec.kind == "pool" and C.idx is not None))):
+                    C.dx_amax = L.amax[4:5]
+                    L.dz_fused = True
+
+    def _ya(self, L) -> dict:
+        return {"y_amax": L.y_amax} if L.y_amax is not None else {}
+
     def _xa(self, L, x) -> dict:
         """fp16x3: max |x| word of conv L's input, reduced here (one launch)
         and reused by the layer's weight gradient."""
         if L.amax is None or L.spec.cin % 32:      # Cin = 3: the tf32 engines
             return {}
-        self.k.absmax(x, L.amax[0:1])
+        if not L.x_fused:
+            self.k.absmax(x, L.amax[0:1])
         return {"x_amax": L.amax[0:1]}
 
     def _dza(self, L, dz) -> tuple:
@@ -436,14 +479,19 @@ class BurstStep:
             return {}, {}
         if L.spec.cin % 32:                        # Cin = 3: the tf32 engines
             return {}, {"wsplit": L.wsplit}
-        self.k.absmax(dz, L.amax[4:5])
+        if not L.dz_fused:
+            self.k.absmax(dz, L.amax[4:5])
         da = {"wsplit": L.wsplit, "dz_amax": L.amax[4:5]}
+        if L.dx_amax is not None:
+            da["dx_amax"] = L.dx_amax
         wa = {"x_amax": L.amax[0:1], "dz_amax": L.amax[4:5]}
         return wa, da
 
     def _fwd(self, i: int) -> None:
         L = self.layers[i]
         sp = L.spec
+        if i == getattr(self, "first_active", None) and self.amax_words is not None:
+            self.amax_words.zero_()           # fused producers atomicMax into them
         lo = {"wsplit": L.wsplit} if L.wsplit is not None else {}
         if sp.bn:
             # conv without bias / activation into z, then the synchronised BN
@@ -462,7 +510,7 @@ class BurstStep:
         if sp.kind == "conv" and sp.down:
             self._sub_fwd(L)
             self.k.conv3x3_fwd(L.xs, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo,
-                               **self._xa(L, L.xs))
+                               **self._xa(L, L.xs), **self._ya(L))
         elif sp.kind == "conv1x1":
             x = self._sub_fwd(L) if sp.down else L.x
             P = L.b * sp.hw * sp.hw
@@ -474,14 +522,14 @@ class BurstStep:
             self.k.concat_fwd(list(L.cat_in), L.y)
         elif sp.kind == "conv":
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo,
-                               **self._xa(L, L.x))
+                               **self._xa(L, L.x), **self._ya(L))
         elif sp.kind == "add":
             self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu)
         elif sp.kind == "gap":
             self.k.global_avgpool_fwd(L.x, L.y)
         elif sp.kind == "pool":
             if L.idx is not None:
-                self.k.maxpool2x2_fwd_idx(L.x, L.y, L.idx)
+                self.k.maxpool2x2_fwd_idx(L.x, L.y, L.idx, **self._ya(L))
             else:
                 self.k.maxpool2x2_fwd(L.x, L.y)
         else:
@@ -600,7 +648,9 @@ class BurstStep:
                 self.k.conv3x3_dgrad(dy, L.w, mask, L.dx, ws=self.ws, **da)
         elif sp.kind == "pool":
             if L.idx is not None:
-                self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx)
+                self.k.maxpool2x2_bwd_idx(L.idx, L.dy, L.dx,
+                                          **({"dx_amax": L.dx_amax} if L.dx_amax is not None
+                                             else {}))
             else:
                 self.k.maxpool2x2_bwd(L.x, L.dy, L.dx)
         else:
@@ -710,8 +760,8 @@ class BurstStep:
         self._split_w()
 
     def _split_w(self) -> None:
-        for w, sp in self.wsplits:
-            sp.refresh(w)
+        if self.wbatch is not None:
+            self.wbatch.refresh()
 
     def run_ops(self, prog) -> None:
         for key, fn in prog:

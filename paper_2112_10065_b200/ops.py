@@ -34,12 +34,15 @@ _SIGS = {
     "bpx_conv3x3_fwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 6
                         + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_fwd_workspace": (ctypes.c_size_t, [ctypes.c_int] * 5),
-    "bpx_conv3x3_fwd_presplit": (ctypes.c_int, [_c_float_p] * 8 + [ctypes.c_int] * 6
+    "bpx_conv3x3_fwd_presplit": (ctypes.c_int, [_c_float_p] * 9 + [ctypes.c_int] * 6
                                  + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
-    "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 8 + [ctypes.c_int] * 5
+    "bpx_conv3x3_dgrad_presplit": (ctypes.c_int, [_c_float_p] * 9 + [ctypes.c_int] * 5
                                    + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_conv3x3_wgrad_presplit": (ctypes.c_int, [_c_float_p] * 6 + [ctypes.c_int] * 5
                                    + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_f16_split_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong,
+                                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "bpx_f16_split_batch_chunk": (ctypes.c_int, []),
     "bpx_absmax": (ctypes.c_int, [_c_float_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_f16_split": (ctypes.c_int, [_c_float_p, ctypes.c_size_t] + [ctypes.c_void_p] * 4),
     "bpx_conv3x3_dgrad": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 5
@@ -62,9 +65,9 @@ _SIGS = {
     "bpx_maxpool2x2_bwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
                            + [ctypes.c_void_p]),
     "bpx_maxpool2x2_fwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
-                               + [ctypes.c_void_p]),
+                               + [ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_maxpool2x2_bwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
-                               + [ctypes.c_void_p]),
+                               + [ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_residual_add_fwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 7
                              + [ctypes.c_void_p]),
     "bpx_residual_skip_bwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 7
@@ -261,6 +264,48 @@ class F16Split:
         return (self.hi.double() + self.lo.double()) * 2.0 ** (-s)
 
 
+class F16SplitBatch:
+    """fp16x3 splits of several weight tensors refreshed together (three
+    graph nodes per update, bpx_f16_split_batch): ``splits[k]`` is the
+    F16Split view of ``ws[k]``.  The tensors must keep their storage."""
+
+    def __init__(self, ws: list):
+        lib = load_library()
+        dev = ws[0].device
+        offs, tot = [], 0
+        for w in ws:
+            _f32(w)
+            if w.numel() % 4 or not w.is_contiguous():
+                raise KernelError("F16SplitBatch: contiguous tensors of 4k floats")
+            offs.append(tot)
+            tot += (w.numel() + 7) // 8 * 8            # 16-B aligned fp16 slices
+        self.hi = torch.empty(tot, dtype=torch.float16, device=dev)
+        self.lo = torch.empty(tot, dtype=torch.float16, device=dev)
+        self.words = torch.zeros(4 * len(ws), dtype=torch.int32, device=dev)
+        chunk = lib.bpx_f16_split_batch_chunk()
+        rows, blk = [], 0
+        self.splits = []
+        for k, (w, o) in enumerate(zip(ws, offs)):
+            n = w.numel()
+            sp = F16Split.__new__(F16Split)
+            sp.n, sp.hi, sp.lo = n, self.hi[o:o + n], self.lo[o:o + n]
+            sp.amax = self.words[4 * k:4 * k + 4]
+            self.splits.append(sp)
+            rows.append([w.data_ptr(), sp.hi.data_ptr(), sp.lo.data_ptr(), sp.amax.data_ptr(),
+                         n // 4, blk])
+            blk += -(-(n // 4) // chunk)
+        self.blocks = blk
+        self.table = torch.tensor(rows, dtype=torch.int64).to(dev)
+        self.ws = ws
+
+    def refresh(self) -> "F16SplitBatch":
+        lib = load_library()
+        _check(lib.bpx_f16_split_batch(_ptr(self.table), len(self.ws), self.blocks,
+                                       _ptr(self.words), self.words.numel(), _stream()),
+               "bpx_f16_split_batch")
+        return self
+
+
 def f16_scale_exp(amax_bits: int) -> int:
     """Scale exponent s of a tensor whose max |v| has fp32 bits ``amax_bits``:
     max |v| 2^s < 2^15 (tc_ptx.cuh f16_scale_exp)."""
@@ -295,10 +340,11 @@ def _split_ptrs(wsplit):
 
 
 def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None, wsplit=None,
-                x_amax=None):
+                x_amax=None, y_amax=None):
     """``wsplit`` (optional F16Split of w) and ``x_amax`` (optional int32 word
     with max |x|, from ``absmax``) are the fp16x3 operand forms the call
-    otherwise prepares itself."""
+    otherwise prepares itself; ``y_amax`` (optional, zeroed int32 word)
+    receives max |y| for the next conv."""
     lib = load_library()
     _f32(x, w, bias, y)
     n, h, wd, cin = x.shape
@@ -306,14 +352,14 @@ def conv3x3_fwd(x, w, bias, y, relu=True, ws: Optional[Workspace] = None, wsplit
     need = lib.bpx_conv3x3_fwd_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, x.device)
     _check(lib.bpx_conv3x3_fwd_presplit(_ptr(x), _ptr(w), *_split_ptrs(wsplit), _ptr(x_amax),
-                                        _ptr(bias), _ptr(y), n, h, wd, cin, cout, int(relu),
+                                        _ptr(y_amax), _ptr(bias), _ptr(y), n, h, wd, cin, cout, int(relu),
                                         wp, wb, _stream()),
            "bpx_conv3x3_fwd")
     return y
 
 
 def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, wsplit=None,
-                  dz_amax=None):
+                  dz_amax=None, dx_amax=None):
     lib = load_library()
     _f32(dz, w, mask_src, dx)
     n, h, wd, cout = dz.shape
@@ -321,7 +367,8 @@ def conv3x3_dgrad(dz, w, mask_src, dx, ws: Optional[Workspace] = None, wsplit=No
     need = lib.bpx_conv3x3_dgrad_workspace(n, h, wd, cin, cout)
     wp, wb = _ws(ws, need, dz.device)
     _check(lib.bpx_conv3x3_dgrad_presplit(_ptr(dz), _ptr(w), *_split_ptrs(wsplit),
-                                          _ptr(dz_amax), _ptr(mask_src), _ptr(dx), n, h, wd,
+                                          _ptr(dz_amax), _ptr(dx_amax), _ptr(mask_src), _ptr(dx),
+                                          n, h, wd,
                                           cin, cout, wp, wb, _stream()),
            "bpx_conv3x3_dgrad")
     return dx
@@ -547,22 +594,24 @@ def global_avgpool_bwd(dy, mask, dx):
     return dx
 
 
-def maxpool2x2_fwd_idx(x, y, idx):
+def maxpool2x2_fwd_idx(x, y, idx, y_amax=None):
     """Pool forward that also records each window's first-max position
     (``idx``: uint8, same shape as ``y``)."""
     lib = load_library()
     _f32(x, y)
     n, h, w, c = x.shape
-    _check(lib.bpx_maxpool2x2_fwd_idx(_ptr(x), _ptr(y), _ptr(idx), n, h, w, c, _stream()),
+    _check(lib.bpx_maxpool2x2_fwd_idx(_ptr(x), _ptr(y), _ptr(idx), n, h, w, c, _ptr(y_amax),
+                                      _stream()),
            "bpx_maxpool2x2_fwd_idx")
     return y
 
 
-def maxpool2x2_bwd_idx(idx, dy, dx):
+def maxpool2x2_bwd_idx(idx, dy, dx, dx_amax=None):
     lib = load_library()
     _f32(dy, dx)
     n, h, w, c = dx.shape
-    _check(lib.bpx_maxpool2x2_bwd_idx(_ptr(idx), _ptr(dy), _ptr(dx), n, h, w, c, _stream()),
+    _check(lib.bpx_maxpool2x2_bwd_idx(_ptr(idx), _ptr(dy), _ptr(dx), n, h, w, c, _ptr(dx_amax),
+                                      _stream()),
            "bpx_maxpool2x2_bwd_idx")
     return dx
 

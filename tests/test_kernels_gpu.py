@@ -399,3 +399,49 @@ def test_f16_split_roundtrip():
     # below fp16's normal range the split is exact to 2^-25 in scaled units
     s = ops.f16_scale_exp(amax)
     assert err[:16].max().item() <= 2.0 ** (-24 - s), err[:16].max().item()
+
+
+def test_f16_split_batch_matches_single():
+    ws = [rnd(64, 3, 3, 64, seed=30).to(DEV), rnd(8, seed=31).to(DEV) * 1e-9,
+          rnd(128, 3, 3, 64, seed=32).to(DEV) * 7.0]
+    b = ops.F16SplitBatch(ws).refresh()
+    for w, sp in zip(ws, b.splits):
+        one = ops.F16Split(w).refresh(w)
+        torch.cuda.synchronize()
+        assert torch.equal(sp.hi, one.hi) and torch.equal(sp.lo, one.lo)
+        assert int(sp.amax[0]) == int(one.amax[0])
+
+
+def test_producers_reduce_amax():
+    # fused max |v| words: conv fwd (fdt, c1), conv dgrad, maxpool fwd / bwd
+    def word(t):
+        return int(t.abs().max().view(torch.int32).item())
+
+    z = lambda: torch.zeros(4, dtype=torch.int32, device=DEV)      # noqa: E731
+    for (n, h, cin, cout) in [(2, 16, 64, 128), (1, 14, 512, 512), (2, 16, 3, 64)]:
+        x = rnd(n, h, h, cin, seed=33).to(DEV)
+        w = rnd(cout, 3, 3, cin, seed=34, scale=0.05).to(DEV)
+        b = rnd(cout, seed=35).to(DEV)
+        y = torch.empty(n, h, h, cout, device=DEV)
+        ya = z()
+        ops.conv3x3_fwd(x, w, b, y, relu=True, y_amax=ya)
+        torch.cuda.synchronize()
+        assert int(ya[0]) == word(y), (n, h, cin, cout)
+        if cin % 64 == 0:
+            dz = rnd(n, h, h, cout, seed=36).to(DEV)
+            dx = torch.empty_like(x)
+            da = z()
+            ops.conv3x3_dgrad(dz, w, torch.relu(x), dx, dx_amax=da)
+            torch.cuda.synchronize()
+            assert int(da[0]) == word(dx)
+    x = rnd(2, 8, 8, 64, seed=37).to(DEV)
+    y = torch.empty(2, 4, 4, 64, device=DEV)
+    idx = torch.empty(2, 4, 4, 64, dtype=torch.uint8, device=DEV)
+    ya = z()
+    ops.maxpool2x2_fwd_idx(x, y, idx, y_amax=ya)
+    dy = rnd(2, 4, 4, 64, seed=38).to(DEV)
+    dx = torch.empty_like(x)
+    da = z()
+    ops.maxpool2x2_bwd_idx(idx, dy, dx, dx_amax=da)
+    torch.cuda.synchronize()
+    assert int(ya[0]) == word(y) and int(da[0]) == word(dx)
