@@ -46,8 +46,8 @@ __global__ void split_kernel(const float4* __restrict__ w, long long n4,
        i += (long long)gridDim.x * blockDim.x) {
     const float4 v = __ldg(w + i);
     uint2 h, l;
-    split_f16x2(v.x * s, v.y * s, h.x, l.x);
-    split_f16x2(v.z * s, v.w * s, h.y, l.y);
+    split_f16x2_s(v.x, v.y, s, h.x, l.x);
+    split_f16x2_s(v.z, v.w, s, h.y, l.y);
     hi[i] = h;
     lo[i] = l;
   }
@@ -101,8 +101,8 @@ __global__ void split_batch_kernel(const Seg* __restrict__ segs, int nseg) {
     if (i < sg.n4) {
       const float4 v = __ldg(sg.w + i);
       uint2 h, l;
-      split_f16x2(v.x * s, v.y * s, h.x, l.x);
-      split_f16x2(v.z * s, v.w * s, h.y, l.y);
+      split_f16x2_s(v.x, v.y, s, h.x, l.x);
+      split_f16x2_s(v.z, v.w, s, h.y, l.y);
       sg.hi[i] = h;
       sg.lo[i] = l;
     }

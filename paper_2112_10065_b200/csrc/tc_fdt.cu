@@ -81,6 +81,7 @@ struct Geo {
   int half_bytes;            // smem stride of one 32-channel halo (1 KB aligned)
   int halo_bytes;            // one halo slot (NCH halves)
   int halo_tx;               // bytes TMA delivers per halo slot
+  int halo_rows;             // halo pixels (rows) per 32-channel half
   int ksplit, units;         // K parts per tile and work units = tiles * ksplit
   float* part;               // ksplit > 1: partial sums [ksplit][npix][N]
   const uint32_t* amax_a;    // max |A| bits (activations / output gradient)
@@ -322,34 +323,66 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       for (int cc = 0; cc < g.C / KS / g.ksplit; ++cc, ++hc) {
         const int hs = hc & 1;
         mbar_wait(&hfull[hs], (hc >> 1) & 1);
-        const char* hbase = halo + hs * g.halo_bytes + c2 * g.half_bytes;
+        char* hb = halo + hs * g.halo_bytes;
+        // split the halo ONCE for all nine taps, in place: the fp32 rows of
+        // channels [0, 32) and [32, 64) of a halo pixel become its fp16 hi
+        // row (64 channels, where the first half was) and lo row (where the
+        // second was), same 128-B swizzle.  Four threads (one quarter-warp
+        // each, 16 channels) per row pair; a warp reads its 8 row pairs
+        // before it overwrites them.
+        {
+          const int cv = warp - CV0, c16 = lane >> 3;
+          char* src = hb + (c16 >> 1) * g.half_bytes;
+          for (int base = cv * 8; base < g.halo_rows; base += NCONV * 8) {   // warp-uniform
+            const int pr = base + (lane & 7), sw = pr & 7;
+            float4 v[4];
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu)
+              v[uu] = *reinterpret_cast<const float4*>(src + pr * 128 +
+                                                       (((4 * (c16 & 1) + uu) ^ sw) << 4));
+            __syncwarp();
+            uint32_t h[8], l[8];
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) {
+              split_f16x2_s(v[uu].x, v[uu].y, scale, h[2 * uu], l[2 * uu]);
+              split_f16x2_s(v[uu].z, v[uu].w, scale, h[2 * uu + 1], l[2 * uu + 1]);
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int off = pr * 128 + (((2 * c16 + e) ^ sw) << 4);
+              *reinterpret_cast<uint4*>(hb + off) =
+                  make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
+              *reinterpret_cast<uint4*>(hb + g.half_bytes + off) =
+                  make_uint4(l[4 * e], l[4 * e + 1], l[4 * e + 2], l[4 * e + 3]);
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(NCONV * 32) : "memory");
+        }
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
           const int dy = DG ? 1 - tap / 3 : tap / 3 - 1, dx = DG ? 1 - tap % 3 : tap % 3 - 1;
           const int hr = g.tw ? (rr + 1 + dy) * (g.tw + 2) + rc + 1 + dx
                               : r + g.W + 1 + dy * g.W + dx;
           const bool ok = (tmask >> tap) & 1u;
-          const char* row = hbase + hr * 128;
-          const uint32_t a = lanebase + s * Cf::A_STAGE + 16 * c2;
-          // two 16-channel passes (8 TMEM columns of hi and of lo each)
+          // this thread's 32 channels: fp16 chunks 4 c2 .. 4 c2 + 3 of the
+          // hi row and of the lo row
+          uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t hi[8], lo[8];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int j = 4 * h + jj;
-              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (ok) v = *reinterpret_cast<const float4*>(row + ((j ^ (hr & 7)) << 4));
-              split_f16x2(v.x * scale, v.y * scale, hi[2 * jj], lo[2 * jj]);
-              split_f16x2(v.z * scale, v.w * scale, hi[2 * jj + 1], lo[2 * jj + 1]);
+          for (int k = 0; k < 4; ++k) {
+            const int off = hr * 128 + (((4 * c2 + k) ^ (hr & 7)) << 4);
+            uint4 vh = make_uint4(0u, 0u, 0u, 0u), vl = vh;
+            if (ok) {
+              vh = *reinterpret_cast<const uint4*>(hb + off);
+              vl = *reinterpret_cast<const uint4*>(hb + g.half_bytes + off);
             }
-            if (h == 0) {
-              if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
-              tc_fence_after();
-            }
-            tmem_st8u(a + 8 * h, hi);
-            tmem_st8u(a + KS / 2 + 8 * h, lo);
+            hi[4 * k] = vh.x; hi[4 * k + 1] = vh.y; hi[4 * k + 2] = vh.z; hi[4 * k + 3] = vh.w;
+            lo[4 * k] = vl.x; lo[4 * k + 1] = vl.y; lo[4 * k + 2] = vl.z; lo[4 * k + 3] = vl.w;
           }
+          if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
+          tc_fence_after();
+          const uint32_t a = lanebase + s * Cf::A_STAGE + 16 * c2;
+          tmem_st16u(a, hi);
+          tmem_st16u(a + KS / 2, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           if (lane == 0) {
@@ -358,6 +391,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
           __syncwarp();
         }
+        fence_proxy_async();                 // our stores before the next TMA fill
         __syncwarp();
         if (lane == 0) mbar_arrive(&hempty[hs]);
       }
@@ -512,6 +546,7 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
   g.half_bytes = g.nhbox * g.hbox * 128;
   g.halo_bytes = NCH * g.half_bytes;
   g.halo_tx = NCH * (g.tw ? (g.tw + 2) * (g.th + 2) * 128 : g.half_bytes);
+  g.halo_rows = g.tw ? (g.tw + 2) * (g.th + 2) : g.nhbox * g.hbox;
   const int smem = Cf::smem(g.halo_bytes);
   if (smem > 227 * 1024) return BPX_ERR_UNSUPPORTED;
   CUtensorMap ta, tb, tbl;

@@ -274,9 +274,16 @@ __device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint
   float ha, hb;
   asm("{\n\t.reg .f16 x, y;\n\tmov.b32 {x, y}, %2;\n\tcvt.f32.f16 %0, x;\n\tcvt.f32.f16 %1, y;\n\t}"
       : "=f"(ha), "=f"(hb) : "r"(h));
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(b - hb), "f"(a - ha));
+  const float2 r = __fadd2_rn(make_float2(a, b), make_float2(-ha, -hb));   // one FADD2
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r.y), "f"(r.x));
   hi = h;
   lo = l;
+}
+// the same for (a, b) * s (one FMUL2 for the pair)
+__device__ __forceinline__ void split_f16x2_s(float a, float b, float s, uint32_t& hi,
+                                              uint32_t& lo) {
+  const float2 x = __fmul2_rn(make_float2(a, b), make_float2(s, s));
+  split_f16x2(x.x, x.y, hi, lo);
 }
 __host__ __device__ constexpr uint32_t make_idesc_f16(int n) {
   // D f32 (bits 4-5 = 1), A = B = f16 (format 0), K-major A, N >> 3, M >> 4

@@ -222,7 +222,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
                        ? *reinterpret_cast<const float*>(box + kk * 128 + (cofs ^ ((kk & 7) << 4)))
                        : 0.f;
           }
-          split_f16x2(v[0] * scale, v[1] * scale, hi[k], lo[k]);
+          split_f16x2_s(v[0], v[1], scale, hi[k], lo[k]);
         }
         tmem_st8u(a + 8 * ps, hi);
         tmem_st8u(a + BK / 2 + 8 * ps, lo);
@@ -265,8 +265,8 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         uint32_t h[8], l[8];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          split_f16x2(v[u].x * scale, v[u].y * scale, h[2 * u], l[2 * u]);
-          split_f16x2(v[u].z * scale, v[u].w * scale, h[2 * u + 1], l[2 * u + 1]);
+          split_f16x2_s(v[u].x, v[u].y, scale, h[2 * u], l[2 * u]);
+          split_f16x2_s(v[u].z, v[u].w, scale, h[2 * u + 1], l[2 * u + 1]);
           if (do_bias) {
             bs[4 * u] += v[u].x; bs[4 * u + 1] += v[u].y;
             bs[4 * u + 2] += v[u].z; bs[4 * u + 3] += v[u].w;
