@@ -281,9 +281,11 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           const uint32_t off = DG ? ks * 2048 : ks * 32;
           const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
           const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
+#ifndef FDT_NOMMA
           mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
           mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
           mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+#endif
         }
         tc_commit_elect(&empty[s]);
         if (kb % PCH == PCH - 1 || kb == nk - 1) {
@@ -330,6 +332,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         // second was), same 128-B swizzle.  Four threads (one quarter-warp
         // each, 16 channels) per row pair; a warp reads its 8 row pairs
         // before it overwrites them.
+#ifndef FDT_NOCONV
         {
           const int cv = warp - CV0, c16 = lane >> 3;
           char* src = hb + (c16 >> 1) * g.half_bytes;
@@ -358,6 +361,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
           asm volatile("bar.sync 1, %0;" ::"n"(NCONV * 32) : "memory");
         }
+#endif
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
           const int dy = DG ? 1 - tap / 3 : tap / 3 - 1, dx = DG ? 1 - tap % 3 : tap % 3 - 1;
@@ -367,6 +371,11 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           // this thread's 32 channels: fp16 chunks 4 c2 .. 4 c2 + 3 of the
           // hi row and of the lo row
           uint32_t hi[16], lo[16];
+#ifdef FDT_NOCONV
+#pragma unroll
+          for (int k = 0; k < 16; ++k) hi[k] = lo[k] = 0u;
+          if (false)
+#endif
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int off = hr * 128 + (((4 * c2 + k) ^ (hr & 7)) << 4);

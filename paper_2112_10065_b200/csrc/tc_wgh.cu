@@ -163,9 +163,11 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         const uint64_t dbh = make_desc_sw128(bx + ks * 2048, 2 * BOX, 1024);
         const uint64_t dbl = make_desc_sw128(bx + BOX + ks * 2048, 2 * BOX, 1024);
         const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
+#ifndef WGH_NOMMA
         mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
         mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
         mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+#endif
       }
       tc_commit_elect(&empty[s]);
       if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
@@ -209,6 +211,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       tc_fence_after();
       const char* box = smem + s * Cf::STAGE + q * BOX;
       const uint32_t a = lanebase + s * Cf::A_STAGE;
+#ifndef WGH_NOCONV
 #pragma unroll
       for (int ps = 0; ps < BK / 16; ++ps) {         // 16 pixels = 8 columns per pass
         uint32_t hi[8], lo[8];
@@ -227,6 +230,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         tmem_st8u(a + 8 * ps, hi);
         tmem_st8u(a + BK / 2 + 8 * ps, lo);
       }
+#endif
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -253,6 +257,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       char* bt = smem + s * Cf::STAGE + Cf::A_BYTES;
       char* raw = bt + (2 * at + (c16 >> 1)) * BOX;      // this thread's 16 fp32 channels
       char* hrow = bt + 2 * at * BOX, *lrow = hrow + BOX;
+#ifndef WGH_NOCONV
 #pragma unroll
       for (int it = 0; it < PPW / 8; ++it) {
         const int pr = pb + 8 * it + (lane & 7);
@@ -279,6 +284,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           *reinterpret_cast<uint4*>(lrow + off) = make_uint4(l[4 * e], l[4 * e + 1], l[4 * e + 2], l[4 * e + 3]);
         }
       }
+#endif
       fence_proxy_async();                // generic-proxy writes -> the MMA's async reads
       __syncwarp();
       if (lane == 0) mbar_arrive(&ready[s]);
