@@ -54,8 +54,11 @@ constexpr int KS = 64;                               // channels per stage
 constexpr int NCH = 2;                               // 32-channel halo halves per stage
 constexpr int PCH = 128 / KS;                        // stages per promotion chunk (K = 128)
 
-// BN output channels per tile, S stages.
-template <int BN, int S_>
+// BN output channels per tile, S stages; PAIR: a cluster of two CTAs runs
+// M tiles 2m, 2m+1 as one M = 256 MMA (cta_group::2), each CTA holding its
+// own A in TMEM and HALF of the B tile (BN/2 channels) in shared memory, so
+// the weights cross L2 once per 256 output pixels instead of once per 128.
+template <int BN, int S_, bool PAIR = false>
 struct Cfg {
   static_assert(BN == 128 || BN == 64, "tile");
   static constexpr int S = S_;
@@ -63,7 +66,8 @@ struct Cfg {
   static constexpr int NDRAIN = BN / 16;                  // 64 accumulator columns per thread
   static constexpr int DR0 = CV0 + NCONV;
   static constexpr int NTHREADS = 32 * (2 + NCONV + NDRAIN);
-  static constexpr int B_BYTES = BN * KS * 2;             // one fp16 tile (hi or lo)
+  static constexpr int BNL = PAIR ? BN / 2 : BN;          // B channels held by this CTA
+  static constexpr int B_BYTES = BNL * KS * 2;            // one fp16 tile (hi or lo)
   static constexpr int STAGE = 2 * B_BYTES;               // B hi | B lo
   static constexpr int A_COL = 2 * BN;                    // accumulators: 2 x BN columns
   static constexpr int A_STAGE = KS;                      // TMEM columns per stage: hi | lo
@@ -82,7 +86,7 @@ struct Geo {
   int halo_bytes;            // one halo slot (NCH halves)
   int halo_tx;               // bytes TMA delivers per halo slot
   int halo_rows;             // halo pixels (rows) per 32-channel half
-  int ksplit, units;         // K parts per tile and work units = tiles * ksplit
+  int ksplit, units;         // K parts per tile and work units = tiles (pairs) * ksplit
   float* part;               // ksplit > 1: partial sums [ksplit][npix][N]
   const uint32_t* amax_a;    // max |A| bits (activations / output gradient)
   const uint32_t* amax_w;    // max |w| bits of the weights' span
@@ -155,11 +159,25 @@ __device__ __forceinline__ Tile tile_of(const Geo& g, int mi) {
   return t;
 }
 
-template <int BN, int S_, bool DG, class EPI>
-__global__ void __launch_bounds__(Cfg<BN, S_>::NTHREADS, 1)
+// Work unit u of this CTA -> its M tile, N tile and K part; pad: a pair's
+// second tile past the last M tile (it recomputes the last tile, stores nothing)
+template <bool PAIR>
+__device__ __forceinline__ void unit_tile(const Geo& g, int u, uint32_t rank, int& mi, int& nti,
+                                          int& kh, bool& pad) {
+  const int t = u / g.ksplit;
+  kh = u % g.ksplit;
+  nti = t % g.nt;
+  mi = PAIR ? 2 * (t / g.nt) + (int)rank : t / g.nt;
+  pad = mi >= g.mt;
+  if (pad) mi = g.mt - 1;
+}
+
+template <int BN, int S_, bool DG, bool PAIR, class EPI>
+__global__ void __launch_bounds__(Cfg<BN, S_, PAIR>::NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
-  using Cf = Cfg<BN, S_>;
+  using Cf = Cfg<BN, S_, PAIR>;
+  constexpr int BNL = Cf::BNL;
   constexpr int S = Cf::S;
   constexpr int NCONV = Cf::NCONV, NDRAIN = Cf::NDRAIN, DR0 = Cf::DR0;
   extern __shared__ char smem_raw[];
@@ -178,26 +196,35 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cpu = g.C / KS / g.ksplit;        // channel chunks per work unit
   const int nk = 9 * cpu;                     // stages per work unit
+  // pairs: units are walked per cluster; the leader (rank 0) issues the MMAs
+  // and owns aready / accfree, which both CTAs' converters / drains arrive on
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int u0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&bfull[s], 1);
-      mbar_init(&aready[s], NCONV);      // one arrival per converter warp
+      mbar_init(&aready[s], PAIR ? 2 * NCONV : NCONV);   // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
       mbar_init(&hempty[b], NCONV);
       mbar_init(&accfull[b], 1);
-      mbar_init(&accfree[b], NDRAIN);    // one arrival per drain warp
+      mbar_init(&accfree[b], PAIR ? 2 * NDRAIN : NDRAIN);  // one arrival per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
+  if (warp == MMA_WARP) {
+    if (PAIR) tmem_alloc2(tmem_slot, 512); else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t aready_l = PAIR ? mapa_rank(aready, 0) : 0u;
+  const uint32_t accfree_l = PAIR ? mapa_rank(accfree, 0) : 0u;
   const int sa = f16_scale_exp(*g.amax_a), sw = f16_scale_exp(*g.amax_w);
 
   if (warp == TMA_WARP) {
@@ -207,10 +234,12 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       tma_prefetch_desc(&tb);
       tma_prefetch_desc(&tbl);
       int i = 0, hc = 0;
-      for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-        const int t = u / g.ksplit, kh = u % g.ksplit;
-        const Tile T = tile_of(g, t / g.nt);
-        const int n0 = (t % g.nt) * BN;
+      for (int u = u0; u < g.units; u += ustep) {
+        int mi, nti, kh;
+        bool pad;
+        unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
+        const Tile T = tile_of(g, mi);
+        const int n0 = nti * BN + (int)rank * BNL;          // this CTA's B channels
         for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           const int hs = hc & 1;
           if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
@@ -233,14 +262,14 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
             char* st = smem + s * Cf::STAGE;
             mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
-            if (DG) {        // BN/64 boxes of 64 ci x KS co rows (MN-major)
+            if (DG) {        // BNL/64 boxes of 64 ci x KS co rows (MN-major)
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) {
+              for (int j = 0; j < BNL / 64; ++j) {
                 tma_load_3d(st + j * KS * 128, &tb, n0 + 64 * j, tap, cc * KS, &bfull[s]);
                 tma_load_3d(st + Cf::B_BYTES + j * KS * 128, &tbl, n0 + 64 * j, tap, cc * KS,
                             &bfull[s]);
               }
-            } else {         // one box of 64 k x BN rows (K-major)
+            } else {         // one box of 64 k x BNL rows (K-major)
               const int k0 = tap * g.C + cc * KS;
               tma_load_2d(st, &tb, k0, n0, &bfull[s]);
               tma_load_2d(st + Cf::B_BYTES, &tbl, k0, n0, &bfull[s]);
@@ -253,21 +282,24 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     // ------------------------------------------------------------ MMA issuer
     // (the whole warp runs the loop; elect.sync picks the issuing lane)
     // M=128, N=BN, f16 x f16 -> f32, A from TMEM; B K-major (fwd) / MN-major (dgrad)
-    constexpr uint32_t idesc = make_idesc_f16(BN) | (DG ? (1u << 16) : 0u);
+    // (pairs: M = 256 across the two CTAs, leader only)
+    constexpr uint32_t idesc = (PAIR ? ((make_idesc_f16(BN) & ~(0x1Fu << 24)) | (16u << 24))
+                                     : make_idesc_f16(BN)) | (DG ? (1u << 16) : 0u);
     int i = 0, c = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
+    for (int u = u0; u < g.units && (!PAIR || rank == 0); u += ustep) {
       for (int kb = 0; kb < nk; ++kb, ++i) {
         const int s = i % S;
         const uint32_t ph = (i / S) & 1;
         const int b = c & 1;
         if (kb % PCH == 0 && c >= 2) {
-          mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
+          if (PAIR) mbar_wait_cluster(&accfree[b], ((c >> 1) - 1) & 1);
+          else mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
           tc_fence_after();
         }
         // aready[s] also covers the stage's B tiles: the converters wait for
         // them before arriving, so the issuer makes one barrier check per
         // stage (its checks come straight out of MMA issue time)
-        mbar_wait(&aready[s], ph);
+        if (PAIR) mbar_wait_cluster(&aready[s], ph); else mbar_wait(&aready[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + KS / 2;
@@ -282,14 +314,20 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
           const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
 #ifndef FDT_NOMMA
-          mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
-          mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
-          mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          if (PAIR) {
+            mma_ts2_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
+            mma_ts2_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+            mma_ts2_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          } else {
+            mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
+            mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+            mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+          }
 #endif
         }
-        tc_commit_elect(&empty[s]);
+        if (PAIR) tc_commit2_elect(&empty[s]); else tc_commit_elect(&empty[s]);
         if (kb % PCH == PCH - 1 || kb == nk - 1) {
-          tc_commit_elect(&accfull[b]);
+          if (PAIR) tc_commit2_elect(&accfull[b]); else tc_commit_elect(&accfull[b]);
           ++c;
         }
       }
@@ -305,11 +343,13 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int hw = g.H * g.W;
     const int rr = g.tw ? r / g.tw : 0, rc = g.tw ? r % g.tw : 0;
     int i = 0, hc = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const int t = u / g.ksplit;
+    for (int u = u0; u < g.units; u += ustep) {
+      int mi, nti, kh;
+      bool pad;
+      unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
       uint32_t tmask = 0x1ff;                 // bit tap: source pixel inside the image
       if (!g.tw) {
-        const int p = (t / g.nt) * 128 + r;
+        const int p = mi * 128 + r;
         tmask = 0;
         if (p < g.npix) {
           const int img = p / hw, rem = p - img * hw;
@@ -396,7 +436,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           tc_fence_before();
           if (lane == 0) {
             mbar_wait(&bfull[s], (i / S) & 1);     // aready[s] implies the B tiles
-            mbar_arrive(&aready[s]);
+            if (PAIR) mbar_arrive_remote(aready_l + 8u * s); else mbar_arrive(&aready[s]);
           }
           __syncwarp();
         }
@@ -415,8 +455,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const float unscale = exp2i(-sa) * exp2i(-sw);
     uint32_t mx = 0;
     int c = 0;
-    for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
-      const int t = u / g.ksplit, kh = u % g.ksplit;
+    for (int u = u0; u < g.units; u += ustep) {
+      int mi, nti, kh;
+      bool pad;
+      unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
       float acc[CW];
 #pragma unroll
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
@@ -434,14 +476,16 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&accfree[b]);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_remote(accfree_l + 8u * b); else mbar_arrive(&accfree[b]);
+        }
       }
-      const Tile T = tile_of(g, t / g.nt);
+      const Tile T = tile_of(g, mi);
       const long long p = g.tw ? ((long long)T.img * g.H + T.oh0 + r / g.tw) * g.W + T.ow0 +
                                      r % g.tw
                                : (long long)T.m0 + r;
-      const int n0 = (t % g.nt) * BN + hf * CW;
-      if (p < g.npix) {
+      const int n0 = nti * BN + hf * CW;
+      if (p < g.npix && !pad) {
         if (g.ksplit > 1) {               // partial; fdt_finish applies the epilogue
           float* o = g.part + ((long long)kh * g.npix + p) * g.N + n0;
 #pragma unroll
@@ -464,10 +508,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    tmem_free(tmem, 512);
+    if (PAIR) tmem_free2(tmem, 512); else tmem_free(tmem, 512);
   }
 }
 
@@ -499,10 +543,27 @@ __global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long
 // alone would leave the persistent grid under two waves -- conv5 at 14x14
 // (196 tiles on 148 SMs), or any layer at the small per-GPU batches of a
 // wide burst plan; the parts' sums meet in fdt_finish.
-inline int ksplit_for(long long tiles, int chunks) {
+inline int ksplit_for(long long tiles, int chunks, int slots) {
   int k = 1;
-  while (k < 8 && tiles * k < 2LL * num_sms() && chunks % (2 * k) == 0) k *= 2;
+  while (k < 8 && tiles * k < 2LL * slots && chunks % (2 * k) == 0) k *= 2;
   return k;
+}
+
+// CTA pairs (cta_group::2): every shape but the 64-wide dgrad (its 32-channel
+// B halves would need a 64-B swizzle) when there are two M tiles to pair
+#ifndef FDT_PAIR
+#define FDT_PAIR 1
+#endif
+inline bool pair_for(int BN, bool dg, long long mt) {
+  return FDT_PAIR && (!dg || BN == 128) && mt >= 2 && num_sms() >= 2;
+}
+
+// work units of a launch: tiles (M tile pairs) x N tiles x K parts
+inline void plan_units(long long mt, int nt, int chunks, bool pair, int& ksplit, int& units) {
+  const long long mtu = pair ? (mt + 1) / 2 : mt;
+  const int slots = pair ? num_sms() / 2 : num_sms();
+  ksplit = ksplit_for(mtu * nt, chunks, slots);
+  units = (int)(mtu * nt * ksplit);
 }
 
 inline bool encode(CUtensorMap* m, const void* p, CUtensorMapDataType dt, int rank,
@@ -525,10 +586,10 @@ inline void tile2d(int H, int W, int& tw, int& th) {
 // the caller did not split them] [split-K partials].
 inline size_t wsplit_bytes(long long nw) { return (size_t)(4 * nw + 16 + 15) / 16 * 16; }
 
-template <int BN, int S, bool DG, class EPI>
+template <int BN, int S, bool DG, bool PAIR, class EPI>
 bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32_t* amax_a,
                  int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
-  using Cf = Cfg<BN, S>;
+  using Cf = Cfg<BN, S, PAIR>;
   Geo g;
   g.H = H; g.W = W;
   g.C = DG ? Cout : Cin;
@@ -539,8 +600,7 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
   g.mt = g.tw ? n * (H / g.th) * (W / g.tw) : cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;
-  g.ksplit = ksplit_for(g.tiles, g.C / KS);
-  g.units = g.tiles * g.ksplit;
+  plan_units(g.mt, g.nt, g.C / KS, PAIR, g.ksplit, g.units);
   g.part = part;
   g.amax_a = amax_a;
   g.amax_w = wt.amax;
@@ -585,23 +645,40 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
       if (!encode(m, src, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, dims, strides, box,
                   CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
-    } else {        // w16 as [Cout][9*Cin]: box 64 k x BN rows, K-major
+    } else {        // w16 as [Cout][9*Cin]: box 64 k x BNL rows, K-major
       const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
       const cuuint64_t strides[1] = {(cuuint64_t)9 * Cin * 2};
-      const cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)BN};
+      const cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BNL};
       if (!encode(m, src, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, dims, strides, box,
                   CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
-  auto kern = fdt_kernel<BN, S, DG, EPI>;
+  auto kern = fdt_kernel<BN, S, DG, PAIR, EPI>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const int grid = g.units < num_sms() ? g.units : num_sms();
-  kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
+  if (PAIR) {
+    const int clusters = g.units < num_sms() / 2 ? g.units : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(Cf::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, g, epi) != cudaSuccess) return BPX_ERR_LAUNCH;
+  } else {
+    const int grid = g.units < num_sms() ? g.units : num_sms();
+    kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
+  }
   if (g.ksplit == 1) return launch_status(1);
   const long long groups = (long long)g.npix * (g.N / 8);
   int fg = (int)cdivll(groups, 256);
@@ -616,14 +693,25 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
 #ifndef FDT_S64
 #define FDT_S64 5
 #endif
+#ifndef FDT_S128P
+#define FDT_S128P 4
+#endif
 
 template <bool DG, class EPI>
 bpx_status_t dispatch(const float* a, const F16Weights& wt, float* part, const uint32_t* amax_a,
                       int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
   const int N = DG ? Cin : Cout;
-  if (N % 128 == 0)
-    return run<128, FDT_S128, DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
-  return run<64, FDT_S64, DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+  int tw, th;
+  tile2d(H, W, tw, th);
+  const long long mt = tw ? (long long)n * (H / th) * (W / tw) : cdivll((long long)n * H * W, 128);
+  if (N % 128 == 0) {
+    if (pair_for(128, DG, mt))
+      return run<128, FDT_S128P, DG, true>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+    return run<128, FDT_S128, DG, false>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+  }
+  if (pair_for(64, DG, mt))
+    return run<64, FDT_S64, DG, !DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+  return run<64, FDT_S64, DG, false>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
 }
 
 // The call's operands in fp16x3 form: A's amax (from the caller or reduced
@@ -673,8 +761,13 @@ size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
   size_t part = 0;
   for (int dg = 0; dg < 2; ++dg) {        // fwd (N = cout) and dgrad (N = cin)
     const int N = dg ? cin : cout, C = dg ? cout : cin;
-    const long long tiles = cdivll(npix, 128) * (N / (N % 128 == 0 ? 128 : 64));
-    const int k = C % fdt::KS == 0 ? fdt::ksplit_for(tiles, C / fdt::KS) : 1;
+    const int BN = N % 128 == 0 ? 128 : 64;
+    int tw, th;
+    fdt::tile2d(h, w, tw, th);
+    const long long mt = tw ? (long long)n * (h / th) * (w / tw) : cdivll(npix, 128);
+    int k = 1, units;
+    if (C % fdt::KS == 0)
+      fdt::plan_units(mt, N / BN, C / fdt::KS, fdt::pair_for(BN, dg, mt), k, units);
     if (k > 1) {
       const size_t need = (size_t)k * npix * N;
       part = part > need ? part : need;
