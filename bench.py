@@ -152,11 +152,19 @@ def _time_gemm_ops(st, reps=5):
         f = sp.fwd_flops() * L.b
         mask = L.x if sp.in_relu else None
         if sp.kind == "conv":
-            fns = {"fwd": lambda L=L, sp=sp: k.conv3x3_fwd(L.x, L.w, L.bias, L.y,
-                                                          relu=sp.relu, ws=ws),
-                   "wgrad": lambda L=L: k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=ws)}
+            # the step's own operand forms: the weights' fp16x3 split and the
+            # max |x| / |dz| words the last step left (same tensors)
+            fp16 = getattr(L, "amax", None) is not None and sp.cin % 32 == 0
+            kf = {"wsplit": L.wsplit, "x_amax": L.amax[0:1]} if fp16 else {}
+            kd = {"wsplit": L.wsplit, "dz_amax": L.amax[4:5]} if fp16 else {}
+            kw = {"x_amax": L.amax[0:1], "dz_amax": L.amax[4:5]} if fp16 else {}
+            fns = {"fwd": lambda L=L, sp=sp, kf=kf: k.conv3x3_fwd(L.x, L.w, L.bias, L.y,
+                                                                 relu=sp.relu, ws=ws, **kf),
+                   "wgrad": lambda L=L, kw=kw: k.conv3x3_wgrad(L.x, L.dy, L.dw, L.dbias, ws=ws,
+                                                               **kw)}
             if i > 0:
-                fns["dgrad"] = lambda L=L, m=mask: k.conv3x3_dgrad(L.dy, L.w, m, L.dx, ws=ws)
+                fns["dgrad"] = lambda L=L, m=mask, kd=kd: k.conv3x3_dgrad(L.dy, L.w, m, L.dx,
+                                                                         ws=ws, **kd)
         else:
             x2 = L.x.view(L.b, sp.cin)
             fns = {"fwd": lambda L=L, sp=sp, x2=x2: k.linear_fwd(x2, L.w, L.bias, L.y,
@@ -176,7 +184,8 @@ def _time_gemm_ops(st, reps=5):
             e1.record()
             torch.cuda.synchronize()
             rows.append({"layer": sp.name, "op": op, "b": L.b, "flops": f,
-                         "ms": e0.elapsed_time(e1) / reps})
+                         "ms": e0.elapsed_time(e1) / reps,
+                         "engine": k.last_engine() if hasattr(k, "last_engine") else "?"})
     return rows
 
 
@@ -194,18 +203,30 @@ def _ncu_traffic(dom):
     return rec["traffic"], rec
 
 
-def _roofline(dom, tf32_peak, peak_src, step_ms, flops_step, gemm_ms):
+# engines on the fp16 tensor-core path (fp16x3: three kind::f16 MMAs per
+# fp32-accurate product) vs the 3xTF32 ones (three kind::tf32 MMAs)
+F16X3_ENGINES = {"fdt", "wgh"}
+
+
+def _roofline(dom, peaks, peak_src, step_ms, flops_step, gemm_ms):
     if dom is None:
         return None
     traffic, rec = _ncu_traffic(dom)
     achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+    f16 = dom.get("engine") in F16X3_ENGINES
+    # fp16 and bf16 dense MMAs run at the same rate; tf32 at half of it
+    peak = peaks["bf16_tflops"] if f16 else peaks["bf16_tflops"] / 2.0
+    kind = "fp16x3" if f16 else "3xTF32"
     return {
         "bound": "tensor", "unit": "TFLOP/s",
-        "kernel": f"{dom['layer']} {dom['op']} (b={dom['b']}; 3xTF32 tcgen05 engine)",
-        "achieved": achieved, "peak": tf32_peak, "frac": achieved / tf32_peak,
-        "frac_of_3xtf32": achieved / (tf32_peak / 3.0),
-        "peak_source": f"{peak_src}: TF32 dense = MEASURED_PEAKS bf16_tflops/2; "
-                       "fp32-accurate 3xTF32 issues 3 MMAs per product",
+        "kernel": f"{dom['layer']} {dom['op']} (b={dom['b']}; {dom.get('engine')} engine, "
+                  f"{kind} tcgen05 MMAs)",
+        "achieved": achieved, "peak": peak, "frac": achieved / peak,
+        "frac_of_3_mma_ceiling": achieved / (peak / 3.0),
+        "peak_source": (f"{peak_src}: " + ("fp16 dense = MEASURED_PEAKS bf16_tflops" if f16 else
+                                          "TF32 dense = MEASURED_PEAKS bf16_tflops/2") +
+                        f"; the fp32-accurate {kind} product issues 3 MMAs, so 1/3 of the peak "
+                        "is its ceiling"),
         "flops_per_launch": dom["flops"], "ms_per_launch": dom["ms"],
         "share_of_step": dom["ms"] / step_ms,
         "step_gemm": {"flops": flops_step, "ms_sum_of_launches": gemm_ms,
@@ -322,7 +343,8 @@ def bench_reference(args):
         "impl": "reference", "metric": METRIC, "value": thr, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (fp32-accurate: fp16x3 / 3xTF32 tensor-core products, fp32 accumulation)",
         "data": "synthetic (x~N(0,1) NHWC, uniform labels, torchvision-style init)",
         "config": {"workload": "VGG-16 global batch 32 fwd+bwd step, CPU path",
                    "global_batch": GLOBAL_BATCH, "sample_batch_per_step": sample},
@@ -421,7 +443,6 @@ def bench_ours(args):
     gemm_ms = sum(r["ms"] for r in op_rows)
     dom = max(op_rows, key=lambda r: r["ms"]) if op_rows else None
     peaks, peak_src = _peaks()
-    tf32_peak = peaks["bf16_tflops"] / 2.0
 
     # end to end through the public API with pinned host inputs
     cfg = SimConfig(warmup_iterations=args.warmup)
@@ -471,7 +492,8 @@ def bench_ours(args):
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (fp32-accurate: fp16x3 / 3xTF32 tensor-core products, fp32 accumulation)",
             "data": "synthetic (x~N(0,1) NHWC 3x224x224, uniform labels, "
                     "torchvision-style random init)",
             "config": {"workload": "VGG-16 global batch 32, burst-parallel plan "
@@ -490,7 +512,7 @@ def bench_ours(args):
             "legacy_engine_calls_per_step": legacy_per_step,
             "parity_checked": bool(parity.get("ok")),
             "parity": parity,
-            "roofline": _roofline(dom, tf32_peak, peak_src, ms / args.steps,
+            "roofline": _roofline(dom, peaks, peak_src, ms / args.steps,
                                   flops_step, gemm_ms),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -44,12 +44,18 @@ constexpr int BK = 64;                          // pixels per stage
 constexpr int BOX = 32 * BK * 4;                // 32 channels x 64 pixels, fp32
 constexpr int PCH = 128 / BK;                   // stages per promotion chunk (K = 128)
 
-template <int BN>
+// PAIR (BN = 128): a cluster of two CTAs (M tiles 2m, 2m+1, same N tile and
+// pixel split) runs one M = 256 MMA (cta_group::2); each CTA loads and splits
+// HALF of the dz tile (64 channels, one fp16 atom), so dz crosses L2 once
+// per 256 rows of dW^T instead of once per 128.
+template <int BN, bool PAIR = false>
 struct Cfg {
   static_assert(BN == 64 || BN == 128, "BN");
-  static constexpr int S = BN == 128 ? 3 : 4;
+  static_assert(!PAIR || BN == 128, "pairs split a 128-channel dz tile");
+  static constexpr int BNL = PAIR ? BN / 2 : BN;          // dz channels held by this CTA
+  static constexpr int S = BNL == 128 ? 3 : 4;
   static constexpr int A_BYTES = 4 * BOX;                 // 128 rows of A
-  static constexpr int B_BYTES = (BN / 32) * BOX;
+  static constexpr int B_BYTES = (BNL / 32) * BOX;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int ACC = 2 * BN;                      // two chunk buffers
   static constexpr int A_COL = ACC;                       // + S stages of (hi | lo)
@@ -73,12 +79,12 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(NT, 1)
 wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
-  using Cf = Cfg<BN>;
-  constexpr int S = Cf::S;
+  using Cf = Cfg<BN, PAIR>;
+  constexpr int S = Cf::S, BNL = Cf::BNL;
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -97,24 +103,32 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
   const int t0 = blockIdx.z * g.tps;
   const int nst = max(0, min(g.tiles, t0 + g.tps) - t0);
+  // pairs: the leader (rank 0) issues the MMAs and owns ready / hfree, which
+  // both CTAs' converters / drains arrive on; its commits reach both CTAs
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int nl0 = n0 + (int)rank * BNL;         // first dz channel held here
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 8);                // one arrival per converter warp
+      mbar_init(&ready[s], PAIR ? 16 : 8);    // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&hfull[b], 1);
-      mbar_init(&hfree[b], 8);                // one arrival per drain warp
+      mbar_init(&hfree[b], PAIR ? 16 : 8);    // one arrival per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
+  if (warp == MMA_WARP) {
+    if (PAIR) tmem_alloc2(tmem_slot, 512); else tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t ready_l = PAIR ? mapa_rank(ready, 0) : 0u;
+  const uint32_t hfree_l = PAIR ? mapa_rank(hfree, 0) : 0u;
   const int sx = f16_scale_exp(*g.amax_x), sd = f16_scale_exp(*g.amax_dz);
 
   if (warp == TMA_WARP) {
@@ -137,23 +151,25 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           tma_load_2d(st + c * BOX, &tx, ci0, p0 + (tap / 3 - 1) * g.W + tap % 3 - 1, &full[s]);
         }
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j)
-          tma_load_2d(st + Cf::A_BYTES + j * BOX, &tdz, n0 + 32 * j, p0, &full[s]);
+        for (int j = 0; j < BNL / 32; ++j)
+          tma_load_2d(st + Cf::A_BYTES + j * BOX, &tdz, nl0 + 32 * j, p0, &full[s]);
       }
     }
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     // M=128, N=BN, f16 x f16 -> f32, A from TMEM, B MN-major (bit 16): atom a
     // (64 channels) of b_hi sits where box 2a landed, b_lo where box 2a+1 did
-    constexpr uint32_t idesc = make_idesc_f16(BN) | (1u << 16);
-    for (int i = 0; i < nst; ++i) {
+    constexpr uint32_t idesc = (PAIR ? ((make_idesc_f16(BN) & ~(0x1Fu << 24)) | (16u << 24))
+                                     : make_idesc_f16(BN)) | (1u << 16);
+    for (int i = 0; i < nst && (!PAIR || rank == 0); ++i) {
       const int s = i % S;
       const int c = i / PCH, b = c & 1;
       if (i % PCH == 0 && c >= 2) {
-        mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
+        if (PAIR) mbar_wait_cluster(&hfree[b], ((c >> 1) - 1) & 1);
+        else mbar_wait(&hfree[b], ((c >> 1) - 1) & 1);
         tc_fence_after();
       }
-      mbar_wait(&ready[s], (i / S) & 1);
+      if (PAIR) mbar_wait_cluster(&ready[s], (i / S) & 1); else mbar_wait(&ready[s], (i / S) & 1);
       tc_fence_after();
       const uint32_t d = tmem + b * BN;
       const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + BK / 2;
@@ -164,13 +180,24 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         const uint64_t dbl = make_desc_sw128(bx + BOX + ks * 2048, 2 * BOX, 1024);
         const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
 #ifndef WGH_NOMMA
-        mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
-        mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
-        mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+        if (PAIR) {
+          mma_ts2_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts2_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts2_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+        } else {
+          mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
+          mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
+          mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+        }
 #endif
       }
-      tc_commit_elect(&empty[s]);
-      if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+      if (PAIR) {
+        tc_commit2_elect(&empty[s]);
+        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit2_elect(&hfull[b]);
+      } else {
+        tc_commit_elect(&empty[s]);
+        if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+      }
     }
   } else if (warp < CB0) {
     // ------------------------------------------------------------ A converters
@@ -234,7 +261,9 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ready[s]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(ready_l + 8u * s); else mbar_arrive(&ready[s]);
+      }
     }
   } else if (warp < DR0) {
     // ------------------------------------------------------------ B converters
@@ -243,11 +272,11 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     // (pixel, 64-channel atom) row pair; BN = 128: warp wb takes atom wb & 1,
     // pixels [32 (wb >> 1), +32); BN = 64: atom 0, pixels [16 wb, +16)
     const int wb = warp - CB0, c16 = lane >> 3;
-    const int at = BN == 128 ? (wb & 1) : 0;
-    constexpr int PPW = BN == 128 ? 32 : 16;                 // pixels per warp per stage
-    const int pb = (BN == 128 ? (wb >> 1) : wb) * PPW;
+    const int at = BNL == 128 ? (wb & 1) : 0;
+    constexpr int PPW = BNL == 128 ? 32 : 16;                // pixels per warp per stage
+    const int pb = (BNL == 128 ? (wb >> 1) : wb) * PPW;
     const float scale = exp2i(sd);
-    const bool do_bias = bias_part != nullptr && blockIdx.x == 0;
+    const bool do_bias = bias_part != nullptr && blockIdx.x == (PAIR ? rank : 0u);
     float bs[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) bs[k] = 0.f;
@@ -287,7 +316,9 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
 #endif
       fence_proxy_async();                // generic-proxy writes -> the MMA's async reads
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ready[s]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(ready_l + 8u * s); else mbar_arrive(&ready[s]);
+      }
     }
     if (do_bias) {
       // fixed-order reduction of the 16 per-thread partials of each channel
@@ -295,14 +326,14 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
 #pragma unroll
       for (int k = 0; k < 16; ++k) bias_scr[bt * 16 + k] = bs[k];
       named_sync(1, 128);
-      if (bt < BN) {
+      if (bt < BNL) {
         const int a = bt / 64, cc = (bt % 64) / 16, k = bt % 16;
         float t = 0.f;
         for (int w = 0; w < 4; ++w) {
-          if (BN == 128 && (w & 1) != a) continue;
+          if (BNL == 128 && (w & 1) != a) continue;
           for (int l8 = 0; l8 < 8; ++l8) t += bias_scr[(w * 32 + cc * 8 + l8) * 16 + k];
         }
-        bias_part[(long long)blockIdx.z * g.Cout + n0 + bt] = t;
+        bias_part[(long long)blockIdx.z * g.Cout + nl0 + bt] = t;
       }
     }
   } else {
@@ -329,7 +360,9 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&hfree[b]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(hfree_l + 8u * b); else mbar_arrive(&hfree[b]);
+      }
     }
     const int r = m0 + q * 32 + lane;
     if (r < nrows) {
@@ -340,16 +373,29 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    tmem_free(tmem, 512);
+    if (PAIR) tmem_free2(tmem, 512); else tmem_free(tmem, 512);
   }
 }
 
 // ------------------------------------------------------------------ host side
 
 inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
+#ifndef WGH_PAIR
+#define WGH_PAIR 1
+#endif
+#ifndef WGH_PAIR_PAD
+#define WGH_PAIR_PAD 0
+#endif
+// pairs for 128-wide N tiles whose M tiles pair up (Cin = 256, 512); with
+// WGH_PAIR_PAD=1 an odd count gets a padding tile (A rows zero, nothing
+// stored) -- measured equal (Cin = 128) or 5 % slower (Cin = 64), so off
+inline bool paired(int cin, int cout) {
+  const int mt = cdiv(9 * cin, 128);
+  return WGH_PAIR && bn_for(cout) == 128 && mt >= 2 && (WGH_PAIR_PAD || mt % 2 == 0);
+}
 
 inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
   g.Cin = cin; g.Cout = cout; g.H = H; g.W = W;
@@ -357,6 +403,7 @@ inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& n
   g.tiles = (int)cdivll(g.npix, BK);
   g.slab = (long long)cout * 9 * cin;
   mt = cdiv(9 * cin, 128);
+  if (paired(cin, cout)) mt += mt & 1;           // whole pairs (a padding tile computes zeros)
   nt = cout / bn_for(cout);
   const int tiles_mn = mt * nt;
   int want = num_sms() / tiles_mn;
@@ -378,17 +425,34 @@ inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C) {
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g, int mt,
                     int nt, int splits, float* part, float* bias_part, cudaStream_t st) {
-  using Cf = Cfg<BN>;
-  auto kern = wgh_kernel<BN>;
+  using Cf = Cfg<BN, PAIR>;
+  auto kern = wgh_kernel<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     attr = true;
   }
-  kern<<<dim3(mt, nt, splits), NT, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+  if (!PAIR) {
+    kern<<<dim3(mt, nt, splits), NT, Cf::SMEM, st>>>(tx, tdz, g, part, bias_part);
+    return launch_status();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(mt, nt, splits);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, tx, tdz, g, part, bias_part) != cudaSuccess)
+    return BPX_ERR_LAUNCH;
   return launch_status();
 }
 
@@ -439,8 +503,10 @@ bpx_status_t wgh_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
   float* part = splits == 1 ? dw : scratch;
   float* bpart = !dbias ? nullptr : (splits == 1 ? dbias : scratch + (size_t)splits * slab);
   bpx_status_t s = wgh::bn_for(cout) == 128
-                       ? wgh::launch<128>(tx, tdz, g, mt, nt, splits, part, bpart, st)
-                       : wgh::launch<64>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+      ? (wgh::paired(cin, cout) ? wgh::launch<128, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+                                : wgh::launch<128, false>(tx, tdz, g, mt, nt, splits, part, bpart,
+                                                          st))
+      : wgh::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
   if (s != BPX_OK || splits == 1) return s;
   s = split_reduce(part, splits, slab, dw, st);
   if (s != BPX_OK || !dbias) return s;
