@@ -92,6 +92,20 @@ struct Geo {
   const uint32_t* amax_w;    // max |w| bits of the weights' span
 };
 
+// FDT_PROF builds (tools/fdt_prof.py): per-role cycle counters of warp 0 of
+// each role, summed over CTAs into a device buffer (bpx_fdt_prof).
+#ifdef FDT_PROF
+__device__ unsigned long long g_prof[16];
+#define PROF_DECL long long _pt = 0
+#define PROF_START() (_pt = clock64())
+#define PROF_ADD(slot, first) do { if ((first) && (threadIdx.x & 31) == 0) \
+    atomicAdd(&g_prof[slot], (unsigned long long)(clock64() - _pt)); } while (0)
+#else
+#define PROF_DECL
+#define PROF_START()
+#define PROF_ADD(slot, first)
+#endif
+
 // Epilogues return the max |v| bits of what they stored: the drain reduces
 // them into *amax (the output's fp16x3 scale word for its consumers).
 __device__ __forceinline__ uint32_t absbits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
@@ -233,6 +247,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       tma_prefetch_desc(&ta);
       tma_prefetch_desc(&tb);
       tma_prefetch_desc(&tbl);
+      PROF_DECL;
       int i = 0, hc = 0;
       for (int u = u0; u < g.units; u += ustep) {
         int mi, nti, kh;
@@ -242,7 +257,9 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         const int n0 = nti * BN + (int)rank * BNL;          // this CTA's B channels
         for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           const int hs = hc & 1;
+          PROF_START();
           if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
+          PROF_ADD(11, true);
           mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_tx);
           char* hb = halo + hs * g.halo_bytes;
 #pragma unroll
@@ -259,7 +276,9 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
           for (int tap = 0; tap < 9; ++tap, ++i) {
             const int s = i % S;
+            PROF_START();
             if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+            PROF_ADD(12, true);
             char* st = smem + s * Cf::STAGE;
             mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
             if (DG) {        // BNL/64 boxes of 64 ci x KS co rows (MN-major)
@@ -286,20 +305,28 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     constexpr uint32_t idesc = (PAIR ? ((make_idesc_f16(BN) & ~(0x1Fu << 24)) | (16u << 24))
                                      : make_idesc_f16(BN)) | (DG ? (1u << 16) : 0u);
     int i = 0, c = 0;
+    PROF_DECL;
+#ifdef FDT_PROF
+    const long long _t0 = clock64();
+#endif
     for (int u = u0; u < g.units && (!PAIR || rank == 0); u += ustep) {
       for (int kb = 0; kb < nk; ++kb, ++i) {
         const int s = i % S;
         const uint32_t ph = (i / S) & 1;
         const int b = c & 1;
         if (kb % PCH == 0 && c >= 2) {
+          PROF_START();
           if (PAIR) mbar_wait_cluster(&accfree[b], ((c >> 1) - 1) & 1);
           else mbar_wait(&accfree[b], ((c >> 1) - 1) & 1);
+          PROF_ADD(1, true);
           tc_fence_after();
         }
+        PROF_START();
         // aready[s] also covers the stage's B tiles: the converters wait for
         // them before arriving, so the issuer makes one barrier check per
         // stage (its checks come straight out of MMA issue time)
         if (PAIR) mbar_wait_cluster(&aready[s], ph); else mbar_wait(&aready[s], ph);
+        PROF_ADD(2, true);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + KS / 2;
@@ -332,6 +359,12 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         }
       }
     }
+#ifdef FDT_PROF
+    if (lane == 0 && (!PAIR || rank == 0)) {
+      atomicAdd(&g_prof[0], (unsigned long long)(clock64() - _t0));
+      atomicAdd(&g_prof[4], (unsigned long long)i);
+    }
+#endif
   } else if (warp < DR0) {
     // ------------------------------------------------------------ A converters
     // thread = TMEM lane = output pixel r of the tile; warp half c2 converts
@@ -343,6 +376,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int hw = g.H * g.W;
     const int rr = g.tw ? r / g.tw : 0, rc = g.tw ? r % g.tw : 0;
     int i = 0, hc = 0;
+    PROF_DECL;
+    const bool pw = warp == CV0;
     for (int u = u0; u < g.units; u += ustep) {
       int mi, nti, kh;
       bool pad;
@@ -364,7 +399,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       }
       for (int cc = 0; cc < g.C / KS / g.ksplit; ++cc, ++hc) {
         const int hs = hc & 1;
+        PROF_START();
         mbar_wait(&hfull[hs], (hc >> 1) & 1);
+        PROF_ADD(6, pw);
+        PROF_START();
         char* hb = halo + hs * g.halo_bytes;
         // split the halo ONCE for all nine taps, in place: the fp32 rows of
         // channels [0, 32) and [32, 64) of a halo pixel become its fp16 hi
@@ -402,6 +440,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           asm volatile("bar.sync 1, %0;" ::"n"(NCONV * 32) : "memory");
         }
 #endif
+        PROF_ADD(7, pw);
         for (int tap = 0; tap < 9; ++tap, ++i) {
           const int s = i % S;
           const int dy = DG ? 1 - tap / 3 : tap / 3 - 1, dx = DG ? 1 - tap % 3 : tap % 3 - 1;
@@ -427,17 +466,21 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             hi[4 * k] = vh.x; hi[4 * k + 1] = vh.y; hi[4 * k + 2] = vh.z; hi[4 * k + 3] = vh.w;
             lo[4 * k] = vl.x; lo[4 * k + 1] = vl.y; lo[4 * k + 2] = vl.z; lo[4 * k + 3] = vl.w;
           }
+          PROF_START();
           if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
+          PROF_ADD(8, pw);
           tc_fence_after();
           const uint32_t a = lanebase + s * Cf::A_STAGE + 16 * c2;
           tmem_st16u(a, hi);
           tmem_st16u(a + KS / 2, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
+          PROF_START();
           if (lane == 0) {
             mbar_wait(&bfull[s], (i / S) & 1);     // aready[s] implies the B tiles
             if (PAIR) mbar_arrive_remote(aready_l + 8u * s); else mbar_arrive(&aready[s]);
           }
+          PROF_ADD(9, pw);
           __syncwarp();
         }
         fence_proxy_async();                 // our stores before the next TMA fill
@@ -455,6 +498,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const float unscale = exp2i(-sa) * exp2i(-sw);
     uint32_t mx = 0;
     int c = 0;
+    PROF_DECL;
+    const bool pw = warp == DR0;
     for (int u = u0; u < g.units; u += ustep) {
       int mi, nti, kh;
       bool pad;
@@ -464,7 +509,9 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
       for (int k = 0; k < nch; ++k, ++c) {
         const int b = c & 1;
+        PROF_START();
         mbar_wait(&accfull[b], (c >> 1) & 1);
+        PROF_ADD(14, pw);
         tc_fence_after();
 #pragma unroll
         for (int j = 0; j < CW; j += 8) {
@@ -480,6 +527,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           if (PAIR) mbar_arrive_remote(accfree_l + 8u * b); else mbar_arrive(&accfree[b]);
         }
       }
+      PROF_START();
       const Tile T = tile_of(g, mi);
       const long long p = g.tw ? ((long long)T.img * g.H + T.oh0 + r / g.tw) * g.W + T.ow0 +
                                      r % g.tw
@@ -503,6 +551,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           }
         }
       }
+      PROF_ADD(15, pw);
     }
     if (g.ksplit == 1) amax_commit(epi.amax, mx);
   }
@@ -818,3 +867,14 @@ bpx_status_t fdt_conv_dgrad(const float* dz, const float* w, const F16Weights* w
 }
 
 }  // namespace bpx
+
+#ifdef FDT_PROF
+// Profiling builds only (BPX_NVCC_EXTRA=-DFDT_PROF): role cycle counters of
+// the fwd/dgrad engine summed over CTAs since the last call (reset here).
+extern "C" __attribute__((visibility("default"))) void bpx_fdt_prof(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, bpx::fdt::g_prof, sizeof(unsigned long long) * 16);
+  static const unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(bpx::fdt::g_prof, z, sizeof(z));
+}
+#endif
