@@ -277,7 +277,7 @@ def test_signal_barrier_single_rank():
 # dense FFMA kernels chosen for them by measurement) -- never by a legacy
 # engine (simt / ts / tc / wg / small).
 ALLOWED = {
-    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgh", "wgt"}},
+    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgh", "wgc", "wgt"}},
     "dense": {"fwd": {"dtc", "dns"}, "dgrad": {"dtc", "dns"}, "wgrad": {"dwt", "dns"}},
 }
 
@@ -445,3 +445,25 @@ def test_producers_reduce_amax():
     ops.maxpool2x2_bwd_idx(idx, dy, dx, dx_amax=da)
     torch.cuda.synchronize()
     assert int(ya[0]) == word(y) and int(da[0]) == word(dx)
+
+
+@pytest.mark.parametrize("shape", [(2, 80, 64, 64), (1, 224, 64, 64)], ids=str)
+def test_conv_wgrad_resident_tiles(shape):
+    # the Cin = Cout = 64 engine (all five M tiles resident, x halo per 16x4
+    # block, promotion into per-CTA slabs): fp64 parity and run-to-run equality
+    n, h, cin, cout = shape
+    x = relu_input(n, h, h, cin, seed=40)
+    dz = rnd(n, h, h, cout, seed=41)
+    _, dw_ref, db_ref = vgg_ref.conv_grads(x, torch.zeros(cout, 3, 3, cin), dz)
+    _, dw32, db32 = vgg_ref.conv_grads(x, torch.zeros(cout, 3, 3, cin), dz, torch.float32)
+    outs = []
+    for _ in range(2):
+        dw = torch.empty(cout, 3, 3, cin, device=DEV)
+        db = torch.empty(cout, device=DEV)
+        ops.conv3x3_wgrad(x.to(DEV), dz.to(DEV), dw, db)
+        assert ops.last_engine() == "wgc"
+        outs.append((dw, db))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    close(outs[0][0], dw_ref, dw32)
+    close(outs[0][1], db_ref, db32)
