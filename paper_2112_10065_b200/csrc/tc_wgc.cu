@@ -23,8 +23,9 @@
 // accumulators need no second TMEM buffer.  The slabs of the CTAs (each a
 // contiguous range of blocks) meet in the fixed-order split_reduce.
 //
-// CTA: 18 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters
-// (lane quadrant = chunk of the M tile), 6-9 B converters, 10-17 drain.
+// CTA: 22 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-9 A converters
+// (lane quadrant = chunk of the M tile; two per quadrant, two pixel rows
+// each), 10-13 B converters, 14-21 drain.
 #include "tma_host.h"
 #include "tc_ptx.cuh"
 #include "tc_api.h"
@@ -33,7 +34,8 @@ namespace bpx {
 namespace wgc {
 using namespace tcx;
 
-constexpr int TMA_WARP = 0, MMA_WARP = 1, CA0 = 2, CB0 = 6, DR0 = 10, NT = 18 * 32;
+constexpr int TMA_WARP = 0, MMA_WARP = 1, CA0 = 2, NCA = 8, CB0 = CA0 + NCA, DR0 = CB0 + 4;
+constexpr int NT = (DR0 + 8) * 32;
 constexpr int C = 64;                         // Cin = Cout
 constexpr int MT = 5;                         // M tiles: 9 * 64 = 576 rows (4.5 x 128)
 constexpr int NROWS = 9 * C;
@@ -49,7 +51,7 @@ constexpr int SMEM = 1024 + S * STAGE + 512 + 128 * 16 * 4;
 static_assert(ACC + SA * A_STAGE <= 512, "TMEM budget");
 static_assert(SMEM <= 227 * 1024, "smem budget");
 #ifndef WGC_PB
-#define WGC_PB 4                              // blocks per promotion chunk (K = 256)
+#define WGC_PB 8                              // blocks per promotion chunk (K = 512)
 #endif
 constexpr int PB = WGC_PB;
 
@@ -90,10 +92,10 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&bready[s], 4);
-      mbar_init(&sempty[s], 1 + 4);        // MMA commit + the four A converter warps
+      mbar_init(&sempty[s], 1 + NCA);      // MMA commit + the A converter warps
     }
     for (int a = 0; a < SA; ++a) {
-      mbar_init(&aready[a], 4);
+      mbar_init(&aready[a], NCA);
       mbar_init(&aempty[a], 1);
     }
     for (int k = 0; k < MT; ++k) {
@@ -149,9 +151,11 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const uint64_t dbh = make_desc_sw128(bx + ks * 2048, 2 * DZB, 1024);
           const uint64_t dbl = make_desc_sw128(bx + DZB + ks * 2048, 2 * DZB, 1024);
           const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
+#ifndef WGC_NOMMA
           mma_ts_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
           mma_ts_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
           mma_ts_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
+#endif
         }
         tc_commit_elect(&aempty[sa]);
         if (last) tc_commit_elect(&accfull[k]);
@@ -163,7 +167,7 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     // thread = TMEM lane = row r of M tile k = channel `lane` of chunk
     // gc = 4k + q = (tap, 32-channel half); its 64 pixels are the block's
     // 16 x 4 pixels shifted by the tap, read out of the halo
-    const int q = warp & 3;
+    const int q = warp & 3, ph = (warp - CA0) >> 2;   // quadrant, pixel-row half
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + A_COL;
     const float scale = exp2i(sx);
     const int cofs = ((lane >> 2) << 4) + (lane & 3) * 4;     // logical chunk, word
@@ -177,12 +181,17 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
         const int gc = 4 * k + q;
         if (ai >= SA) mbar_wait(&aempty[sa], ((ai / SA) - 1) & 1);
         tc_fence_after();
+#ifdef WGC_NOCONV
+        if (false) {
+#else
         if (gc < 2 * 9) {                        // rows past 576 stay garbage, never stored
+#endif
           const int tap = gc >> 1, dy = tap / 3, dx = tap % 3;   // halo offsets (+1 folded in)
           const char* hb = st + (gc & 1) * XH;
           const uint32_t a = lanebase + sa * A_STAGE;
 #pragma unroll
-          for (int py = 0; py < BH; ++py) {        // one 16-pixel block row = 8 columns
+          for (int pp = 0; pp < BH / 2; ++pp) {    // one 16-pixel block row = 8 columns
+            const int py = 2 * ph + pp;
             uint32_t hi[8], lo[8];
 #pragma unroll
             for (int k2 = 0; k2 < 8; ++k2) {
@@ -224,6 +233,9 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       char* raw = bt + (c16 >> 1) * DZB;
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
+#ifdef WGC_NOCONV
+        break;
+#endif
         const int pr = 16 * wb + 8 * it + (lane & 7), sw = pr & 7;
         float4 v[4];
 #pragma unroll
@@ -293,14 +305,12 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
 #pragma unroll
             for (int j = 0; j < 32; ++j) o[(long long)j * NROWS] = v[j];
           } else {
+            // fire-and-forget adds in L2; one thread per address, issued in
+            // chunk order (same-address order is kept), RN: deterministic
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              float t[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) t[u] = o[(long long)(j + u) * NROWS];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) o[(long long)(j + u) * NROWS] = t[u] + v[j + u];
-            }
+            for (int j = 0; j < 32; ++j)
+              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(o + (long long)j * NROWS),
+                           "f"(v[j]) : "memory");
           }
         }
       }
