@@ -151,6 +151,8 @@ size_t bpx_conv3x3_wgrad_workspace(int n, int h, int w_, int cin, int cout) {
   d = d > g ? d : g;
   g = wgc_conv_ws(n, h, w_, cin, cout);
   d = d > g ? d : g;
+  g = wg1_conv_ws(n, h, w_, cin, cout);
+  d = d > g ? d : g;
   size_t e = small_conv_wgrad_ws(n, h, w_, cin, cout);
   size_t f = thin_conv_wgrad_ws(n, h, w_, cin, cout);
   e = e > f ? e : f;
@@ -174,6 +176,10 @@ bpx_status_t bpx_conv3x3_wgrad_presplit(const float* x, const float* dz, const u
   BPX_CHECK_ARG(x && dz && dw && n >= 0 && h > 0 && w_ > 0 && cin > 0 && cout > 0);
   BPX_CHECK_ARG(ws || ws_bytes == 0);
   cudaStream_t st = as_stream(stream);
+  if (wg1_conv_ok(n, h, w_, cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
+      (!dbias || aligned16(dbias)) && aligned16(ws))
+    return use("wg1"), wg1_conv_wgrad(x, dz, x_amax, dz_amax, dw, dbias, n, h, w_, ws, ws_bytes,
+                                      st);
   if (wgc_conv_ok(n, h, w_, cin, cout) && aligned16(x) && aligned16(dz) && aligned16(dw) &&
       (!dbias || aligned16(dbias)) && aligned16(ws))
     return use("wgc"), wgc_conv_wgrad(x, dz, x_amax, dz_amax, dw, dbias, n, h, w_, ws, ws_bytes,

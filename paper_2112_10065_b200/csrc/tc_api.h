@@ -92,6 +92,15 @@ bpx_status_t wgh_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
                             cudaStream_t st);
 }  // namespace bpx
 
+// Weight gradient of the Cin = 3 -> 64 first conv (tc_wg1.cu).
+namespace bpx {
+bool wg1_conv_ok(int n, int h, int w, int cin, int cout);
+size_t wg1_conv_ws(int n, int h, int w, int cin, int cout);
+bpx_status_t wg1_conv_wgrad(const float* x, const float* dz, const uint32_t* amax_x,
+                            const uint32_t* amax_dz, float* dw, float* dbias, int n, int h,
+                            int w_, void* ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace bpx
+
 // Weight gradient for Cin = Cout = 64 with all M tiles resident (tc_wgc.cu).
 namespace bpx {
 bool wgc_conv_ok(int n, int h, int w, int cin, int cout);

@@ -277,7 +277,7 @@ def test_signal_barrier_single_rank():
 # dense FFMA kernels chosen for them by measurement) -- never by a legacy
 # engine (simt / ts / tc / wg / small).
 ALLOWED = {
-    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgh", "wgc", "wgt"}},
+    "conv": {"fwd": {"fdt", "c1"}, "dgrad": {"fdt"}, "wgrad": {"wgh", "wgc", "wg1"}},
     "dense": {"fwd": {"dtc", "dns"}, "dgrad": {"dtc", "dns"}, "wgrad": {"dwt", "dns"}},
 }
 
@@ -467,3 +467,20 @@ def test_conv_wgrad_resident_tiles(shape):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     close(outs[0][0], dw_ref, dw32)
     close(outs[0][1], db_ref, db32)
+
+
+@pytest.mark.parametrize("shape", [(2, 224, 3, 64), (3, 32, 3, 64)], ids=str)
+def test_conv_wgrad_first_layer(shape):
+    # Cin = 3: im2col rows in every TMEM lane quadrant, x halo by TMA
+    n, h, cin, cout = shape
+    x = rnd(n, h, h, cin, seed=42)
+    dz = rnd(n, h, h, cout, seed=43)
+    _, dw_ref, db_ref = vgg_ref.conv_grads(x, torch.zeros(cout, 3, 3, cin), dz)
+    _, dw32, db32 = vgg_ref.conv_grads(x, torch.zeros(cout, 3, 3, cin), dz, torch.float32)
+    dw = torch.empty(cout, 3, 3, cin, device=DEV)
+    db = torch.empty(cout, device=DEV)
+    ops.conv3x3_wgrad(x.to(DEV), dz.to(DEV), dw, db)
+    assert ops.last_engine() == "wg1"
+    torch.cuda.synchronize()
+    close(dw, dw_ref, dw32)
+    close(db, db_ref, db32)
