@@ -154,7 +154,7 @@ def _time_gemm_ops(st, reps=5):
         if sp.kind == "conv":
             # the step's own operand forms: the weights' fp16x3 split and the
             # max |x| / |dz| words the last step left (same tensors)
-            fp16 = getattr(L, "amax", None) is not None and sp.cin % 32 == 0
+            fp16 = getattr(L, "amax", None) is not None
             kf = {"wsplit": L.wsplit, "x_amax": L.amax[0:1]} if fp16 else {}
             kd = {"wsplit": L.wsplit, "dz_amax": L.amax[4:5]} if fp16 else {}
             kw = {"x_amax": L.amax[0:1], "dz_amax": L.amax[4:5]} if fp16 else {}

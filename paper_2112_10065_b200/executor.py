@@ -314,7 +314,11 @@ class BurstStep:
             self.wbatch = self.k.F16SplitBatch([L.w for L in convs]) if convs else None
             for j, L in enumerate(convs):
                 L.wsplit = self.wbatch.splits[j]
-                L.amax = words[8 * j:8 * j + 8]
+                # the fp16x3 engines' shapes (fdt / wgh / wgc / wg1): Cout % 64
+                # and Cin % 32 or the 3-channel first conv; the 32-wide towers
+                # of the four-tower net run the FFMA / TS engines without words
+                if L.spec.cout % 64 == 0 and (L.spec.cin % 32 == 0 or L.spec.cin == 3):
+                    L.amax = words[8 * j:8 * j + 8]
             self._split_w()
             self.amax_words = words
             self._fuse_amax(consumers)
@@ -441,7 +445,7 @@ class BurstStep:
             return
         for i, L in enumerate(self.layers):
             sp = L.spec
-            if L.amax is None or sp.cin % 32 or sp.bn or sp.down:
+            if L.amax is None or sp.bn or sp.down:
                 continue
             if L.src_i >= 0 and not L.reshard_in and self.layers[L.src_i].g == L.g:
                 S = self.layers[L.src_i]
@@ -455,7 +459,7 @@ class BurstStep:
                 # (an inactive consumer's flags are never set: compare g)
                 if (C.active and C.g == L.g and not C.reshard_in and not C.dx_acc and
                         not C.spec.bn and
-                        ((C.spec.kind == "conv" and not C.spec.down and C.spec.cin % 32 == 0) or
+                        ((C.spec.kind == "conv" and not C.spec.down) or
                          (C.spec.kind == "pool" and C.idx is not None))):
                     C.dx_amax = L.amax[4:5]
                     L.dz_fused = True
@@ -466,7 +470,7 @@ class BurstStep:
     def _xa(self, L, x) -> dict:
         """fp16x3: max |x| word of conv L's input, reduced here (one launch)
         and reused by the layer's weight gradient."""
-        if L.amax is None or L.spec.cin % 32:      # Cin = 3: the tf32 engines
+        if L.amax is None:
             return {}
         if not L.x_fused:
             self.k.absmax(x, L.amax[0:1])
@@ -475,10 +479,8 @@ class BurstStep:
     def _dza(self, L, dz) -> tuple:
         """fp16x3 keyword arguments of conv L's wgrad and dgrad: the stored
         max |x| word and max |dz| reduced here."""
-        if L.amax is None:
-            return {}, {}
-        if L.spec.cin % 32:                        # Cin = 3: the tf32 engines
-            return {}, {"wsplit": L.wsplit}
+        if L.amax is None:      # no words of its own; it may still feed one
+            return {}, ({"dx_amax": L.dx_amax} if L.dx_amax is not None else {})
         if not L.dz_fused:
             self.k.absmax(dz, L.amax[4:5])
         da = {"wsplit": L.wsplit, "dz_amax": L.amax[4:5]}

@@ -44,7 +44,7 @@ def main():
         flops = l.fwd_flops() * b
         if l.kind == "conv":
             sp = xa = dya = None
-            if not a.inline_prep and hasattr(ops, "F16Split") and l.cin % 32 == 0:
+            if not a.inline_prep and hasattr(ops, "F16Split"):
                 sp = ops.F16Split(w).refresh(w)
                 xa = ops.absmax(x, torch.zeros(4, dtype=torch.int32, device=dev))
                 dya = ops.absmax(dy, torch.zeros(4, dtype=torch.int32, device=dev))
