@@ -186,10 +186,15 @@ __device__ __forceinline__ void unit_tile(const Geo& g, int u, uint32_t rank, in
   if (pad) mi = g.mt - 1;
 }
 
-template <int BN, int S_, bool DG, bool PAIR, class EPI>
+// MT (dgrad with the mask, no split-K, where the tile fits): the ReLU mask
+// tile of the unit (the layer input, 128 pixels x BN channels) comes by
+// TMA into shared memory, issued mid-unit, so the epilogue reads it there
+// instead of issuing 16 dependent global loads per thread.
+template <int BN, int S_, bool DG, bool PAIR, class EPI, bool MT = false>
 __global__ void __launch_bounds__(Cfg<BN, S_, PAIR>::NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           const __grid_constant__ CUtensorMap tbl, Geo g, EPI epi) {
+           const __grid_constant__ CUtensorMap tbl, const __grid_constant__ CUtensorMap tm,
+           Geo g, EPI epi) {
   using Cf = Cfg<BN, S_, PAIR>;
   constexpr int BNL = Cf::BNL;
   constexpr int S = Cf::S;
@@ -205,7 +210,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   uint64_t* hempty = hfull + 2;      // halo slot consumed by all nine taps
   uint64_t* accfull = hempty + 2;
   uint64_t* accfree = accfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfree + 2);
+  uint64_t* mfull = accfree + 2;     // MT: mask tile landed
+  uint64_t* mfree = mfull + 1;       // MT: mask tile read by the drain
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mfree + 1);
+  char* mtile = halo + 2 * g.halo_bytes + 1024;               // MT: BN / 32 x 16 KB, 1 KB aligned
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cpu = g.C / KS / g.ksplit;        // channel chunks per work unit
@@ -228,6 +236,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       mbar_init(&accfull[b], 1);
       mbar_init(&accfree[b], PAIR ? 2 * NDRAIN : NDRAIN);  // one arrival per drain warp
     }
+    mbar_init(mfull, 1);
+    mbar_init(mfree, NDRAIN);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -247,8 +257,9 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       tma_prefetch_desc(&ta);
       tma_prefetch_desc(&tb);
       tma_prefetch_desc(&tbl);
+      if (MT) tma_prefetch_desc(&tm);
       PROF_DECL;
-      int i = 0, hc = 0;
+      int i = 0, hc = 0, mu = 0;
       for (int u = u0; u < g.units; u += ustep) {
         int mi, nti, kh;
         bool pad;
@@ -292,6 +303,19 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
               const int k0 = tap * g.C + cc * KS;
               tma_load_2d(st, &tb, k0, n0, &bfull[s]);
               tma_load_2d(st + Cf::B_BYTES, &tbl, k0, n0, &bfull[s]);
+            }
+            if (MT && tap == 4 && cc == (kh + 1) * cpu - 1) {    // the unit's mask tile
+              if (mu >= 1) mbar_wait(mfree, (mu - 1) & 1);
+              mbar_expect_tx(mfull, (uint32_t)(BN * 128 * 4));
+#pragma unroll
+              for (int h = 0; h < BN / 32; ++h) {     // all BN channels of this CTA's rows
+                if (g.tw)
+                  tma_load_4d(mtile + h * 16384, &tm, nti * BN + 32 * h, T.ow0, T.oh0, T.img,
+                              mfull);
+                else
+                  tma_load_2d(mtile + h * 16384, &tm, nti * BN + 32 * h, T.m0, mfull);
+              }
+              ++mu;
             }
           }
         }
@@ -497,7 +521,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int r = q * 32 + lane;
     const float unscale = exp2i(-sa) * exp2i(-sw);
     uint32_t mx = 0;
-    int c = 0;
+    int c = 0, mu_d = 0;
     PROF_DECL;
     const bool pw = warp == DR0;
     for (int u = u0; u < g.units; u += ustep) {
@@ -533,7 +557,28 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                                      r % g.tw
                                : (long long)T.m0 + r;
       const int n0 = nti * BN + hf * CW;
-      if (p < g.npix && !pad) {
+      if (MT) {
+        // the mask from the staged tile: row r, 128-B swizzled rows per 32 channels
+        mbar_wait(mfull, mu_d & 1);
+        if (p < g.npix) {
+          float* o = epi.out + p * g.N + n0;
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 mk = *reinterpret_cast<const float4*>(
+                mtile + ((hf * CW + j) >> 5) * 16384 + r * 128 +
+                ((((j & 31) >> 2) ^ (r & 7)) << 4));
+            float4 v = make_float4(acc[j] * unscale, acc[j + 1] * unscale, acc[j + 2] * unscale,
+                                   acc[j + 3] * unscale);
+            v.x = mk.x > 0.f ? v.x : 0.f; v.y = mk.y > 0.f ? v.y : 0.f;
+            v.z = mk.z > 0.f ? v.z : 0.f; v.w = mk.w > 0.f ? v.w : 0.f;
+            *reinterpret_cast<float4*>(o + j) = v;
+            mx = max(mx, max(max(absbits(v.x), absbits(v.y)), max(absbits(v.z), absbits(v.w))));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mfree);
+        ++mu_d;
+      } else if (p < g.npix && !pad) {
         if (g.ksplit > 1) {               // partial; fdt_finish applies the epilogue
           float* o = g.part + ((long long)kh * g.npix + p) * g.N + n0;
 #pragma unroll
@@ -635,6 +680,45 @@ inline void tile2d(int H, int W, int& tw, int& th) {
 // the caller did not split them] [split-K partials].
 inline size_t wsplit_bytes(long long nw) { return (size_t)(4 * nw + 16 + 15) / 16 * 16; }
 
+inline const float* mask_of(const EBiasAct&) { return nullptr; }
+inline const float* mask_of(const EMask& e) { return e.mask; }
+#ifndef FDT_MT
+#define FDT_MT 1
+#endif
+
+template <int BN, int S, bool DG, bool PAIR, class EPI, bool MT>
+bpx_status_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl,
+                    const CUtensorMap& tm, const Geo& g, int smem, EPI epi, cudaStream_t st) {
+  using Cf = Cfg<BN, S, PAIR>;
+  auto kern = fdt_kernel<BN, S, DG, PAIR, EPI, MT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  if (PAIR) {
+    const int clusters = g.units < num_sms() / 2 ? g.units : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(Cf::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, tm, g, epi) != cudaSuccess)
+      return BPX_ERR_LAUNCH;
+  } else {
+    const int grid = g.units < num_sms() ? g.units : num_sms();
+    kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, tm, g, epi);
+  }
+  return BPX_OK;
+}
+
 template <int BN, int S, bool DG, bool PAIR, class EPI>
 bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32_t* amax_a,
                  int n, int H, int W, int Cin, int Cout, EPI epi, cudaStream_t st) {
@@ -703,31 +787,33 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
-  auto kern = fdt_kernel<BN, S, DG, PAIR, EPI>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  // MT: the dgrad mask staged by TMA where it fits
+  const float* mptr = mask_of(epi);
+  const int smem_mt = smem + 512 + BN * 128 * 4;
+  const bool mt = FDT_MT && DG && mptr && g.ksplit == 1 && smem_mt <= 227 * 1024;
+  CUtensorMap tm = ta;
+  if (mt) {
+    if (g.tw) {
+      const cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+      const cuuint64_t strides[3] = {(cuuint64_t)g.N * 4, (cuuint64_t)W * g.N * 4,
+                                     (cuuint64_t)H * W * g.N * 4};
+      const cuuint32_t box[4] = {32, (cuuint32_t)g.tw, (cuuint32_t)g.th, 1};
+      if (!encode(&tm, mptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
+        return BPX_ERR_INVALID_ARGUMENT;
+    } else {
+      const cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)g.npix};
+      const cuuint64_t strides[1] = {(cuuint64_t)g.N * 4};
+      const cuuint32_t box[2] = {32, 128};
+      if (!encode(&tm, mptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B))
+        return BPX_ERR_INVALID_ARGUMENT;
+    }
   }
-  if (PAIR) {
-    const int clusters = g.units < num_sms() / 2 ? g.units : num_sms() / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(Cf::NTHREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, g, epi) != cudaSuccess) return BPX_ERR_LAUNCH;
-  } else {
-    const int grid = g.units < num_sms() ? g.units : num_sms();
-    kern<<<grid, Cf::NTHREADS, smem, st>>>(ta, tb, tbl, g, epi);
-  }
+  const bpx_status_t ls =
+      mt ? launch<BN, S, DG, PAIR, EPI, true>(ta, tb, tbl, tm, g, smem_mt, epi, st)
+         : launch<BN, S, DG, PAIR, EPI, false>(ta, tb, tbl, tm, g, smem, epi, st);
+  if (ls != BPX_OK) return ls;
   if (g.ksplit == 1) return launch_status(1);
   const long long groups = (long long)g.npix * (g.N / 8);
   int fg = (int)cdivll(groups, 256);
