@@ -252,25 +252,21 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const int sa = f16_scale_exp(*g.amax_a), sw = f16_scale_exp(*g.amax_w);
 
   if (warp == TMA_WARP) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // ------------------------------------------------------------ TMA producers
+    // lane 1 streams the halos (each waits only for its slot), lane 0 the B
+    // tiles and mask tiles: one thread doing both issued a halo only after
+    // the previous chunk's nine B tiles, each waiting for an MMA slot
+    if (lane == 1) {
       tma_prefetch_desc(&ta);
-      tma_prefetch_desc(&tb);
-      tma_prefetch_desc(&tbl);
-      if (MT) tma_prefetch_desc(&tm);
-      PROF_DECL;
-      int i = 0, hc = 0, mu = 0;
+      int hc = 0;
       for (int u = u0; u < g.units; u += ustep) {
         int mi, nti, kh;
         bool pad;
         unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
         const Tile T = tile_of(g, mi);
-        const int n0 = nti * BN + (int)rank * BNL;          // this CTA's B channels
         for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           const int hs = hc & 1;
-          PROF_START();
           if (hc >= 2) mbar_wait(&hempty[hs], ((hc >> 1) - 1) & 1);
-          PROF_ADD(11, true);
           mbar_expect_tx(&hfull[hs], (uint32_t)g.halo_tx);
           char* hb = halo + hs * g.halo_bytes;
 #pragma unroll
@@ -285,6 +281,22 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                             T.m0 - g.W - 1 + j * g.hbox, &hfull[hs]);
             }
           }
+        }
+      }
+    } else if (lane == 0) {
+      tma_prefetch_desc(&ta);
+      tma_prefetch_desc(&tb);
+      tma_prefetch_desc(&tbl);
+      if (MT) tma_prefetch_desc(&tm);
+      PROF_DECL;
+      int i = 0, hc = 0, mu = 0;
+      for (int u = u0; u < g.units; u += ustep) {
+        int mi, nti, kh;
+        bool pad;
+        unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
+        const Tile T = tile_of(g, mi);
+        const int n0 = nti * BN + (int)rank * BNL;          // this CTA's B channels
+        for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           for (int tap = 0; tap < 9; ++tap, ++i) {
             const int s = i % S;
             PROF_START();
