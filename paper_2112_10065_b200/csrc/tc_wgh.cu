@@ -138,7 +138,14 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       tma_prefetch_desc(&tdz);
       int na = 0;
       for (int c = 0; c < 4; ++c) na += (m0 / 32 + c) < chunks;
+#ifdef WGH_NOX
+      na = 0;
+#endif
+#ifdef WGH_NODZ
+      const uint32_t bytes = (uint32_t)(na * BOX);
+#else
       const uint32_t bytes = (uint32_t)(na * BOX + Cf::B_BYTES);
+#endif
       for (int i = 0; i < nst; ++i) {
         const int s = i % S;
         if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
@@ -150,9 +157,11 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const int tap = gc / cpt, ci0 = (gc - tap * cpt) * 32;
           tma_load_2d(st + c * BOX, &tx, ci0, p0 + (tap / 3 - 1) * g.W + tap % 3 - 1, &full[s]);
         }
+#ifndef WGH_NODZ
 #pragma unroll
         for (int j = 0; j < BNL / 32; ++j)
           tma_load_2d(st + Cf::A_BYTES + j * BOX, &tdz, nl0 + 32 * j, p0, &full[s]);
+#endif
       }
     }
   } else if (warp == MMA_WARP) {
@@ -238,7 +247,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       tc_fence_after();
       const char* box = smem + s * Cf::STAGE + q * BOX;
       const uint32_t a = lanebase + s * Cf::A_STAGE;
-#ifndef WGH_NOCONV
+#if !defined(WGH_NOCONV) && !defined(WGH_NOACONV)
 #pragma unroll
       for (int ps = 0; ps < BK / 16; ++ps) {         // 16 pixels = 8 columns per pass
         uint32_t hi[8], lo[8];
