@@ -80,7 +80,8 @@ struct Geo {
   int H, W, C;               // C = gathered channels (Cin fwd, Cout dgrad)
   int N;                     // output channels
   int npix, mt, nt, tiles;
-  int tw, th;                // 2-D tile (tw * th = 128) or 0 = flattened tiles
+  int tw, th;                // 2-D tile (tw * th <= 128) or 0 = flattened tiles
+  int trows;                 // output pixels per tile: tw * th, or 128
   int hbox, nhbox;           // rows per halo TMA box, boxes per 32-channel halo
   int half_bytes;            // smem stride of one 32-channel halo (1 KB aligned)
   int halo_bytes;            // one halo slot (NCH halves)
@@ -318,7 +319,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             }
             if (MT && tap == 4 && cc == (kh + 1) * cpu - 1) {    // the unit's mask tile
               if (mu >= 1) mbar_wait(mfree, (mu - 1) & 1);
-              mbar_expect_tx(mfull, (uint32_t)(BN * 128 * 4));
+              mbar_expect_tx(mfull, (uint32_t)(BN * g.trows * 4));
 #pragma unroll
               for (int h = 0; h < BN / 32; ++h) {     // all BN channels of this CTA's rows
                 if (g.tw)
@@ -418,7 +419,9 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       int mi, nti, kh;
       bool pad;
       unit_tile<PAIR>(g, u, rank, mi, nti, kh, pad);
-      uint32_t tmask = 0x1ff;                 // bit tap: source pixel inside the image
+      // bit tap: source pixel inside the image (2-D tiles: TMA zero-fills
+      // the border; rows past tw * th read nothing)
+      uint32_t tmask = r < g.trows ? 0x1ffu : 0u;
       if (!g.tw) {
         const int p = mi * 128 + r;
         tmask = 0;
@@ -565,9 +568,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       }
       PROF_START();
       const Tile T = tile_of(g, mi);
-      const long long p = g.tw ? ((long long)T.img * g.H + T.oh0 + r / g.tw) * g.W + T.ow0 +
-                                     r % g.tw
-                               : (long long)T.m0 + r;
+      const long long p = r >= g.trows ? (long long)g.npix
+                          : g.tw ? ((long long)T.img * g.H + T.oh0 + r / g.tw) * g.W + T.ow0 +
+                                       r % g.tw
+                                 : (long long)T.m0 + r;
       const int n0 = nti * BN + hf * CW;
       if (MT) {
         // the mask from the staged tile: row r, 128-B swizzled rows per 32 channels
@@ -681,11 +685,26 @@ inline bool encode(CUtensorMap* m, const void* p, CUtensorMapDataType dt, int ra
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 2-D output tile tw x th = 128 that divides the image, widest first.
+// 2-D output tile tw x th that divides the image: tw * th = 128, widest
+// first; else, for images 64 pixels wide or more (whose flattened halo,
+// 128 + 2W + 2 rows, needs two TMA boxes and crowds the B stages out of
+// smem), the tile with the most pixels <= 128 (at least 120, rows past
+// tw * th idle), e.g. 25 x 5 at 100 x 100 (189 halo rows instead of 330).
 inline void tile2d(int H, int W, int& tw, int& th) {
   tw = th = 0;
   for (int w = 32; w >= 16; w >>= 1)
     if (W % w == 0 && H % (128 / w) == 0) { tw = w; th = 128 / w; return; }
+  if (128 + 2 * W + 2 <= 256) return;
+  int best = 0;
+  for (int w = 8; w <= 64; ++w) {
+    if (W % w) continue;
+    for (int h = 128 / w; h >= 2; --h)
+      if (H % h == 0) {
+        if (w * h > best) { best = w * h; tw = w; th = h; }
+        break;
+      }
+  }
+  if (best < 120) tw = th = 0;
 }
 
 // Workspace: [amax word of A (16 B)] [weights: hi | lo fp16 + amax word when
@@ -742,6 +761,7 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
   if (g.C % KS || g.N % BN) return BPX_ERR_UNSUPPORTED;
   g.npix = n * H * W;
   tile2d(H, W, g.tw, g.th);
+  g.trows = g.tw ? g.tw * g.th : 128;
   g.mt = g.tw ? n * (H / g.th) * (W / g.tw) : cdiv(g.npix, 128);
   g.nt = g.N / BN;
   g.tiles = g.mt * g.nt;

@@ -43,6 +43,8 @@ CONV_SHAPES = [
     (1, 224, 64, 64), (1, 112, 64, 128),
     # the four-tower net's 32 -> 32 tower convs (35 / 17 / 8 px; thin FFMA wgrad)
     (4, 35, 32, 32), (3, 17, 32, 32), (5, 8, 32, 32),
+    # the residual net's 100 x 100 stage: 25 x 5 tiles (125 of 128 rows)
+    (1, 100, 128, 128), (2, 100, 64, 128),
 ]
 
 
@@ -57,6 +59,8 @@ def test_conv_fwd(shape):
     ref32 = vgg_ref.layer_fwd(spec, x, w, b, dtype=torch.float32)
     y = torch.empty(n, h, h, cout, device=DEV)
     ops.conv3x3_fwd(x.to(DEV), w.to(DEV), b.to(DEV), y, relu=True)
+    if cin % 64 == 0 and cout % 64 == 0:
+        assert ops.last_engine() == "fdt"
     torch.cuda.synchronize()
     close(y, ref, ref32)
 
@@ -72,6 +76,8 @@ def test_conv_dgrad_masked(shape):
     dx32 = vgg_ref.conv_grads(x, w, dz, torch.float32)[0] * (x > 0)
     dx = torch.empty(n, h, h, cin, device=DEV)
     ops.conv3x3_dgrad(dz.to(DEV), w.to(DEV), x.to(DEV), dx)
+    if cin % 64 == 0 and cout % 64 == 0:
+        assert ops.last_engine() == "fdt"
     torch.cuda.synchronize()
     close(dx, dx_ref, dx32)
 
