@@ -84,14 +84,17 @@ BPX_API size_t bpx_conv3x3_fwd_workspace(int n, int h, int w_, int cin, int cout
  * "fp16x3"): w_hi / w_lo / w_amax = the weights split by bpx_f16_split
  * (fp16 [cout][3][3][cin] each, and the split span's max |w| bits), made
  * once per update instead of once per call; x_amax = max |x| as bits
- * (bpx_absmax, or written by the producer of x).  Each may be NULL (the
- * call then prepares it in its workspace).  y_amax (nullable): atomicMax'ed
+ * (bpx_absmax, or written by the producer of x; the 3-channel first conv
+ * (Cin = 3, Cout = 64) reduces x into it itself as it reads x -- atomicMax,
+ * a no-op on a word that already holds it -- so a zeroed word will do).
+ * Each may be NULL (the call then prepares it in its workspace).  y_amax
+ * (nullable): atomicMax'ed
  * with the max |y| bits -- the next conv's x_amax, fused into this
  * producer (zero it first).  bpx_conv3x3_dgrad_presplit likewise, with
  * dz_amax for dz and dx_amax for dx.                                       */
 BPX_API bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w,
                                       const void* w_hi, const void* w_lo,
-                                      const unsigned* w_amax, const unsigned* x_amax,
+                                      const unsigned* w_amax, unsigned* x_amax,
                                       unsigned* y_amax, const float* bias, float* y,
                                       int n, int h, int w_, int cin, int cout, int relu,
                                       void* ws, size_t ws_bytes, void* stream);

@@ -59,7 +59,7 @@ static bool split_args(const void* hi, const void* lo, const unsigned* amax, F16
 
 bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const void* w_hi,
                                       const void* w_lo, const unsigned* w_amax,
-                                      const unsigned* x_amax, unsigned* y_amax,
+                                      unsigned* x_amax, unsigned* y_amax,
                                       const float* bias, float* y, int n, int h, int w_,
                                       int cin, int cout, int relu, void* ws, size_t ws_bytes,
                                       void* stream) {
@@ -70,8 +70,13 @@ bpx_status_t bpx_conv3x3_fwd_presplit(const float* x, const float* w, const void
   cudaStream_t st = as_stream(stream);
   if (c1_conv_fwd_ok(cin, cout)) {
     use("c1");
-    bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, y_amax, st);
+    bpx_status_t s = c1_conv_fwd(x, w, bias, y, n, h, w_, relu, x_amax, y_amax, st);
     if (s != BPX_ERR_UNSUPPORTED) return s;
+    // the other engines leave x_amax alone: keep the first conv's promise
+    if (x_amax && aligned16(x)) {
+      absmax_into(x, (size_t)n * h * w_ * cin, x_amax, st);
+      count_launches(1);
+    }
   }
   const size_t ny = (size_t)n * h * w_ * cout;
   if (small_conv_fwd_ok(cin, cout))

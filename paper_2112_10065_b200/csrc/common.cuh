@@ -58,5 +58,9 @@ size_t colsum_workspace_floats(long long rows, int cols);
 // Fixed-order split reduction: out[i] = sum_s parts[s*n + i].
 bpx_status_t split_reduce(const float* parts, int splits, size_t n, float* out,
                           cudaStream_t st);
+// The same for a weight gradient and its bias gradient in ONE launch:
+// dw[i] = sum_s pw[s*nw + i], db[j] = sum_s pb[s*nb + j] (db may be null).
+bpx_status_t split_reduce_wb(const float* pw, size_t nw, float* dw, const float* pb, size_t nb,
+                             float* db, int splits, cudaStream_t st);
 
 }  // namespace bpx

@@ -44,7 +44,8 @@ constexpr int SMEM = 1024 + 2 * COUT * KP * 4 + 2 * STAGE_OUT + 128;
 __global__ void __launch_bounds__(NTHREADS, CPS)
 c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
               const float* __restrict__ bias, const __grid_constant__ CUtensorMap ty, int H,
-              int W, long long npix, int relu, uint32_t* __restrict__ amax) {
+              int W, long long npix, int relu, uint32_t* __restrict__ x_amax,
+              uint32_t* __restrict__ amax) {
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -107,6 +108,7 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
     const int q = warp & 3, r = q * 32 + lane;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16);
     const int hw = H * W;
+    uint32_t xm = 0;                      // max |x| bits: each pixel is one tile row's centre
     int it = 0;
     for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int b = it & 1;
@@ -129,6 +131,8 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
           }
         }
       }
+      xm = max(xm, max(__float_as_uint(v[12]) & 0x7fffffffu,
+                       max(__float_as_uint(v[13]) & 0x7fffffffu, __float_as_uint(v[14]) & 0x7fffffffu)));
       float hi[KP], lo[KP];
 #pragma unroll
       for (int k = 0; k < KP; ++k) split(v[k], hi[k], lo[k]);
@@ -143,6 +147,10 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&aready[b]);
+    }
+    if (x_amax) {
+      xm = __reduce_max_sync(0xffffffffu, xm);
+      if (lane == 0 && xm) atomicMax(x_amax, xm);
     }
   } else {
     const int q = warp & 3, r = q * 32 + lane;
@@ -213,7 +221,8 @@ c1_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w,
 bool c1_conv_fwd_ok(int cin, int cout) { return cin == 3 && cout == c1::COUT; }
 
 bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                         int h, int w_, int relu, uint32_t* y_amax, cudaStream_t st) {
+                         int h, int w_, int relu, uint32_t* x_amax, uint32_t* y_amax,
+                         cudaStream_t st) {
   const long long npix = (long long)n * h * w_;
   if (npix == 0) return launch_status(0);
   if (!aligned16(y) || npix > 0x7fffffffLL) return BPX_ERR_UNSUPPORTED;
@@ -238,7 +247,7 @@ bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, floa
   const long long tiles = (npix + 127) / 128;
   const int grid = (int)(tiles < c1::CPS * num_sms() ? tiles : c1::CPS * num_sms());
   c1::c1_fwd_kernel<<<grid, c1::NTHREADS, c1::SMEM, st>>>(x, w, bias, ty, h, w_, npix, relu,
-                                                               y_amax);
+                                                               x_amax, y_amax);
   return launch_status();
 }
 

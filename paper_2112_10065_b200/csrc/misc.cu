@@ -150,6 +150,89 @@ bpx_status_t split_reduce(const float* parts, int splits, size_t n, float* out,
   return launch_status();
 }
 
+// Two segments (weight and bias partials) of the same split count.  Block b
+// of the wide form takes 32 float4 columns of segment b < ba ? w : b; the
+// flat form strides over the concatenated index.  Summation order as above.
+struct Seg2 {
+  const float4* p[2];
+  float4* o[2];
+  long long n4[2];
+};
+__global__ void split_reduce2_kernel(Seg2 g, int splits) {
+  const long long tot = g.n4[0] + g.n4[1];
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < tot;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int sg = j >= g.n4[0];
+    const long long i = sg ? j - g.n4[0] : j, n4 = g.n4[sg];
+    const float4* parts = g.p[sg];
+    float4 s = parts[i];
+    int k = 1;
+    for (; k + 8 <= splits; k += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = parts[(k + u) * n4 + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+    }
+    for (; k < splits; ++k) {
+      float4 v = parts[k * n4 + i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    g.o[sg][i] = s;
+  }
+}
+__global__ void split_reduce2_wide(Seg2 g, int splits, int ba) {
+  __shared__ float4 red[8][32];
+  const int sg = (int)blockIdx.x >= ba;
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const long long i = (long long)(sg ? blockIdx.x - ba : blockIdx.x) * 32 + lane;
+  const long long n4 = g.n4[sg];
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n4) {
+    for (int k = grp; k < splits; k += 8) {
+      float4 v = g.p[sg][k * n4 + i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+  }
+  red[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && i < n4) {
+    for (int q = 1; q < 8; ++q) {
+      const float4 v = red[q][lane];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    g.o[sg][i] = s;
+  }
+}
+
+bpx_status_t split_reduce_wb(const float* pw, size_t nw, float* dw, const float* pb, size_t nb,
+                             float* db, int splits, cudaStream_t st) {
+  const bool vec = nw % 4 == 0 && nb % 4 == 0 && aligned16(pw) && aligned16(dw) &&
+                   (!db || (aligned16(pb) && aligned16(db)));
+  if (!db || !vec) {          // one segment, or the scalar forms
+    bpx_status_t s = split_reduce(pw, splits, nw, dw, st);
+    if (s != BPX_OK || !db) return s;
+    return split_reduce(pb, splits, nb, db, st);
+  }
+  Seg2 g;
+  g.p[0] = reinterpret_cast<const float4*>(pw);
+  g.p[1] = reinterpret_cast<const float4*>(pb);
+  g.o[0] = reinterpret_cast<float4*>(dw);
+  g.o[1] = reinterpret_cast<float4*>(db);
+  g.n4[0] = (long long)(nw / 4);
+  g.n4[1] = (long long)(nb / 4);
+  if (splits >= 32 && g.n4[0] <= 64LL * num_sms()) {
+    const int ba = (int)cdivll(g.n4[0], 32), bb = (int)cdivll(g.n4[1], 32);
+    split_reduce2_wide<<<ba + bb, 256, 0, st>>>(g, splits, ba);
+  } else {
+    int grid = 4 * num_sms();
+    const long long tot = g.n4[0] + g.n4[1];
+    if (cdivll(tot, 256) < grid) grid = (int)cdivll(tot, 256);
+    split_reduce2_kernel<<<grid, 256, 0, st>>>(g, splits);
+  }
+  return launch_status();
+}
+
 // ----------------------------------------------------------------- maxpool
 // NHWC, 2x2 stride 2, float4 over channels (C % 4 == 0).
 __global__ void maxpool_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y,

@@ -57,5 +57,6 @@ bpx_status_t dns_linear_wgrad(const float* x, const float* dy, float* dw, float*
 namespace bpx {
 bool c1_conv_fwd_ok(int cin, int cout);
 bpx_status_t c1_conv_fwd(const float* x, const float* w, const float* bias, float* y, int n,
-                         int h, int w_, int relu, uint32_t* y_amax, cudaStream_t st);
+                         int h, int w_, int relu, uint32_t* x_amax, uint32_t* y_amax,
+                         cudaStream_t st);
 }  // namespace bpx

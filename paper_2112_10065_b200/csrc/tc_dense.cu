@@ -9,9 +9,8 @@
 // K split over CTAs (fixed-order finish kernel applies the epilogue).  A is
 // one TMA box (fwd: 32 k x 128 rows, 128-B swizzle) or four (dgrad: 32 i x
 // 32 o, 128-B swizzle) per 32-K stage; A converter warps split it into TF32
-// hi/lo in TMEM (TS form).  The activations' lo split is made by one tiny
-// kernel per call and both halves come by TMA, so shared memory carries
-// only the MMA's B reads.  3xTF32 with 128-K chunk promotion into RN fp32
+// hi/lo in TMEM (TS form) and write the activations' lo split next to their
+// TMA tile in shared memory.  3xTF32 with 128-K chunk promotion into RN fp32
 // registers, as in the conv engines.
 //
 // CTA: 10 warps.  warp 0 TMA, warp 1 MMA + TMEM owner, 2-5 A converters,
@@ -59,7 +58,7 @@ struct Geo {
 template <int NB, bool DG>
 __global__ void __launch_bounds__(NTHREADS, CPS)
 dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           const __grid_constant__ CUtensorMap tbl, Geo g) {
+           Geo g) {
   using Cf = Cfg<NB>;
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
@@ -98,20 +97,18 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     if (lane == 0) {
       tma_prefetch_desc(&ta);
       tma_prefetch_desc(&tb);
-      tma_prefetch_desc(&tbl);
       for (int i = 0; i < nst; ++i) {
         const int s = i % S;
         if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
         const int k = k0 + i * BK;
         char* st = smem + s * Cf::STAGE;
-        mbar_expect_tx(&full[s], A_BYTES + 2 * Cf::B_BYTES);
+        mbar_expect_tx(&full[s], A_BYTES + Cf::B_BYTES);
         if (DG) {           // W[o][i] rows o = k..k+31, columns i = m0 + 32j
           for (int j = 0; j < 4; ++j) tma_load_2d(st + j * 4096, &ta, m0 + 32 * j, k, &full[s]);
         } else {            // W[o][k] rows o = m0..m0+127, columns k..k+31
           tma_load_2d(st, &ta, k, m0, &full[s]);
         }
         tma_load_2d(st + A_BYTES, &tb, k, 0, &full[s]);
-        tma_load_2d(st + A_BYTES + Cf::B_BYTES, &tbl, k, 0, &full[s]);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -153,7 +150,19 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     for (int i = 0; i < nst; ++i) {
       const int s = i % S;
       mbar_wait(&full[s], (i / S) & 1);
-      const char* st = smem + s * Cf::STAGE;
+      char* st = smem + s * Cf::STAGE;
+      {   // the activations' lo split, granule for granule (same swizzle)
+        const int t = (warp - 2) * 32 + lane;
+#pragma unroll
+        for (int j = t; j < Cf::B_BYTES / 16; j += 128) {
+          const float4 v = *reinterpret_cast<const float4*>(st + A_BYTES + 16 * j);
+          float h, l0, l1, l2, l3;
+          split(v.x, h, l0); split(v.y, h, l1); split(v.z, h, l2); split(v.w, h, l3);
+          *reinterpret_cast<float4*>(st + A_BYTES + Cf::B_BYTES + 16 * j) =
+              make_float4(l0, l1, l2, l3);
+        }
+        fence_proxy_async();        // generic stores -> the MMA's async-proxy reads
+      }
       float hi[BK], lo[BK];
       if (DG) {     // box q holds rows k (o) x 32 columns (i); lane reads column `lane`
         const char* box = st + q * 4096;
@@ -227,16 +236,9 @@ dtc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   }
 }
 
-__global__ void lo_kernel(const float* __restrict__ x, float* __restrict__ lo, long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    float h, l;
-    split(x[i], h, l);
-    lo[i] = l;
-  }
-}
-
-// out[n][m] = epilogue(sum_s part[s][n][m]); mode 0: + bias, ReLU; mode 1: mask
+// out[n][m] = epilogue(sum_s part[s][n][m]); mode 0: + bias, ReLU; mode 1: mask.
+// (Folded into the GEMM as a last-CTA-per-tile finish it measured slower:
+// one CTA per M tile sums all the parts at the kernel's tail.)
 __global__ void dtc_finish(const float* __restrict__ part, int splits, long long NM, int M,
                            const float* __restrict__ bias, int relu,
                            const float* __restrict__ mask, int mode, float* __restrict__ out) {
@@ -283,15 +285,15 @@ inline void geometry(int M, int K, bool dg, int& splits, int& kslice) {
 }
 
 template <int NB, bool DG>
-bpx_status_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl,
-                    Geo g, int mt, int splits, cudaStream_t st) {
+bpx_status_t launch(const CUtensorMap& ta, const CUtensorMap& tb, Geo g, int mt, int splits,
+                    cudaStream_t st) {
   auto kern = dtc_kernel<NB, DG>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NB>::SMEM);
     attr = true;
   }
-  kern<<<dim3(mt, splits), NTHREADS, Cfg<NB>::SMEM, st>>>(ta, tb, tbl, g);
+  kern<<<dim3(mt, splits), NTHREADS, Cfg<NB>::SMEM, st>>>(ta, tb, g);
   return launch_status();
 }
 
@@ -303,31 +305,25 @@ bpx_status_t run(bool dg, const float* W, const float* act, int batch, int M, in
   geometry(M, K, dg, splits, kslice);
   const int mt = cdiv(M, 128);
   const int nb = nb_for(batch);
-  const size_t need = (size_t)batch * K + (size_t)splits * batch * M;
+  const size_t need = (size_t)splits * batch * M + 4;
   if (ws_floats < need) return BPX_ERR_WORKSPACE;
-  float* lo = ws;
-  float* part = ws + (size_t)batch * K;
-  part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(part) + 15) & ~uintptr_t(15));
-  CUtensorMap ta, tb, tbl;
+  float* part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + 15) & ~uintptr_t(15));
+  CUtensorMap ta, tb;
   const bool ok = (dg ? encode2d(&ta, W, M, K, 32, 32) : encode2d(&ta, W, K, M, 32, 128)) &&
-                  encode2d(&tb, act, K, batch, 32, nb) && encode2d(&tbl, lo, K, batch, 32, nb);
+                  encode2d(&tb, act, K, batch, 32, nb);
   if (!ok) return BPX_ERR_INVALID_ARGUMENT;
-  const long long nlo = (long long)batch * K;
-  int lg = (int)cdivll(nlo, 256);
-  if (lg > 2 * num_sms()) lg = 2 * num_sms();
-  lo_kernel<<<lg, 256, 0, st>>>(act, lo, nlo);
   Geo g{M, K, batch, kslice, dg ? 1 : 0, part};
   bpx_status_t s;
-  if (nb == 16) s = dg ? launch<16, true>(ta, tb, tbl, g, mt, splits, st)
-                            : launch<16, false>(ta, tb, tbl, g, mt, splits, st);
-  else s = dg ? launch<32, true>(ta, tb, tbl, g, mt, splits, st)
-              : launch<32, false>(ta, tb, tbl, g, mt, splits, st);
+  if (nb == 16) s = dg ? launch<16, true>(ta, tb, g, mt, splits, st)
+                            : launch<16, false>(ta, tb, g, mt, splits, st);
+  else s = dg ? launch<32, true>(ta, tb, g, mt, splits, st)
+              : launch<32, false>(ta, tb, g, mt, splits, st);
   if (s != BPX_OK) return s;
   const long long NM = (long long)batch * M;
   int fg = (int)cdivll(NM, 256);
   if (fg > 8 * num_sms()) fg = 8 * num_sms();
   dtc_finish<<<fg, 256, 0, st>>>(part, splits, NM, M, bias, relu, mask, dg ? 1 : 0, out);
-  return launch_status(2);
+  return launch_status();
 }
 
 }  // namespace dtc
@@ -342,8 +338,8 @@ size_t dtc_linear_ws(int b, int in, int out) {
   int s1, k1, s2, k2;
   dtc::geometry(out, in, false, s1, k1);    // fwd: M = out, K = in
   dtc::geometry(in, out, true, s2, k2);     // dgrad: M = in, K = out
-  const size_t a = (size_t)b * in + (size_t)s1 * b * out;
-  const size_t c = (size_t)b * out + (size_t)s2 * b * in;
+  const size_t a = (size_t)s1 * b * out;
+  const size_t c = (size_t)s2 * b * in;
   return ((a > c ? a : c) + 4) * sizeof(float);
 }
 

@@ -347,15 +347,10 @@ bpx_status_t wg1_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
     attr = true;
   }
   wg1::wg1_kernel<<<grid, wg1::NT, wg1::SMEM, st>>>(tx, tdz, g, part, bpart);
-  {
-    cudaError_t e = cudaPeekAtLastError();
-    if (e != cudaSuccess) fprintf(stderr, "wg1 launch: %s (smem %d grid %d)\n", cudaGetErrorString(e), wg1::SMEM, grid);
-  }
   bpx_status_t s = launch_status();
   if (s != BPX_OK) return s;
-  s = split_reduce(part, grid, (size_t)wg1::CO * wg1::R, dw, st);
-  if (s != BPX_OK || !dbias) return s;
-  return split_reduce(bpart, grid, (size_t)wg1::CO, dbias, st);
+  return split_reduce_wb(part, (size_t)wg1::CO * wg1::R, dw, bpart, (size_t)wg1::CO, dbias, grid,
+                         st);
 }
 
 }  // namespace bpx

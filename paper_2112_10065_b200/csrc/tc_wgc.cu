@@ -397,9 +397,7 @@ bpx_status_t wgc_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
   wgc::wgc_kernel<<<grid, wgc::NT, wgc::SMEM, st>>>(tx, tdz, g, part, bpart);
   bpx_status_t s = launch_status();
   if (s != BPX_OK) return s;
-  s = split_reduce(part, grid, (size_t)g.slab, dw, st);
-  if (s != BPX_OK || !dbias) return s;
-  return split_reduce(bpart, grid, (size_t)wgc::C, dbias, st);
+  return split_reduce_wb(part, (size_t)g.slab, dw, bpart, (size_t)wgc::C, dbias, grid, st);
 }
 
 }  // namespace bpx

@@ -517,9 +517,7 @@ bpx_status_t wgh_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
                                                           st))
       : wgh::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
   if (s != BPX_OK || splits == 1) return s;
-  s = split_reduce(part, splits, slab, dw, st);
-  if (s != BPX_OK || !dbias) return s;
-  return split_reduce(bpart, splits, (size_t)cout, dbias, st);
+  return split_reduce_wb(part, slab, dw, bpart, (size_t)cout, dbias, splits, st);
 }
 
 }  // namespace bpx

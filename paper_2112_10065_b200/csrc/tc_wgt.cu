@@ -645,9 +645,7 @@ bpx_status_t wgt_conv_wgrad(const float* x, const float* dz, float* dw, float* d
       : (ga ? wgt::launch<64, false, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
             : wgt::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st));
   if (s != BPX_OK || splits == 1) return s;
-  s = split_reduce(part, splits, slab, dw, st);
-  if (s != BPX_OK || !dbias) return s;
-  return split_reduce(bpart, splits, (size_t)cout, dbias, st);
+  return split_reduce_wb(part, slab, dw, bpart, (size_t)cout, dbias, splits, st);
 }
 
 }  // namespace bpx

@@ -307,11 +307,16 @@ class BurstStep:
         # and one max |v| word per conv operand (x for fwd + wgrad, dz for
         # dgrad + wgrad), reduced once per step and shared by the engines
         self.wbatch = None
+        self._words_zeroed = False
         self.amax_words = None
         if hasattr(self.k, "F16Split"):
             convs = [L for L in self.layers if L.active and L.spec.kind == "conv"]
-            words = torch.zeros(max(1, len(convs)) * 8, dtype=torch.int32, device=dev)
-            self.wbatch = self.k.F16SplitBatch([L.w for L in convs]) if convs else None
+            if convs:       # the operand words ride on the weight split's memset
+                self.wbatch = self.k.F16SplitBatch([L.w for L in convs],
+                                                   extra_words=8 * len(convs))
+                words = self.wbatch.extra
+            else:
+                words = torch.zeros(8, dtype=torch.int32, device=dev)
             for j, L in enumerate(convs):
                 L.wsplit = self.wbatch.splits[j]
                 # the fp16x3 engines' shapes (fdt / wgh / wgc / wg1): Cout % 64
@@ -438,8 +443,9 @@ class BurstStep:
         a conv forward (fdt / c1 epilogue) or a 2x2 max pool on the same g
         (a chain edge, no reshard), dz from the dgrad of its only consumer
         (a conv or a pool) on the same g.  Every other operand gets one
-        bpx_absmax launch.  The words are zeroed at the start of the step's
-        forward (first active layer)."""
+        bpx_absmax launch.  The words are zeroed with the weights' split after
+        each update (one memset), or by the first active layer's forward when
+        no update preceded it."""
         self.first_active = min((i for i, L in enumerate(self.layers) if L.active), default=-1)
         if os.environ.get("BPX_FUSE_AMAX", "1") == "0":
             return
@@ -447,6 +453,8 @@ class BurstStep:
             sp = L.spec
             if L.amax is None or sp.bn or sp.down:
                 continue
+            if L.src_i < 0 and sp.kind == "conv" and sp.cin == 3 and sp.cout == 64:
+                L.x_fused = True      # the first-conv engine (c1) reduces x as it reads it
             if L.src_i >= 0 and not L.reshard_in and self.layers[L.src_i].g == L.g:
                 S = self.layers[L.src_i]
                 if ((S.spec.kind == "conv" and not S.spec.bn) or
@@ -493,7 +501,11 @@ class BurstStep:
         L = self.layers[i]
         sp = L.spec
         if i == getattr(self, "first_active", None) and self.amax_words is not None:
-            self.amax_words.zero_()           # fused producers atomicMax into them
+            # fused producers atomicMax into the words: zeroed by the weight
+            # split after the last update, else here
+            if not self._words_zeroed:
+                self.amax_words.zero_()
+            self._words_zeroed = False
         lo = {"wsplit": L.wsplit} if L.wsplit is not None else {}
         if sp.bn:
             # conv without bias / activation into z, then the synchronised BN
@@ -764,6 +776,7 @@ class BurstStep:
     def _split_w(self) -> None:
         if self.wbatch is not None:
             self.wbatch.refresh()
+            self._words_zeroed = True
 
     def run_ops(self, prog) -> None:
         for key, fn in prog:

@@ -267,9 +267,11 @@ class F16Split:
 class F16SplitBatch:
     """fp16x3 splits of several weight tensors refreshed together (three
     graph nodes per update, bpx_f16_split_batch): ``splits[k]`` is the
-    F16Split view of ``ws[k]``.  The tensors must keep their storage."""
+    F16Split view of ``ws[k]``.  The tensors must keep their storage.
+    ``extra`` = ``extra_words`` int32 words of the caller's, zeroed by every
+    refresh's memset."""
 
-    def __init__(self, ws: list):
+    def __init__(self, ws: list, extra_words: int = 0):
         lib = load_library()
         dev = ws[0].device
         offs, tot = [], 0
@@ -281,7 +283,9 @@ class F16SplitBatch:
             tot += (w.numel() + 7) // 8 * 8            # 16-B aligned fp16 slices
         self.hi = torch.empty(tot, dtype=torch.float16, device=dev)
         self.lo = torch.empty(tot, dtype=torch.float16, device=dev)
-        self.words = torch.zeros(4 * len(ws), dtype=torch.int32, device=dev)
+        self.words = torch.zeros(4 * len(ws) + extra_words, dtype=torch.int32, device=dev)
+        # caller-owned words zeroed by the same memset on every refresh
+        self.extra = self.words[4 * len(ws):]
         chunk = lib.bpx_f16_split_batch_chunk()
         rows, blk = [], 0
         self.splits = []

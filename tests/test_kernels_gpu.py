@@ -490,3 +490,55 @@ def test_conv_wgrad_first_layer(shape):
     torch.cuda.synchronize()
     close(dw, dw_ref, dw32)
     close(db, db_ref, db32)
+
+
+def test_split_k_paths_deterministic():
+    """Split-K paths (fixed-order finishes): conv5 fwd / dgrad at B = 32
+    (fdt split-K), a wgrad with K splits (wgh, weight + bias partials
+    reduced in one launch), fc fwd / dgrad (dtc with the activations' lo
+    split made in-kernel, dns): two runs are bitwise equal and match
+    fp64."""
+    n, h, c = 32, 14, 512
+    x = relu_input(n, h, h, c, seed=41)
+    w = rnd(c, 3, 3, c, seed=42, scale=math.sqrt(2 / (9 * c)))
+    b = rnd(c, seed=43, scale=0.1)
+    dz = rnd(n, h, h, c, seed=44)
+    X, Wd, B, DZ = x.to(DEV), w.to(DEV), b.to(DEV), dz.to(DEV)
+    outs = []
+    for _ in range(2):
+        y = torch.empty(n, h, h, c, device=DEV)
+        ops.conv3x3_fwd(X, Wd, B, y, relu=True)
+        dx = torch.empty(n, h, h, c, device=DEV)
+        ops.conv3x3_dgrad(DZ, Wd, X, dx)
+        dw = torch.empty(c, 3, 3, c, device=DEV)
+        db = torch.empty(c, device=DEV)
+        ops.conv3x3_wgrad(X, DZ, dw, db)
+        outs.append((y, dx, dw, db))
+    torch.cuda.synchronize()
+    for a, b2 in zip(*outs):
+        assert torch.equal(a, b2)
+    spec = LayerSpec("c", "conv", c, c, h, True, False)
+    close(outs[0][0], vgg_ref.layer_fwd(spec, x, w, b),
+          vgg_ref.layer_fwd(spec, x, w, b, dtype=torch.float32))
+    dx_ref, dw_ref, db_ref = vgg_ref.conv_grads(x, w, dz)
+    dx32, dw32, db32 = vgg_ref.conv_grads(x, w, dz, torch.float32)
+    close(outs[0][1], dx_ref * (x > 0), dx32 * (x > 0))
+    close(outs[0][2], dw_ref, dw32)
+    close(outs[0][3], db_ref, db32)
+    for fin, fout in ((25088, 4096), (4096, 1000)):
+        xa = relu_input(32, fin, seed=45).to(DEV)
+        wa = rnd(fout, fin, seed=46, scale=0.01).to(DEV)
+        ba = rnd(fout, seed=47, scale=0.1).to(DEV)
+        dya = rnd(32, fout, seed=48).to(DEV)
+        res = []
+        for _ in range(2):
+            ya = torch.empty(32, fout, device=DEV)
+            ops.linear_fwd(xa, wa, ba, ya, True)
+            dxa = torch.empty(32, fin, device=DEV)
+            ops.linear_dgrad(dya, wa, xa, dxa)
+            res.append((ya, dxa))
+        torch.cuda.synchronize()
+        for a, b2 in zip(*res):
+            assert torch.equal(a, b2)
+        y64 = torch.relu(xa.double() @ wa.double().t() + ba.double())
+        assert vgg_ref.normwise_rel(res[0][0].cpu(), y64.cpu()) < 2e-6
