@@ -72,8 +72,11 @@ struct Cfg {
   static constexpr int A_COL = 2 * BN;                    // accumulators: 2 x BN columns
   static constexpr int A_STAGE = KS;                      // TMEM columns per stage: hi | lo
   static_assert(A_COL + S * A_STAGE <= 512, "TMEM budget");
-  // dynamic smem = 1024 (align) + S*STAGE + 2 halo slots + 512 (barriers)
-  static int smem(int halo_bytes) { return 1024 + S * STAGE + 2 * halo_bytes + 512; }
+  // dynamic smem = 1024 (align) + B stages (S, or the nine resident tiles)
+  // + 2 halo slots + 512 (barriers)
+  static int smem(int halo_bytes, bool rb) {
+    return 1024 + (rb ? 9 : S) * STAGE + 2 * halo_bytes + 512;
+  }
 };
 
 struct Geo {
@@ -191,7 +194,9 @@ __device__ __forceinline__ void unit_tile(const Geo& g, int u, uint32_t rank, in
 // tile of the unit (the layer input, 128 pixels x BN channels) comes by
 // TMA into shared memory, issued mid-unit, so the epilogue reads it there
 // instead of issuing 16 dependent global loads per thread.
-template <int BN, int S_, bool DG, bool PAIR, class EPI, bool MT = false>
+// RB (one 64-channel chunk and one N tile per launch, e.g. conv1_2): the nine
+// B tiles are loaded once and stay resident; the B ring disappears.
+template <int BN, int S_, bool DG, bool PAIR, class EPI, bool MT = false, bool RB = false>
 __global__ void __launch_bounds__(Cfg<BN, S_, PAIR>::NTHREADS, 1)
 fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tbl, const __grid_constant__ CUtensorMap tm,
@@ -203,9 +208,10 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   extern __shared__ char smem_raw[];
   // offset from smem_raw (not a uintptr_t round trip) keeps the shared address space: LDS/STS, not generic LD/ST
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  char* halo = smem + S * Cf::STAGE;                          // 2 slots
+  constexpr int NBS = RB ? 9 : S;                             // B stages in smem
+  char* halo = smem + NBS * Cf::STAGE;                        // 2 slots
   uint64_t* bfull = reinterpret_cast<uint64_t*>(halo + 2 * g.halo_bytes);
-  uint64_t* aready = bfull + S;
+  uint64_t* aready = bfull + NBS;
   uint64_t* empty = aready + S;
   uint64_t* hfull = empty + S;       // halo slot loaded
   uint64_t* hempty = hfull + 2;      // halo slot consumed by all nine taps
@@ -226,8 +232,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (tid == 0) {
+    for (int s = 0; s < NBS; ++s) mbar_init(&bfull[s], 1);
     for (int s = 0; s < S; ++s) {
-      mbar_init(&bfull[s], 1);
       mbar_init(&aready[s], PAIR ? 2 * NCONV : NCONV);   // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
@@ -299,13 +305,17 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         const int n0 = nti * BN + (int)rank * BNL;          // this CTA's B channels
         for (int cc = kh * cpu; cc < (kh + 1) * cpu; ++cc, ++hc) {
           for (int tap = 0; tap < 9; ++tap, ++i) {
-            const int s = i % S;
+            const int s = RB ? tap : i % S;
+            if (!RB || i < 9) {      // resident B: the first unit's nine loads only
             PROF_START();
-            if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+            if (!RB && i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
             PROF_ADD(12, true);
             char* st = smem + s * Cf::STAGE;
             mbar_expect_tx(&bfull[s], 2 * Cf::B_BYTES);
-            if (DG) {        // BNL/64 boxes of 64 ci x KS co rows (MN-major)
+            if (DG && BNL == 32) {   // a pair's half: 32 ci x KS co rows, 64-B swizzle
+              tma_load_3d(st, &tb, n0, tap, cc * KS, &bfull[s]);
+              tma_load_3d(st + Cf::B_BYTES, &tbl, n0, tap, cc * KS, &bfull[s]);
+            } else if (DG) { // BNL/64 boxes of 64 ci x KS co rows (MN-major)
 #pragma unroll
               for (int j = 0; j < BNL / 64; ++j) {
                 tma_load_3d(st + j * KS * 128, &tb, n0 + 64 * j, tap, cc * KS, &bfull[s]);
@@ -316,6 +326,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
               const int k0 = tap * g.C + cc * KS;
               tma_load_2d(st, &tb, k0, n0, &bfull[s]);
               tma_load_2d(st + Cf::B_BYTES, &tbl, k0, n0, &bfull[s]);
+            }
             }
             if (MT && tap == 4 && cc == (kh + 1) * cpu - 1) {    // the unit's mask tile
               if (mu >= 1) mbar_wait(mfree, (mu - 1) & 1);
@@ -367,14 +378,18 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + KS / 2;
-        const uint32_t bh = smem_u32(smem + s * Cf::STAGE);
-        const uint64_t dbh0 = DG ? make_desc_sw128(bh, KS * 128, 1024) : make_desc_sw128(bh, 16, 1024);
+        const uint32_t bh = smem_u32(smem + (RB ? kb : s) * Cf::STAGE);
+        // dgrad B is MN-major: 64-channel atoms with the 128-B swizzle, or a
+        // pair's 32-channel halves with the 64-B swizzle (8 k-rows = 512 B)
+        const uint64_t dbh0 = !DG ? make_desc_sw128(bh, 16, 1024)
+                              : BNL == 32 ? make_desc_sw64(bh, KS * 64, 512)
+                                          : make_desc_sw128(bh, KS * 128, 1024);
         const uint64_t dbl0 = dbh0 + (Cf::B_BYTES >> 4);
 #pragma unroll
         for (int ks = 0; ks < KS / 16; ++ks) {
           // descriptor start address is (addr >> 4) in bits [0,14): dgrad
           // steps 16 k-rows (2 KB), fwd 16 fp16 of the 128-B K row (32 B)
-          const uint32_t off = DG ? ks * 2048 : ks * 32;
+          const uint32_t off = DG ? ks * (BNL == 32 ? 1024 : 2048) : ks * 32;
           const uint64_t dbh = dbh0 + (off >> 4), dbl = dbl0 + (off >> 4);
           const uint32_t acc = (kb % PCH != 0 || ks > 0) ? 1u : 0u;
 #ifndef FDT_NOMMA
@@ -516,7 +531,8 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
           tc_fence_before();
           PROF_START();
           if (lane == 0) {
-            mbar_wait(&bfull[s], (i / S) & 1);     // aready[s] implies the B tiles
+            // aready[s] implies the B tiles (resident: loaded once, phase 0)
+            if (RB) mbar_wait(&bfull[tap], 0u); else mbar_wait(&bfull[s], (i / S) & 1);
             if (PAIR) mbar_arrive_remote(aready_l + 8u * s); else mbar_arrive(&aready[s]);
           }
           PROF_ADD(9, pw);
@@ -659,13 +675,20 @@ inline int ksplit_for(long long tiles, int chunks, int slots) {
   return k;
 }
 
-// CTA pairs (cta_group::2): every shape but the 64-wide dgrad (its 32-channel
-// B halves would need a 64-B swizzle) when there are two M tiles to pair
+// CTA pairs (cta_group::2) when there are two M tiles to pair (the 64-wide
+// dgrad's 32-channel MN-major B halves take the 64-B swizzle)
 #ifndef FDT_PAIR
 #define FDT_PAIR 1
 #endif
-inline bool pair_for(int BN, bool dg, long long mt) {
-  return FDT_PAIR && (!dg || BN == 128) && mt >= 2 && num_sms() >= 2;
+#ifndef FDT_PAIR64DG
+#define FDT_PAIR64DG 1
+#endif
+// (64-wide dgrad pairs only where the nine B tiles also stay resident, i.e.
+// Cin = Cout = 64: conv1_2 dgrad 0.521 -> 0.511 ms; conv2_1's dgrad, with two
+// 64-channel chunks, measured 3 % slower paired -- B200 same-box A/B)
+inline bool pair_for(int BN, bool dg, long long mt, int C = 0) {
+  return FDT_PAIR && (!dg || BN == 128 || (FDT_PAIR64DG && C == 64)) && mt >= 2 &&
+         num_sms() >= 2;
 }
 
 // work units of a launch: tiles (M tile pairs) x N tiles x K parts
@@ -716,12 +739,15 @@ inline const float* mask_of(const EMask& e) { return e.mask; }
 #ifndef FDT_MT
 #define FDT_MT 1
 #endif
+#ifndef FDT_RB
+#define FDT_RB 1
+#endif
 
-template <int BN, int S, bool DG, bool PAIR, class EPI, bool MT>
+template <int BN, int S, bool DG, bool PAIR, class EPI, bool MT, bool RB>
 bpx_status_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl,
                     const CUtensorMap& tm, const Geo& g, int smem, EPI epi, cudaStream_t st) {
   using Cf = Cfg<BN, S, PAIR>;
-  auto kern = fdt_kernel<BN, S, DG, PAIR, EPI, MT>;
+  auto kern = fdt_kernel<BN, S, DG, PAIR, EPI, MT, RB>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -781,8 +807,22 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
   g.halo_bytes = NCH * g.half_bytes;
   g.halo_tx = NCH * (g.tw ? (g.tw + 2) * (g.th + 2) * 128 : g.half_bytes);
   g.halo_rows = g.tw ? (g.tw + 2) * (g.th + 2) : g.nhbox * g.hbox;
-  const int smem = Cf::smem(g.halo_bytes);
-  if (smem > 227 * 1024) return BPX_ERR_UNSUPPORTED;
+  // shared memory: the MT mask tile where it fits; the nine B tiles resident
+  // when one 64-channel chunk and one N tile make up the whole launch
+  // (64-wide tiles only: conv1_2) and they fit beside it
+  const int cap = 227 * 1024, mt_bytes = 512 + BN * 128 * 4;
+  const bool want_mt = FDT_MT && DG && mask_of(epi) && g.ksplit == 1;
+  // (the forward measured 4 % slower with B resident: dgrad only)
+  const bool rb_shape = FDT_RB && DG && BN == 64 && g.C == KS && g.nt == 1 && g.ksplit == 1;
+  bool rb = false, mt;
+  if (rb_shape && Cf::smem(g.halo_bytes, true) + (want_mt ? mt_bytes : 0) <= cap) {
+    rb = true;
+    mt = want_mt;
+  } else {
+    mt = want_mt && Cf::smem(g.halo_bytes, false) + mt_bytes <= cap;
+  }
+  const int smem = Cf::smem(g.halo_bytes, rb);
+  if (smem > cap) return BPX_ERR_UNSUPPORTED;
   CUtensorMap ta, tb, tbl;
   if (g.tw) {        // activations [n][H][W][C]: box 32 ch x (tw+2) x (th+2) x 1 image
     const cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
@@ -806,9 +846,9 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
     if (DG) {       // w16 as [Cout][9][Cin]: box 64 ci x 1 tap x KS co, MN-major
       const cuuint64_t dims[3] = {(cuuint64_t)Cin, 9, (cuuint64_t)Cout};
       const cuuint64_t strides[2] = {(cuuint64_t)Cin * 2, (cuuint64_t)9 * Cin * 2};
-      const cuuint32_t box[3] = {64, 1, (cuuint32_t)KS};
+      const cuuint32_t box[3] = {Cf::BNL == 32 ? 32u : 64u, 1, (cuuint32_t)KS};
       if (!encode(m, src, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, dims, strides, box,
-                  CU_TENSOR_MAP_SWIZZLE_128B))
+                  Cf::BNL == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
         return BPX_ERR_INVALID_ARGUMENT;
     } else {        // w16 as [Cout][9*Cin]: box 64 k x BNL rows, K-major
       const cuuint64_t dims[2] = {(cuuint64_t)9 * Cin, (cuuint64_t)Cout};
@@ -819,10 +859,9 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
-  // MT: the dgrad mask staged by TMA where it fits
+  // MT: the dgrad mask staged by TMA
   const float* mptr = mask_of(epi);
-  const int smem_mt = smem + 512 + BN * 128 * 4;
-  const bool mt = FDT_MT && DG && mptr && g.ksplit == 1 && smem_mt <= 227 * 1024;
+  const int smem_mt = smem + mt_bytes;
   CUtensorMap tm = ta;
   if (mt) {
     if (g.tw) {
@@ -842,9 +881,12 @@ bpx_status_t run(const float* a, const F16Weights& wt, float* part, const uint32
         return BPX_ERR_INVALID_ARGUMENT;
     }
   }
+  constexpr bool RBT = BN == 64;             // instantiate resident B for 64-wide tiles
   const bpx_status_t ls =
-      mt ? launch<BN, S, DG, PAIR, EPI, true>(ta, tb, tbl, tm, g, smem_mt, epi, st)
-         : launch<BN, S, DG, PAIR, EPI, false>(ta, tb, tbl, tm, g, smem, epi, st);
+      rb ? (mt ? launch<BN, S, DG, PAIR, EPI, true, RBT>(ta, tb, tbl, tm, g, smem_mt, epi, st)
+               : launch<BN, S, DG, PAIR, EPI, false, RBT>(ta, tb, tbl, tm, g, smem, epi, st))
+         : (mt ? launch<BN, S, DG, PAIR, EPI, true, false>(ta, tb, tbl, tm, g, smem_mt, epi, st)
+               : launch<BN, S, DG, PAIR, EPI, false, false>(ta, tb, tbl, tm, g, smem, epi, st));
   if (ls != BPX_OK) return ls;
   if (g.ksplit == 1) return launch_status(1);
   const long long groups = (long long)g.npix * (g.N / 8);
@@ -876,8 +918,9 @@ bpx_status_t dispatch(const float* a, const F16Weights& wt, float* part, const u
       return run<128, FDT_S128P, DG, true>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
     return run<128, FDT_S128, DG, false>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
   }
-  if (pair_for(64, DG, mt))
-    return run<64, FDT_S64, DG, !DG>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
+  if (pair_for(64, DG, mt, DG ? Cout : Cin))
+    return run<64, FDT_S64, DG, (!DG || FDT_PAIR64DG)>(a, wt, part, amax_a, n, H, W, Cin, Cout,
+                                                        epi, st);
   return run<64, FDT_S64, DG, false>(a, wt, part, amax_a, n, H, W, Cin, Cout, epi, st);
 }
 
@@ -934,7 +977,7 @@ size_t fdt_conv_ws(int n, int h, int w, int cin, int cout) {
     const long long mt = tw ? (long long)n * (h / th) * (w / tw) : cdivll(npix, 128);
     int k = 1, units;
     if (C % fdt::KS == 0)
-      fdt::plan_units(mt, N / BN, C / fdt::KS, fdt::pair_for(BN, dg, mt), k, units);
+      fdt::plan_units(mt, N / BN, C / fdt::KS, fdt::pair_for(BN, dg, mt, C), k, units);
     if (k > 1) {
       const size_t need = (size_t)k * npix * N;
       part = part > need ? part : need;

@@ -336,5 +336,11 @@ __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t lbo
                                                     uint32_t sbo) {
   return make_desc(saddr, lbo, sbo) | ((uint64_t)2 << 61);
 }
+// 64-byte-swizzle descriptor (layout type 4): 512-B atoms of 8 rows x 64 B
+// (e.g. a 32-element MN-major fp16 operand: SBO = 512 per 8 K-rows)
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t saddr, uint32_t lbo,
+                                                   uint32_t sbo) {
+  return make_desc(saddr, lbo, sbo) | ((uint64_t)4 << 61);
+}
 }  // namespace tcx
 }  // namespace bpx
