@@ -43,6 +43,16 @@ constexpr int TMA_WARP = 0, MMA_WARP = 1, CA0 = 2, CB0 = 6, DR0 = 10, NT = 18 * 
 constexpr int BK = 64;                          // pixels per stage
 constexpr int BOX = 32 * BK * 4;                // 32 channels x 64 pixels, fp32
 constexpr int PCH = 128 / BK;                   // stages per promotion chunk (K = 128)
+// SSA (experiment, Cin % 64 == 0): A (x^T) is read by the MMA straight from
+// shared memory as an MN-major operand -- x's natural [pixel][channel]
+// layout -- after the A converters split its boxes IN PLACE into fp16 hi/lo
+// atoms (as the B converters do for dz), instead of the column-wise
+// transpose into TMEM.  Correct, but 9-14 % slower on every VGG wgrad layer
+// (B200 same-box A/B: the three SS-form MMAs re-read A from shared memory,
+// 4 KB each): off
+#ifndef WGH_SSA
+#define WGH_SSA 0
+#endif
 
 // PAIR (BN = 128): a cluster of two CTAs (M tiles 2m, 2m+1, same N tile and
 // pixel split) runs one M = 256 MMA (cta_group::2); each CTA loads and splits
@@ -79,7 +89,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, bool SSA = false>
 __global__ void __launch_bounds__(NT, 1)
 wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdz,
            Geo g, float* __restrict__ part, float* __restrict__ bias_part) {
@@ -169,7 +179,8 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     // M=128, N=BN, f16 x f16 -> f32, A from TMEM, B MN-major (bit 16): atom a
     // (64 channels) of b_hi sits where box 2a landed, b_lo where box 2a+1 did
     constexpr uint32_t idesc = (PAIR ? ((make_idesc_f16(BN) & ~(0x1Fu << 24)) | (16u << 24))
-                                     : make_idesc_f16(BN)) | (1u << 16);
+                                     : make_idesc_f16(BN)) | (1u << 16) |
+                               (SSA ? (1u << 15) : 0u);           // A MN-major (SSA)
     for (int i = 0; i < nst && (!PAIR || rank == 0); ++i) {
       const int s = i % S;
       const int c = i / PCH, b = c & 1;
@@ -182,14 +193,27 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       tc_fence_after();
       const uint32_t d = tmem + b * BN;
       const uint32_t ah = tmem + Cf::A_COL + s * Cf::A_STAGE, al = ah + BK / 2;
-      const uint32_t bx = smem_u32(smem + s * Cf::STAGE + Cf::A_BYTES);
+      const uint32_t ax = smem_u32(smem + s * Cf::STAGE);
+      const uint32_t bx = ax + Cf::A_BYTES;
 #pragma unroll
       for (int ks = 0; ks < BK / 16; ++ks) {
         const uint64_t dbh = make_desc_sw128(bx + ks * 2048, 2 * BOX, 1024);
         const uint64_t dbl = make_desc_sw128(bx + BOX + ks * 2048, 2 * BOX, 1024);
         const uint32_t acc = (i % PCH != 0 || ks > 0) ? 1u : 0u;
 #ifndef WGH_NOMMA
-        if (PAIR) {
+        if (SSA) {         // A atoms a = 0, 1 (64 rows each) where boxes 2a / 2a+1 landed
+          const uint64_t dah = make_desc_sw128(ax + ks * 2048, 2 * BOX, 1024);
+          const uint64_t dal = make_desc_sw128(ax + BOX + ks * 2048, 2 * BOX, 1024);
+          if (PAIR) {
+            mma_ss2_f16_elect(d, dal, dbh, idesc, acc);
+            mma_ss2_f16_elect(d, dah, dbl, idesc, 1u);
+            mma_ss2_f16_elect(d, dah, dbh, idesc, 1u);
+          } else {
+            mma_ss_f16_elect(d, dal, dbh, idesc, acc);
+            mma_ss_f16_elect(d, dah, dbl, idesc, 1u);
+            mma_ss_f16_elect(d, dah, dbh, idesc, 1u);
+          }
+        } else if (PAIR) {
           mma_ts2_f16_elect(d, al + 8 * ks, dbh, idesc, acc);
           mma_ts2_f16_elect(d, ah + 8 * ks, dbl, idesc, 1u);
           mma_ts2_f16_elect(d, ah + 8 * ks, dbh, idesc, 1u);
@@ -206,6 +230,73 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       } else {
         tc_commit_elect(&empty[s]);
         if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+      }
+    }
+  } else if (warp < CB0 && SSA) {
+    // ------------------------------------------------------------ A converters (SSA)
+    // split x IN PLACE into MN-major fp16 atoms: atom a = channels [64a, +64)
+    // of the M tile (boxes 2a, 2a+1: one tap); warp wa takes atom wa & 1,
+    // pixel rows [32 (wa >> 1), +32), four threads (16 channels) per row
+    // pair; rows whose tap-shifted pixel is outside the image become zeros
+    const int wa = warp - CA0, c16 = lane >> 3, at = wa & 1, pb = (wa >> 1) * 32;
+    const bool valid = (m0 / 32 + 2 * at) < chunks;
+    const int tap = valid ? (m0 / 32 + 2 * at) / cpt : 4;
+    const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+    const float scale = exp2i(sx);
+    long long p = (long long)t0 * BK + lane;
+    int img = (int)(p / ((long long)g.H * g.W));
+    int rem = (int)(p - (long long)img * g.H * g.W);
+    int oh = rem / g.W, ow = rem - (rem / g.W) * g.W;
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % S;
+      uint32_t vm = 0;                   // validity of pixel rows [pb, pb + 32)
+#pragma unroll
+      for (int h = 0; h < BK / 32; ++h) {
+        const bool ok = valid && p < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
+                        (unsigned)(ow + dx) < (unsigned)g.W;
+        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        if (h == (pb >> 5)) vm = b;
+        p += 32;
+        ow += 32;
+        while (ow >= g.W) {
+          ow -= g.W;
+          if (++oh == g.H) { oh = 0; ++img; }
+        }
+      }
+      mbar_wait(&full[s], (i / S) & 1);
+      char* hrow = smem + s * Cf::STAGE + 2 * at * BOX, *lrow = hrow + BOX;
+      const char* raw = hrow + (c16 >> 1) * BOX;          // this thread's 16 fp32 channels
+#if !defined(WGH_NOCONV) && !defined(WGH_NOACONV)
+      if (valid) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int pr = pb + 8 * it + (lane & 7), sw = pr & 7;
+          const bool ok = (vm >> (8 * it + (lane & 7))) & 1u;
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = *reinterpret_cast<const float4*>(raw + pr * 128 + (((4 * (c16 & 1) + u) ^ sw) << 4));
+          __syncwarp();                   // the row pair is read before anyone overwrites it
+          uint32_t h[8], l[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (!ok) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            split_f16x2_s(v[u].x, v[u].y, scale, h[2 * u], l[2 * u]);
+            split_f16x2_s(v[u].z, v[u].w, scale, h[2 * u + 1], l[2 * u + 1]);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int off = pr * 128 + (((2 * c16 + e) ^ sw) << 4);
+            *reinterpret_cast<uint4*>(hrow + off) = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
+            *reinterpret_cast<uint4*>(lrow + off) = make_uint4(l[4 * e], l[4 * e + 1], l[4 * e + 2], l[4 * e + 3]);
+          }
+        }
+      }
+#endif
+      fence_proxy_async();                // generic-proxy writes -> the MMA's async reads
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(ready_l + 8u * s); else mbar_arrive(&ready[s]);
       }
     }
   } else if (warp < CB0) {
@@ -434,11 +525,11 @@ inline bool encode_rows(CUtensorMap* m, const float* p, long long npix, int C) {
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, bool SSA>
 bpx_status_t launch(const CUtensorMap& tx, const CUtensorMap& tdz, const Geo& g, int mt,
                     int nt, int splits, float* part, float* bias_part, cudaStream_t st) {
   using Cf = Cfg<BN, PAIR>;
-  auto kern = wgh_kernel<BN, PAIR>;
+  auto kern = wgh_kernel<BN, PAIR, SSA>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
@@ -511,11 +602,17 @@ bpx_status_t wgh_conv_wgrad(const float* x, const float* dz, const uint32_t* ama
   float* scratch = reinterpret_cast<float*>(static_cast<char*>(ws) + 16);
   float* part = splits == 1 ? dw : scratch;
   float* bpart = !dbias ? nullptr : (splits == 1 ? dbias : scratch + (size_t)splits * slab);
-  bpx_status_t s = wgh::bn_for(cout) == 128
-      ? (wgh::paired(cin, cout) ? wgh::launch<128, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
-                                : wgh::launch<128, false>(tx, tdz, g, mt, nt, splits, part, bpart,
-                                                          st))
-      : wgh::launch<64, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+  const bool ssa = WGH_SSA && cin % 64 == 0;
+  bpx_status_t s;
+  if (wgh::bn_for(cout) == 128 && wgh::paired(cin, cout))
+    s = ssa ? wgh::launch<128, true, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+            : wgh::launch<128, true, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+  else if (wgh::bn_for(cout) == 128)
+    s = ssa ? wgh::launch<128, false, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+            : wgh::launch<128, false, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
+  else
+    s = ssa ? wgh::launch<64, false, true>(tx, tdz, g, mt, nt, splits, part, bpart, st)
+            : wgh::launch<64, false, false>(tx, tdz, g, mt, nt, splits, part, bpart, st);
   if (s != BPX_OK || splits == 1) return s;
   return split_reduce_wb(part, slab, dw, bpart, (size_t)cout, dbias, splits, st);
 }
