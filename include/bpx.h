@@ -182,10 +182,11 @@ BPX_API bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy,
  * transitions where hw halves, and the pool before the classifier).
  * Residual join (post-activation basic block, ResNet "option A" shortcut):
  *   y = relu?(a + P(s)),  a, y: [n][h][w][c],  s: [n][h*f][w*f][cs], cs <= c,
- *   P = stride-f subsample (f = 2 if down) + zero channel padding cs -> c.  */
+ *   P = stride-f subsample (f = 2 if down) + zero channel padding cs -> c.
+ * y_amax (nullable): atomicMax'ed with max |y| bits (zero it first).      */
 BPX_API bpx_status_t bpx_residual_add_fwd(const float* a, const float* s, float* y, int n,
                                   int h, int w_, int c, int cs, int down, int relu,
-                                  void* stream);
+                                  unsigned* y_amax, void* stream);
 /* Gradient into the skip source h ([n][h*f][w*f][cs], grad wrt h's
  * pre-activation; mask = h's ReLU output):
  *   dh = (accumulate ? dh : 0) + [sampled pixel] * (dmain + (mask > 0) * dz[.., :cs])
@@ -241,19 +242,22 @@ BPX_API bpx_status_t bpx_global_avgpool_bwd(const float* dy, const float* mask, 
  *   y        = act(gamma * (z - mu) * rstd + beta),  mu, var from stats / ntot
  *   sums     = [sum g ; sum g * xhat]  (= the local [dbeta ; dgamma])
  *   dz       = gamma * rstd * (g - sums0/ntot - xhat * sums1/ntot)
- * Fixed-order fp64 sums: bitwise reproducible.  c % 4 == 0, c <= 4096.     */
+ * Fixed-order fp64 sums: bitwise reproducible.  c % 4 == 0, c <= 4096.
+ * y_amax / dz_amax (nullable): atomicMax'ed with the output's max |v| bits
+ * (the fp16x3 scale word of the conv that reads it; zero it first).        */
 BPX_API size_t bpx_bn_workspace(long long npix, int c);
 BPX_API bpx_status_t bpx_bn_stats(const float* z, long long npix, int c, float* stats,
                           void* ws, size_t ws_bytes, void* stream);
 BPX_API bpx_status_t bpx_bn_apply(const float* z, const float* stats, const float* gamma_beta,
                           long long npix, long long ntot, int c, float eps, int relu,
-                          float* y, void* stream);
+                          float* y, unsigned* y_amax, void* stream);
 BPX_API bpx_status_t bpx_bn_bwd_sums(const float* g, const float* z, const float* stats,
                              long long npix, long long ntot, int c, float eps, float* sums,
                              void* ws, size_t ws_bytes, void* stream);
 BPX_API bpx_status_t bpx_bn_bwd_apply(const float* g, const float* z, const float* stats,
                               const float* sums, const float* gamma_beta, long long npix,
-                              long long ntot, int c, float eps, float* dz, void* stream);
+                              long long ntot, int c, float eps, float* dz,
+                              unsigned* dz_amax, void* stream);
 
 /* Mean softmax cross-entropy over the GLOBAL batch: loss_out[0] =
  * sum_{local rows} CE / b_global (fixed order); loss_out must hold

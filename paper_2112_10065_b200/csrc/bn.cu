@@ -24,19 +24,25 @@ namespace bpx {
 namespace bn {
 
 constexpr int NT = 256;
-constexpr int NB = 128;          // partial blocks (fixed: results independent of the GPU)
+// statistics passes: NB blocks of NTP threads -- a constant (results are
+// independent of the GPU), with ~8 MB of loads in flight on a whole B200
+// (128 blocks of 256 threads left them at ~25 % of the HBM rate); 256 parts
+// keep the fixed-order finish short
+constexpr int NB = 256;
+constexpr int NTP = 1024;
+constexpr int UNR = 4;           // rows (vectors) loaded per thread before their adds
 
 // partial[blk][0..c) = sum a, [c..2c) = sum a * f(b)  where MODE 0: f = a (squares);
 // MODE 1: f = (b - mu) * rstd with mu/rstd from stats (xhat of z = b)
 template <int MODE>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NTP)
 partial_kernel(const float* __restrict__ a, const float* __restrict__ b,
                const float* __restrict__ stats, long long npix, long long ntot, int c, float eps,
                double* __restrict__ part) {
   extern __shared__ double sh[];               // [rows in flight][2c]
   const int C4 = c / 4;
-  const int tpr = C4 < NT ? C4 : NT;           // threads per pixel row
-  const int rpi = NT / tpr;                    // rows in flight
+  const int tpr = C4 < NTP ? C4 : NTP;         // threads per pixel row
+  const int rpi = NTP / tpr;                   // rows in flight
   const int rr = threadIdx.x / tpr, cq = threadIdx.x % tpr;
   const int J = C4 / tpr;                      // channel groups per thread (c <= 4096)
   const long long chunk = (npix + gridDim.x - 1) / gridDim.x;
@@ -55,22 +61,35 @@ partial_kernel(const float* __restrict__ a, const float* __restrict__ b,
       }
     }
     if (rr < rpi && threadIdx.x < rpi * tpr) {
-      for (long long p = p0 + rr; p < p1; p += rpi) {
-        const float4 va = __ldg(reinterpret_cast<const float4*>(a + p * c + c0));
-        const float av[4] = {va.x, va.y, va.z, va.w};
-        if (MODE == 0) {
+      // rows p0 + rr + k * rpi in order; UNR loads issued before their adds
+      for (long long p = p0 + rr; p < p1; p += (long long)UNR * rpi) {
+        float4 va[UNR], vb[UNR];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            s1[e] += av[e];
-            s2[e] += (double)av[e] * av[e];
-          }
-        } else {
-          const float4 vb = __ldg(reinterpret_cast<const float4*>(b + p * c + c0));
-          const float bv[4] = {vb.x, vb.y, vb.z, vb.w};
+        for (int u = 0; u < UNR; ++u) {
+          const long long q = p + (long long)u * rpi;
+          va[u] = q < p1 ? __ldg(reinterpret_cast<const float4*>(a + q * c + c0))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (MODE == 1)
+            vb[u] = q < p1 ? __ldg(reinterpret_cast<const float4*>(b + q * c + c0))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            s1[e] += av[e];
-            s2[e] += (double)av[e] * ((bv[e] - mu[e]) * rs[e]);
+        for (int u = 0; u < UNR; ++u) {
+          if (p + (long long)u * rpi >= p1) break;
+          const float av[4] = {va[u].x, va[u].y, va[u].z, va[u].w};
+          if (MODE == 0) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              s1[e] += av[e];
+              s2[e] += (double)av[e] * av[e];
+            }
+          } else {
+            const float bv[4] = {vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              s1[e] += av[e];
+              s2[e] += (double)av[e] * ((bv[e] - mu[e]) * rs[e]);
+            }
           }
         }
       }
@@ -100,20 +119,46 @@ partial_kernel(const float* __restrict__ a, const float* __restrict__ b,
   }
 }
 
+// out[i] = sum_k part[k][i]: 8 warps per 32 outputs, warp w sums the parts
+// k = w, w + 8, ... (4 loads in flight), then a fixed-order combine
 __global__ void finish_kernel(const double* __restrict__ part, int nb, int n2,
                               float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n2) return;
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   double s = 0;
-  for (int k = 0; k < nb; ++k) s += part[(size_t)k * n2 + i];
-  out[i] = (float)s;
+  if (i < n2) {
+    int k = w;
+    for (; k + 24 < nb; k += 32) {
+      const double v0 = part[(size_t)k * n2 + i], v1 = part[(size_t)(k + 8) * n2 + i];
+      const double v2 = part[(size_t)(k + 16) * n2 + i], v3 = part[(size_t)(k + 24) * n2 + i];
+      s += v0; s += v1; s += v2; s += v3;
+    }
+    for (; k < nb; k += 8) s += part[(size_t)k * n2 + i];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && i < n2) {
+    for (int q = 1; q < 8; ++q) s += red[q][lane];
+    out[i] = (float)s;
+  }
 }
 
-// per-channel coefficients into shared memory, then one float4 pass
+// Elementwise passes: per-channel coefficients in shared memory, float4
+// over NHWC with UNR vectors in flight per thread.  The grid stride is a
+// multiple of c/4 whenever NT is (c <= 1024), so a thread's channel group is
+// fixed and no 64-bit modulo runs per element.  amax (nullable): atomicMax of
+// the output's max |v| bits -- the fp16x3 scale word of the conv reading it.
+__device__ __forceinline__ void amax_commit_bn(uint32_t* amax, uint32_t mx) {
+  if (!amax) return;
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(amax, mx);
+}
+
 __global__ void __launch_bounds__(NT)
 apply_kernel(const float* __restrict__ z, const float* __restrict__ stats,
              const float* __restrict__ gb, long long npix, long long ntot, int c, float eps,
-             int relu, float* __restrict__ y) {
+             int relu, float* __restrict__ y, uint32_t* __restrict__ amax) {
   extern __shared__ float coef[];               // scale[c], shift[c]
   for (int i = threadIdx.x; i < c; i += NT) {
     const double m = (double)stats[i] / (double)ntot;
@@ -126,25 +171,40 @@ apply_kernel(const float* __restrict__ z, const float* __restrict__ stats,
   __syncthreads();
   const long long n4 = npix * c / 4;
   const int C4 = c / 4;
-  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n4;
-       e += (long long)gridDim.x * NT) {
-    const int c0 = 4 * (int)(e % C4);
-    const float4 v = reinterpret_cast<const float4*>(z)[e];
-    float r[4] = {v.x, v.y, v.z, v.w};
+  const long long stride = (long long)gridDim.x * NT;
+  const bool fixed = stride % C4 == 0;
+  const long long e0 = blockIdx.x * (long long)NT + threadIdx.x;
+  const int cf = 4 * (int)(e0 % C4);
+  uint32_t mx = 0;
+  for (long long e = e0; e < n4; e += UNR * stride) {
+    float4 v[UNR];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float t = fmaf(r[k], coef[c0 + k], coef[c + c0 + k]);
-      r[k] = relu ? fmaxf(t, 0.f) : t;
+    for (int u = 0; u < UNR; ++u)
+      v[u] = e + u * stride < n4 ? reinterpret_cast<const float4*>(z)[e + u * stride]
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const long long eu = e + u * stride;
+      if (eu >= n4) break;
+      const int c0 = fixed ? cf : 4 * (int)(eu % C4);
+      float r[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float t = fmaf(r[k], coef[c0 + k], coef[c + c0 + k]);
+        r[k] = relu ? fmaxf(t, 0.f) : t;
+        mx = max(mx, __float_as_uint(r[k]) & 0x7fffffffu);
+      }
+      reinterpret_cast<float4*>(y)[eu] = make_float4(r[0], r[1], r[2], r[3]);
     }
-    reinterpret_cast<float4*>(y)[e] = make_float4(r[0], r[1], r[2], r[3]);
   }
+  amax_commit_bn(amax, mx);
 }
 
 __global__ void __launch_bounds__(NT)
 bwd_apply_kernel(const float* __restrict__ g, const float* __restrict__ z,
                  const float* __restrict__ stats, const float* __restrict__ sums,
                  const float* __restrict__ gb, long long npix, long long ntot, int c, float eps,
-                 float* __restrict__ dz) {
+                 float* __restrict__ dz, uint32_t* __restrict__ amax) {
   extern __shared__ float coef[];               // a = gamma*rstd, mu, rstd, t0, t1
   for (int i = threadIdx.x; i < c; i += NT) {
     const double m = (double)stats[i] / (double)ntot;
@@ -159,31 +219,48 @@ bwd_apply_kernel(const float* __restrict__ g, const float* __restrict__ z,
   __syncthreads();
   const long long n4 = npix * c / 4;
   const int C4 = c / 4;
-  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n4;
-       e += (long long)gridDim.x * NT) {
-    const int c0 = 4 * (int)(e % C4);
-    const float4 gv = reinterpret_cast<const float4*>(g)[e];
-    const float4 zv = reinterpret_cast<const float4*>(z)[e];
-    const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, zz[4] = {zv.x, zv.y, zv.z, zv.w};
-    float r[4];
+  const long long stride = (long long)gridDim.x * NT;
+  const bool fixed = stride % C4 == 0;
+  const long long e0 = blockIdx.x * (long long)NT + threadIdx.x;
+  const int cf = 4 * (int)(e0 % C4);
+  uint32_t mx = 0;
+  for (long long e = e0; e < n4; e += UNR * stride) {
+    float4 gv[UNR], zv[UNR];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int ch = c0 + k;
-      const float xh = (zz[k] - coef[c + ch]) * coef[2 * c + ch];
-      r[k] = coef[ch] * (gg[k] - coef[3 * c + ch] - xh * coef[4 * c + ch]);
+    for (int u = 0; u < UNR; ++u) {
+      const bool in = e + u * stride < n4;
+      gv[u] = in ? reinterpret_cast<const float4*>(g)[e + u * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+      zv[u] = in ? reinterpret_cast<const float4*>(z)[e + u * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    reinterpret_cast<float4*>(dz)[e] = make_float4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const long long eu = e + u * stride;
+      if (eu >= n4) break;
+      const int c0 = fixed ? cf : 4 * (int)(eu % C4);
+      const float gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+      const float zz[4] = {zv[u].x, zv[u].y, zv[u].z, zv[u].w};
+      float r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ch = c0 + k;
+        const float xh = (zz[k] - coef[c + ch]) * coef[2 * c + ch];
+        r[k] = coef[ch] * (gg[k] - coef[3 * c + ch] - xh * coef[4 * c + ch]);
+        mx = max(mx, __float_as_uint(r[k]) & 0x7fffffffu);
+      }
+      reinterpret_cast<float4*>(dz)[eu] = make_float4(r[0], r[1], r[2], r[3]);
+    }
   }
+  amax_commit_bn(amax, mx);
 }
 
 inline int rows_in_flight(int c) {
-  const int C4 = c / 4, tpr = C4 < NT ? C4 : NT;
-  return NT / tpr;
+  const int C4 = c / 4, tpr = C4 < NTP ? C4 : NTP;
+  return NTP / tpr;
 }
 
 inline int grid_for(long long n4) {
-  long long g = (n4 + NT - 1) / NT;
-  long long cap = 4LL * num_sms();
+  long long g = (n4 + (long long)NT * UNR - 1) / ((long long)NT * UNR);
+  long long cap = 8LL * num_sms();
   return (int)(g < cap ? (g > 0 ? g : 1) : cap);
 }
 
@@ -202,9 +279,9 @@ bpx_status_t partial(int mode, const float* a, const float* b, const float* stat
     cudaFuncSetAttribute(mode ? k1 : k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr[mode] = sm;
   }
-  if (mode == 0) k0<<<NB, NT, sm, st>>>(a, b, stats, npix, ntot, c, eps, part);
-  else k1<<<NB, NT, sm, st>>>(a, b, stats, npix, ntot, c, eps, part);
-  finish_kernel<<<cdiv(2 * c, 256), 256, 0, st>>>(part, NB, 2 * c, out);
+  if (mode == 0) k0<<<NB, NTP, sm, st>>>(a, b, stats, npix, ntot, c, eps, part);
+  else k1<<<NB, NTP, sm, st>>>(a, b, stats, npix, ntot, c, eps, part);
+  finish_kernel<<<cdiv(2 * c, 32), 256, 0, st>>>(part, NB, 2 * c, out);
   return launch_status(2);
 }
 
@@ -223,19 +300,20 @@ size_t bpx_bn_workspace(long long npix, int c) {
 bpx_status_t bpx_bn_stats(const float* z, long long npix, int c, float* stats, void* ws,
                           size_t ws_bytes, void* stream) {
   BPX_CHECK_ARG(z && stats && npix >= 0 && c > 0 && c % 4 == 0 && c <= 4096 && aligned16(z));
-  BPX_CHECK_ARG(c / 4 <= bn::NT || (c / 4) % bn::NT == 0);
+  BPX_CHECK_ARG(c / 4 <= bn::NTP || (c / 4) % bn::NTP == 0);
   return bn::partial(0, z, nullptr, nullptr, npix, npix, c, 0.f, stats, ws, ws_bytes,
                      as_stream(stream));
 }
 
 bpx_status_t bpx_bn_apply(const float* z, const float* stats, const float* gamma_beta,
                           long long npix, long long ntot, int c, float eps, int relu, float* y,
-                          void* stream) {
+                          unsigned* y_amax, void* stream) {
   BPX_CHECK_ARG(z && stats && gamma_beta && y && c > 0 && c % 4 == 0 && c <= 4096 &&
                 ntot > 0 && aligned16(z) && aligned16(y));
   if (npix == 0) return BPX_OK;
   bn::apply_kernel<<<bn::grid_for(npix * c / 4), bn::NT, 2 * c * sizeof(float),
-                     as_stream(stream)>>>(z, stats, gamma_beta, npix, ntot, c, eps, relu, y);
+                     as_stream(stream)>>>(z, stats, gamma_beta, npix, ntot, c, eps, relu, y,
+                                          y_amax);
   return launch_status();
 }
 
@@ -244,19 +322,20 @@ bpx_status_t bpx_bn_bwd_sums(const float* g, const float* z, const float* stats,
                              size_t ws_bytes, void* stream) {
   BPX_CHECK_ARG(g && z && stats && sums && c > 0 && c % 4 == 0 && c <= 4096 && ntot > 0 &&
                 aligned16(g) && aligned16(z));
-  BPX_CHECK_ARG(c / 4 <= bn::NT || (c / 4) % bn::NT == 0);
+  BPX_CHECK_ARG(c / 4 <= bn::NTP || (c / 4) % bn::NTP == 0);
   return bn::partial(1, g, z, stats, npix, ntot, c, eps, sums, ws, ws_bytes, as_stream(stream));
 }
 
 bpx_status_t bpx_bn_bwd_apply(const float* g, const float* z, const float* stats,
                               const float* sums, const float* gamma_beta, long long npix,
-                              long long ntot, int c, float eps, float* dz, void* stream) {
+                              long long ntot, int c, float eps, float* dz, unsigned* dz_amax,
+                              void* stream) {
   BPX_CHECK_ARG(g && z && stats && sums && gamma_beta && dz && c > 0 && c % 4 == 0 &&
                 c <= 4096 && ntot > 0 && aligned16(g) && aligned16(z) && aligned16(dz));
   if (npix == 0) return BPX_OK;
   bn::bwd_apply_kernel<<<bn::grid_for(npix * c / 4), bn::NT, 5 * c * sizeof(float),
                          as_stream(stream)>>>(g, z, stats, sums, gamma_beta, npix, ntot, c, eps,
-                                              dz);
+                                              dz, dz_amax);
   return launch_status();
 }
 

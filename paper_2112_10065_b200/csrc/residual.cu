@@ -20,6 +20,7 @@
 // dgrad has written dh in place and the skip term is accumulated (acc = 1).
 #include "common.cuh"
 #include "simt_api.h"
+#include "tc_api.h"
 
 namespace bpx {
 namespace {
@@ -51,6 +52,71 @@ __global__ void resadd_fwd_kernel(const float4* __restrict__ a, const float4* __
       v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
     }
     y[e] = relu ? relu4(v) : v;
+  }
+}
+
+// Same-shape joins (f = 1, cs = c: every diamond but the stage transitions)
+// are plain elementwise passes: no per-element index arithmetic, 4 vectors
+// in flight per thread; the forward also reduces max |y| for the fp16x3
+// scale word of the conv that reads y (amax nullable).
+constexpr int UNR = 4;
+__global__ void resadd_flat_kernel(const float4* __restrict__ a, const float4* __restrict__ s,
+                                   float4* __restrict__ y, long long total, int relu,
+                                   uint32_t* __restrict__ amax) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  uint32_t mx = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += UNR * stride) {
+    float4 va[UNR], vs[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const bool in = e + u * stride < total;
+      va[u] = in ? a[e + u * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+      vs[u] = in ? s[e + u * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (e + u * stride >= total) break;
+      float4 v = make_float4(va[u].x + vs[u].x, va[u].y + vs[u].y, va[u].z + vs[u].z,
+                             va[u].w + vs[u].w);
+      if (relu) v = relu4(v);
+      mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                       max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+      y[e + u * stride] = v;
+    }
+  }
+  if (amax) {
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(amax, mx);
+  }
+}
+__global__ void skip_flat_kernel(const float4* __restrict__ dz, const float4* __restrict__ dmain,
+                                 const float4* __restrict__ mask, float4* __restrict__ dh,
+                                 long long total, int acc) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += UNR * stride) {
+    float4 g[UNR], m[UNR], v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const long long q = e + u * stride;
+      const bool in = q < total;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      g[u] = in ? dz[q] : z4;
+      m[u] = in ? mask[q] : z4;
+      v[u] = in && acc ? dh[q] : z4;
+      if (in && dmain) {
+        const float4 d = dmain[q];
+        v[u].x += d.x; v[u].y += d.y; v[u].z += d.z; v[u].w += d.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (e + u * stride >= total) break;
+      v[u].x += m[u].x > 0.f ? g[u].x : 0.f; v[u].y += m[u].y > 0.f ? g[u].y : 0.f;
+      v[u].z += m[u].z > 0.f ? g[u].z : 0.f; v[u].w += m[u].w > 0.f ? g[u].w : 0.f;
+      dh[e + u * stride] = v[u];
+    }
   }
 }
 
@@ -166,15 +232,26 @@ using namespace bpx;
 extern "C" {
 
 bpx_status_t bpx_residual_add_fwd(const float* a, const float* s, float* y, int n, int h,
-                                  int w_, int c, int cs, int down, int relu, void* stream) {
+                                  int w_, int c, int cs, int down, int relu, unsigned* y_amax,
+                                  void* stream) {
   BPX_CHECK_ARG(n >= 0 && h >= 0 && w_ >= 0 && c % 4 == 0 && cs % 4 == 0);
   BPX_CHECK_ARG(cs > 0 && cs <= c && (down == 0 || down == 1));
   const long long total = (long long)n * h * w_ * (c / 4);
   if (total == 0) return BPX_OK;
   BPX_CHECK_ARG(a && s && y && aligned16(a) && aligned16(s) && aligned16(y));
+  if (!down && cs == c) {
+    resadd_flat_kernel<<<grid_for(cdivll(total, UNR)), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(s),
+        reinterpret_cast<float4*>(y), total, relu, y_amax);
+    return launch_status();
+  }
   resadd_fwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(s),
       reinterpret_cast<float4*>(y), total, h, w_, c / 4, cs / 4, down ? 2 : 1, relu);
+  if (y_amax) {         // the transition joins: one reduction over y
+    absmax_into(y, (size_t)total * 4, y_amax, as_stream(stream));
+    return launch_status(2);
+  }
   return launch_status();
 }
 
@@ -189,6 +266,13 @@ bpx_status_t bpx_residual_skip_bwd(const float* dz, const float* dmain, const fl
   if (total == 0) return BPX_OK;
   BPX_CHECK_ARG(dz && mask && dh && aligned16(dz) && aligned16(mask) && aligned16(dh) &&
                 aligned16(dmain));
+  if (!down && cs == c) {
+    skip_flat_kernel<<<grid_for(cdivll(total, UNR)), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4*>(dz), reinterpret_cast<const float4*>(dmain),
+        reinterpret_cast<const float4*>(mask), reinterpret_cast<float4*>(dh), total,
+        accumulate);
+    return launch_status();
+  }
   skip_bwd_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(dz), reinterpret_cast<const float4*>(dmain),
       reinterpret_cast<const float4*>(mask), reinterpret_cast<float4*>(dh), total, h * f,

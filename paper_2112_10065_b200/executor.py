@@ -60,6 +60,7 @@ class _Layer:
     x_fused: bool = False                  # amax[0] written by the producer of x
     dz_fused: bool = False                 # amax[4] written by the writer of dy
     y_amax: Optional[torch.Tensor] = None  # word this layer's fwd kernel max-reduces y into
+    bn_y_amax: Optional[torch.Tensor] = None  # BN conv: word its normalise pass reduces y into
     dx_amax: Optional[torch.Tensor] = None  # word this layer's bwd kernel reduces dx into
     src_i: int = -1                        # input layer (-1: the network input / concat)
     srcs_i: tuple = ()                     # concat: joined layers
@@ -421,7 +422,8 @@ class BurstStep:
         L = self.layers[i]
         self.k.bn_stats(L.z, L.bnf, ws=self.ws)
         self._bn_allreduce(i, "bnf", L.bnf)
-        self.k.bn_apply(L.z, L.bnf, L.bias, self._bn_ntot(L), L.y, L.spec.relu)
+        kw = {"y_amax": L.bn_y_amax} if L.bn_y_amax is not None else {}
+        self.k.bn_apply(L.z, L.bnf, L.bias, self._bn_ntot(L), L.y, L.spec.relu, **kw)
 
     def _bn_bwd(self, i: int) -> torch.Tensor:
         """dy -> dz.  The local sums are the layer's [dbeta ; dgamma] (summed
@@ -434,15 +436,18 @@ class BurstStep:
             L.bnb.copy_(L.dbias)
             self._bn_allreduce(i, "bnb", L.bnb)
             sums = L.bnb
-        self.k.bn_bwd_apply(L.dy, L.z, L.bnf, sums, L.bias, self._bn_ntot(L), L.dz)
+        kw = {"dz_amax": L.amax[4:5]} if L.amax is not None and L.dz_fused else {}
+        self.k.bn_bwd_apply(L.dy, L.z, L.bnf, sums, L.bias, self._bn_ntot(L), L.dz, **kw)
         return L.dz
 
     def _fuse_amax(self, consumers) -> None:
         """Fuse each conv's fp16x3 scale words into the kernels that write its
         operands where that kernel writes the operand buffer itself: x from
         a conv forward (fdt / c1 epilogue) or a 2x2 max pool on the same g
-        (a chain edge, no reshard), dz from the dgrad of its only consumer
-        (a conv or a pool) on the same g.  Every other operand gets one
+        (a chain edge, no reshard), a residual join or a BN conv's normalise
+        pass, dz from the dgrad of its only consumer (a conv or a pool) on
+        the same g or, for a BN conv, from its own BN backward.  Every other
+        operand gets one
         bpx_absmax launch.  The words are zeroed with the weights' split after
         each update (one memset), or by the first active layer's forward when
         no update preceded it."""
@@ -451,16 +456,23 @@ class BurstStep:
             return
         for i, L in enumerate(self.layers):
             sp = L.spec
-            if L.amax is None or sp.bn or sp.down:
+            if L.amax is None or sp.down:
                 continue
+            if sp.bn:
+                L.dz_fused = True     # its own BN backward (bn_bwd_apply) writes dz
             if L.src_i < 0 and sp.kind == "conv" and sp.cin == 3 and sp.cout == 64:
                 L.x_fused = True      # the first-conv engine (c1) reduces x as it reads it
             if L.src_i >= 0 and not L.reshard_in and self.layers[L.src_i].g == L.g:
                 S = self.layers[L.src_i]
-                if ((S.spec.kind == "conv" and not S.spec.bn) or
+                if S.spec.kind == "conv" and S.spec.bn and S.active:
+                    S.bn_y_amax = L.amax[0:1]      # the BN normalise pass writes x
+                    L.x_fused = True
+                elif ((S.spec.kind == "conv" and not S.spec.bn) or S.spec.kind == "add" or
                         (S.spec.kind == "pool" and S.idx is not None)):
                     S.y_amax = L.amax[0:1]
                     L.x_fused = True
+            if sp.bn:
+                continue              # consumers' data gradients are not its dz
             cons = consumers[i]
             if len(cons) == 1:
                 C = self.layers[cons[0]]
@@ -538,7 +550,7 @@ class BurstStep:
             self.k.conv3x3_fwd(L.x, L.w, L.bias, L.y, relu=sp.relu, ws=self.ws, **lo,
                                **self._xa(L, L.x), **self._ya(L))
         elif sp.kind == "add":
-            self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu)
+            self.k.residual_add_fwd(L.x, L.s, L.y, relu=sp.relu, **self._ya(L))
         elif sp.kind == "gap":
             self.k.global_avgpool_fwd(L.x, L.y)
         elif sp.kind == "pool":

@@ -69,7 +69,7 @@ _SIGS = {
     "bpx_maxpool2x2_bwd_idx": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 4
                                + [ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_residual_add_fwd": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_int] * 7
-                             + [ctypes.c_void_p]),
+                             + [ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_residual_skip_bwd": (ctypes.c_int, [_c_float_p] * 4 + [ctypes.c_int] * 7
                               + [ctypes.c_void_p]),
     "bpx_subsample2_fwd": (ctypes.c_int, [_c_float_p] * 2 + [ctypes.c_int] * 4
@@ -100,12 +100,13 @@ _SIGS = {
                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_bn_apply": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_longlong] * 2
                      + [ctypes.c_int, ctypes.c_float, ctypes.c_int, _c_float_p,
-                        ctypes.c_void_p]),
+                        ctypes.c_void_p, ctypes.c_void_p]),
     "bpx_bn_bwd_sums": (ctypes.c_int, [_c_float_p] * 3 + [ctypes.c_longlong] * 2
                         + [ctypes.c_int, ctypes.c_float, _c_float_p, ctypes.c_void_p,
                            ctypes.c_size_t, ctypes.c_void_p]),
     "bpx_bn_bwd_apply": (ctypes.c_int, [_c_float_p] * 5 + [ctypes.c_longlong] * 2
-                         + [ctypes.c_int, ctypes.c_float, _c_float_p, ctypes.c_void_p]),
+                         + [ctypes.c_int, ctypes.c_float, _c_float_p, ctypes.c_void_p,
+                            ctypes.c_void_p]),
     "bpx_sgd_update": (ctypes.c_int, [_c_float_p, _c_float_p, ctypes.c_size_t,
                                       ctypes.c_float, ctypes.c_void_p]),
     "bpx_reshard_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p,
@@ -461,16 +462,18 @@ def maxpool2x2_bwd(x, dy, dx):
     return dx
 
 
-def residual_add_fwd(a, s, y, relu=True):
+def residual_add_fwd(a, s, y, relu=True, y_amax=None):
     """y = relu(a + P(s)): the join of a residual diamond; ``s`` may have
-    fewer channels (zero-padded) and twice the spatial size (subsampled)."""
+    fewer channels (zero-padded) and twice the spatial size (subsampled).
+    ``y_amax`` (int32 word, optional): atomicMax'ed with max |y| bits."""
     lib = load_library()
     _f32(a, s, y)
     n, h, w, c = a.shape
     cs = s.shape[3]
     down = 1 if s.shape[1] == 2 * h and h > 0 else 0
     _check(lib.bpx_residual_add_fwd(_ptr(a), _ptr(s), _ptr(y), n, h, w, c, cs, down,
-                                    int(relu), _stream()), "bpx_residual_add_fwd")
+                                    int(relu), _ptr(y_amax), _stream()),
+           "bpx_residual_add_fwd")
     return y
 
 
@@ -651,12 +654,14 @@ def bn_stats(z, stats, ws: Optional[Workspace] = None):
     _check(lib.bpx_bn_stats(_ptr(z), npix, c, _ptr(stats), wp, wb, _stream()), "bpx_bn_stats")
 
 
-def bn_apply(z, stats, gamma_beta, ntot, y, relu, eps=BN_EPS):
+def bn_apply(z, stats, gamma_beta, ntot, y, relu, eps=BN_EPS, y_amax=None):
+    """y_amax (int32 word, optional): atomicMax'ed with max |y| bits."""
     lib = load_library()
     _f32(z, stats, gamma_beta, y)
     npix, c = _npc(z)
     _check(lib.bpx_bn_apply(_ptr(z), _ptr(stats), _ptr(gamma_beta), npix, int(ntot), c,
-                            float(eps), int(relu), _ptr(y), _stream()), "bpx_bn_apply")
+                            float(eps), int(relu), _ptr(y), _ptr(y_amax), _stream()),
+           "bpx_bn_apply")
 
 
 def bn_bwd_sums(g, z, stats, ntot, sums, ws: Optional[Workspace] = None, eps=BN_EPS):
@@ -668,12 +673,14 @@ def bn_bwd_sums(g, z, stats, ntot, sums, ws: Optional[Workspace] = None, eps=BN_
                                _ptr(sums), wp, wb, _stream()), "bpx_bn_bwd_sums")
 
 
-def bn_bwd_apply(g, z, stats, sums, gamma_beta, ntot, dz, eps=BN_EPS):
+def bn_bwd_apply(g, z, stats, sums, gamma_beta, ntot, dz, eps=BN_EPS, dz_amax=None):
+    """dz_amax (int32 word, optional): atomicMax'ed with max |dz| bits."""
     lib = load_library()
     _f32(g, z, stats, sums, gamma_beta, dz)
     npix, c = _npc(z)
     _check(lib.bpx_bn_bwd_apply(_ptr(g), _ptr(z), _ptr(stats), _ptr(sums), _ptr(gamma_beta),
-                                npix, int(ntot), c, float(eps), _ptr(dz), _stream()),
+                                npix, int(ntot), c, float(eps), _ptr(dz), _ptr(dz_amax),
+                                _stream()),
            "bpx_bn_bwd_apply")
 
 
