@@ -20,7 +20,7 @@ def step(path):
             continue
         v = float(d['Metric Value'].replace(',', ''))
         u = d['Metric Unit']
-        us = v / 1000 if u == 'nsecond' else v if u == 'usecond' else v * 1000
+        us = v / 1000 if u in ('ns', 'nsecond') else v if u in ('us', 'usecond') else v * 1000
         seq.append((d['Kernel Name'].split('(')[0].replace('void ', '')[:60], us))
     idx = [i for i, (k, _) in enumerate(seq) if 'sgd_kernel' in k]
     a, b = idx[-2], idx[-1]
