@@ -451,6 +451,33 @@ def test_producers_reduce_amax():
     ops.maxpool2x2_bwd_idx(idx, dy, dx, dx_amax=da)
     torch.cuda.synchronize()
     assert int(ya[0]) == word(y) and int(da[0]) == word(dx)
+    # the residual nets' producers: BN normalise / BN backward, residual join
+    # (same-shape flat path and the stride-2 transition), first conv's x
+    c = 128
+    zt = rnd(2, 10, 10, c, seed=39, scale=2.0).to(DEV)
+    gt = rnd(2, 10, 10, c, seed=40).to(DEV)
+    gb = torch.cat([torch.zeros(c), torch.ones(c)]).to(DEV)
+    st = torch.empty(2 * c, device=DEV)
+    ops.bn_stats(zt, st)
+    yb, ya = torch.empty_like(zt), z()
+    ops.bn_apply(zt, st, gb, 200, yb, relu=True, y_amax=ya)
+    sums, dzb, da = torch.empty(2 * c, device=DEV), torch.empty_like(zt), z()
+    ops.bn_bwd_sums(gt, zt, st, 200, sums)
+    ops.bn_bwd_apply(gt, zt, st, sums, gb, 200, dzb, dz_amax=da)
+    torch.cuda.synchronize()
+    assert int(ya[0]) == word(yb) and int(da[0]) == word(dzb)
+    for s_shape in ((2, 10, 10, c), (2, 20, 20, 64)):
+        sk = rnd(*s_shape, seed=41).to(DEV)
+        yr, ra = torch.empty_like(zt), z()
+        ops.residual_add_fwd(zt, sk, yr, relu=True, y_amax=ra)
+        torch.cuda.synchronize()
+        assert int(ra[0]) == word(yr), s_shape
+    xi = rnd(2, 16, 16, 3, seed=42).to(DEV)
+    wi = rnd(64, 3, 3, 3, seed=43, scale=0.1).to(DEV)
+    yi, xa = torch.empty(2, 16, 16, 64, device=DEV), z()
+    ops.conv3x3_fwd(xi, wi, torch.zeros(64, device=DEV), yi, relu=True, x_amax=xa)
+    torch.cuda.synchronize()
+    assert ops.last_engine() == "c1" and int(xa[0]) == word(xi)
 
 
 @pytest.mark.parametrize("shape", [(2, 80, 64, 64), (1, 224, 64, 64)], ids=str)
