@@ -65,7 +65,8 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []               # (arrival time, line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -75,16 +76,24 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first
+            # sample so a short timed region is still covered
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
+        self.t1 = time.time()
         if self.proc is not None:
+            time.sleep(0.15)          # the sample that closes the region
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -94,7 +103,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        t1 = (self.t1 or time.time()) + 0.15
+        for ts, ln in self.lines:
+            if self.t0 is not None and not (self.t0 <= ts <= t1):
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
