@@ -313,29 +313,35 @@ __device__ __forceinline__ void commit_amax(uint32_t* amax, uint32_t mx) {
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(amax, mx);
 }
 
+// A block walks whole output rows (b, yo); within a row, thread j takes
+// (xo, channel group) = (j / c4, j % c4) in 32-bit arithmetic -- a flat
+// 64-bit index decomposed per element (three 64-bit div/mods) had made the
+// pools issue-bound.
 __global__ void maxpool_fwd_idx_kernel(const float4* __restrict__ x, float4* __restrict__ y,
                                        uchar4* __restrict__ idx, int n, int h, int w, int c4,
                                        uint32_t* amax) {
-  const int oh = h / 2, ow = w / 2;
-  const long long total = (long long)n * oh * ow * c4;
+  const int oh = h / 2, ow = w / 2, per = ow * c4;
+  const long long rs = (long long)w * c4;
   uint32_t mx = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    int c = (int)(i % c4); long long p = i / c4;
-    int xo = (int)(p % ow); p /= ow;
-    int yo = (int)(p % oh); int b = (int)(p / oh);
-    const float4* base = x + (((long long)b * h + 2 * yo) * w + 2 * xo) * c4 + c;
-    const long long rs = (long long)w * c4;
-    const float4 a = base[0], bb = base[c4], cc = base[rs], d = base[rs + c4];
-    float4 r;
-    uchar4 k;
-    k.x = argmax4(a.x, bb.x, cc.x, d.x, r.x);
-    k.y = argmax4(a.y, bb.y, cc.y, d.y, r.y);
-    k.z = argmax4(a.z, bb.z, cc.z, d.z, r.z);
-    k.w = argmax4(a.w, bb.w, cc.w, d.w, r.w);
-    y[i] = r;
-    idx[i] = k;
-    mx = max(mx, abs4(r));
+  for (int row = blockIdx.x; row < n * oh; row += gridDim.x) {
+    const int b = row / oh, yo = row - b * oh;
+    const float4* xr = x + ((long long)b * h + 2 * yo) * rs;
+    float4* yr = y + (long long)row * per;
+    uchar4* ir = idx + (long long)row * per;
+    for (int j = threadIdx.x; j < per; j += blockDim.x) {
+      const int xo = j / c4, c = j - xo * c4;
+      const float4* base = xr + 2 * xo * c4 + c;
+      const float4 a = base[0], bb = base[c4], cc = base[rs], d = base[rs + c4];
+      float4 r;
+      uchar4 k;
+      k.x = argmax4(a.x, bb.x, cc.x, d.x, r.x);
+      k.y = argmax4(a.y, bb.y, cc.y, d.y, r.y);
+      k.z = argmax4(a.z, bb.z, cc.z, d.z, r.z);
+      k.w = argmax4(a.w, bb.w, cc.w, d.w, r.w);
+      yr[j] = r;
+      ir[j] = k;
+      mx = max(mx, abs4(r));
+    }
   }
   commit_amax(amax, mx);
 }
@@ -343,30 +349,37 @@ __global__ void maxpool_fwd_idx_kernel(const float4* __restrict__ x, float4* __r
 __global__ void maxpool_bwd_idx_kernel(const uchar4* __restrict__ idx,
                                        const float4* __restrict__ dy, float4* __restrict__ dx,
                                        int n, int h, int w, int c4, uint32_t* amax) {
-  const int oh = h / 2, ow = w / 2;
-  const long long total = (long long)n * oh * ow * c4;
+  const int oh = h / 2, ow = w / 2, per = ow * c4;
+  const long long rs = (long long)w * c4;
   uint32_t mx = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    int c = (int)(i % c4); long long p = i / c4;
-    int xo = (int)(p % ow); p /= ow;
-    int yo = (int)(p % oh); int b = (int)(p / oh);
-    const long long o = (((long long)b * h + 2 * yo) * w + 2 * xo) * c4 + c;
-    const long long rs = (long long)w * c4;
-    const uchar4 k = idx[i];
-    const float4 g = dy[i];
-    float4 r[4];
+  for (int row = blockIdx.x; row < n * oh; row += gridDim.x) {
+    const int b = row / oh, yo = row - b * oh;
+    float4* xr = dx + ((long long)b * h + 2 * yo) * rs;
+    const float4* gr = dy + (long long)row * per;
+    const uchar4* ir = idx + (long long)row * per;
+    for (int j = threadIdx.x; j < per; j += blockDim.x) {
+      const int xo = j / c4, c = j - xo * c4;
+      const long long o = 2 * xo * c4 + c;
+      const uchar4 k = ir[j];
+      const float4 g = gr[j];
+      float4 r[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      r[j].x = k.x == j ? g.x : 0.f;
-      r[j].y = k.y == j ? g.y : 0.f;
-      r[j].z = k.z == j ? g.z : 0.f;
-      r[j].w = k.w == j ? g.w : 0.f;
+      for (int q = 0; q < 4; ++q) {
+        r[q].x = k.x == q ? g.x : 0.f;
+        r[q].y = k.y == q ? g.y : 0.f;
+        r[q].z = k.z == q ? g.z : 0.f;
+        r[q].w = k.w == q ? g.w : 0.f;
+      }
+      xr[o] = r[0]; xr[o + c4] = r[1]; xr[o + rs] = r[2]; xr[o + rs + c4] = r[3];
+      mx = max(mx, max(max(abs4(r[0]), abs4(r[1])), max(abs4(r[2]), abs4(r[3]))));
     }
-    dx[o] = r[0]; dx[o + c4] = r[1]; dx[o + rs] = r[2]; dx[o + rs + c4] = r[3];
-    mx = max(mx, max(max(abs4(r[0]), abs4(r[1])), max(abs4(r[2]), abs4(r[3]))));
   }
   commit_amax(amax, mx);
+}
+
+static int pool_grid(int rows) {          // blocks walk output rows
+  const int cap = 8 * num_sms();
+  return rows < 1 ? 1 : (rows > cap ? cap : rows);
 }
 
 static int ew_grid(long long work) {
@@ -520,7 +533,7 @@ bpx_status_t bpx_maxpool2x2_fwd_idx(const float* x, float* y, uint8_t* idx, int 
   BPX_CHECK_ARG(aligned16(x) && aligned16(y) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
   long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
   if (total == 0) return BPX_OK;
-  maxpool_fwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
+  maxpool_fwd_idx_kernel<<<pool_grid(n * (h / 2)), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
       reinterpret_cast<uchar4*>(idx), n, h, w_, c / 4, y_amax);
   return launch_status();
@@ -532,7 +545,7 @@ bpx_status_t bpx_maxpool2x2_bwd_idx(const uint8_t* idx, const float* dy, float* 
   BPX_CHECK_ARG(aligned16(dy) && aligned16(dx) && (reinterpret_cast<uintptr_t>(idx) & 3) == 0);
   long long total = (long long)n * (h / 2) * (w_ / 2) * (c / 4);
   if (total == 0) return BPX_OK;
-  maxpool_bwd_idx_kernel<<<ew_grid(total), 256, 0, as_stream(stream)>>>(
+  maxpool_bwd_idx_kernel<<<pool_grid(n * (h / 2)), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const uchar4*>(idx), reinterpret_cast<const float4*>(dy),
       reinterpret_cast<float4*>(dx), n, h, w_, c / 4, dx_amax);
   return launch_status();
