@@ -648,11 +648,18 @@ template <class EPI>
 __global__ void fdt_finish(const float* __restrict__ part, int ksplit, long long npix, int N,
                            EPI epi) {
   const long long groups = npix * (N / 8);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // stride a multiple of N/8 (N a power of two <= 512): a thread keeps its
+  // channel group and steps whole pixels -- no 64-bit div/mod per element
+  const bool fixed = stride % (N / 8) == 0;
+  const long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int nf = (int)(e0 % (N / 8)) * 8;
+  const long long pstep = stride / (N / 8);
   uint32_t mx = 0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < groups;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long p = e / (N / 8);
-    const int n0 = (int)(e % (N / 8)) * 8;
+  long long pf = e0 / (N / 8);
+  for (long long e = e0; e < groups; e += stride, pf += pstep) {
+    const long long p = fixed ? pf : e / (N / 8);
+    const int n0 = fixed ? nf : (int)(e % (N / 8)) * 8;
     float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int k = 0; k < ksplit; ++k) {
       const float4* src = reinterpret_cast<const float4*>(part + ((long long)k * npix + p) * N + n0);
