@@ -268,6 +268,12 @@ inline bool encode2d(CUtensorMap* m, const float* p, long long inner, long long 
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef DTC_DGW
+#define DTC_DGW 2          // dgrad: waves of CTA slots
+#endif
+#ifndef DTC_MINST
+#define DTC_MINST 8        // stages per split, at least (4: fc2 dgrad 0.028 vs 0.025 ms)
+#endif
 inline int nb_for(int batch) { return batch <= 16 ? 16 : 32; }   // M=128 MMAs take N % 16 == 0
 
 // split count: one wave of CTA slots (CPS per SM) for the forward, two for the data gradient
@@ -277,8 +283,8 @@ inline void geometry(int M, int K, bool dg, int& splits, int& kslice) {
   const int mt = cdiv(M, 128);
   const int kst = cdiv(K, BK);
   const int slots = CPS * num_sms();
-  int want = dg ? cdiv(2 * slots, mt) : slots / mt;
-  if (want > kst / 4) want = kst / 4;
+  int want = dg ? cdiv(DTC_DGW * slots, mt) : slots / mt;
+  if (want > kst / DTC_MINST) want = kst / DTC_MINST;
   if (want < 1) want = 1;
   kslice = cdiv(kst, want) * BK;
   splits = cdiv(K, kslice);
