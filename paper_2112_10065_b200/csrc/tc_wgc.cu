@@ -54,6 +54,12 @@ static_assert(SMEM <= 227 * 1024, "smem budget");
 #define WGC_PB 8                              // blocks per promotion chunk (K = 512)
 #endif
 constexpr int PB = WGC_PB;
+// ALT: the two A-converter warps of a lane quadrant take alternate A slots
+// (all four pixel rows each) instead of two rows of every slot, so one
+// warp's conversion overlaps the other's wait::st and hand-off (as in fdt)
+#ifndef WGC_ALT
+#define WGC_ALT 1
+#endif
 
 struct Geo {
   int H, W;
@@ -95,7 +101,7 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       mbar_init(&sempty[s], 1 + NCA);      // MMA commit + the A converter warps
     }
     for (int a = 0; a < SA; ++a) {
-      mbar_init(&aready[a], NCA);
+      mbar_init(&aready[a], WGC_ALT ? NCA / 2 : NCA);   // the warps that wrote the slot
       mbar_init(&aempty[a], 1);
     }
     for (int k = 0; k < MT; ++k) {
@@ -179,6 +185,9 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       for (int k = 0; k < MT; ++k, ++ai) {
         const int sa = ai % SA;
         const int gc = 4 * k + q;
+#if WGC_ALT
+        if ((ai & 1) != ph) continue;            // the quadrant's other warp takes this slot
+#endif
         if (ai >= SA) mbar_wait(&aempty[sa], ((ai / SA) - 1) & 1);
         tc_fence_after();
 #ifdef WGC_NOCONV
@@ -190,8 +199,8 @@ wgc_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
           const char* hb = st + (gc & 1) * XH;
           const uint32_t a = lanebase + sa * A_STAGE;
 #pragma unroll
-          for (int pp = 0; pp < BH / 2; ++pp) {    // one 16-pixel block row = 8 columns
-            const int py = 2 * ph + pp;
+          for (int pp = 0; pp < (WGC_ALT ? BH : BH / 2); ++pp) {   // a 16-pixel row = 8 columns
+            const int py = WGC_ALT ? pp : 2 * ph + pp;
             uint32_t hi[8], lo[8];
 #pragma unroll
             for (int k2 = 0; k2 < 8; ++k2) {
