@@ -53,6 +53,16 @@ constexpr int PCH = 128 / BK;                   // stages per promotion chunk (K
 #ifndef WGH_SSA
 #define WGH_SSA 0
 #endif
+// ALT (CTA pairs): warps 2-9 are one pool of converters in two groups of
+// four taking alternate stages, each warp doing one lane quadrant's x
+// conversion and a quarter of its CTA's dz half, so one group's stage
+// overlaps the other's hand-off (as the fwd/dgrad engine's converters do).
+// B200 same-box: paired layers 3-6 % faster (conv3_2 0.372 -> 0.360 ms,
+// conv4_2 0.382 -> 0.363); unpaired ones, whose warps would also split a
+// whole 128-channel dz tile, 5-10 % slower -- so pairs only
+#ifndef WGH_ALT
+#define WGH_ALT 1
+#endif
 
 // PAIR (BN = 128): a cluster of two CTAs (M tiles 2m, 2m+1, same N tile and
 // pixel split) runs one M = 256 MMA (cta_group::2); each CTA loads and splits
@@ -70,7 +80,7 @@ struct Cfg {
   static constexpr int ACC = 2 * BN;                      // two chunk buffers
   static constexpr int A_COL = ACC;                       // + S stages of (hi | lo)
   static constexpr int A_STAGE = BK;                      // 32 hi + 32 lo columns
-  static constexpr int BIAS = 128 * 16 * 4;               // B converters' bias partials
+  static constexpr int BIAS = 256 * 16 * 4;               // converters' bias partials
   static constexpr int SMEM = 1024 + S * STAGE + 512 + BIAS;
   static_assert(ACC + S * A_STAGE <= 512, "TMEM budget");
   static_assert(SMEM <= 227 * 1024, "smem budget");
@@ -121,7 +131,7 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], PAIR ? 16 : 8);    // one arrival per converter warp
+      mbar_init(&ready[s], (PAIR ? 16 : 8) / (WGH_ALT && !SSA && PAIR ? 2 : 1));   // per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -230,6 +240,136 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
       } else {
         tc_commit_elect(&empty[s]);
         if (i % PCH == PCH - 1 || i == nst - 1) tc_commit_elect(&hfull[b]);
+      }
+    }
+  } else if (warp < DR0 && WGH_ALT && !SSA && PAIR) {
+    // ------------------------------------------------------------ converters (ALT)
+    // warps 2-9 in two groups of four taking alternate stages; in its stage a
+    // warp converts A for lane quadrant q (as the A converters below) AND
+    // splits dz rows share q in place (as the B converters below), so one
+    // group's work on stage i + 1 overlaps the other's hand-off of stage i
+    const int cw = warp - CA0, grp = cw >> 2, q = cw & 3;
+    // --- A (x^T) for lane quadrant q
+    const bool valid = (m0 / 32 + q) < chunks;
+    const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
+    const int gc = m0 / 32 + q, tap = valid ? gc / cpt : 4;
+    const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+    const float scx = exp2i(sx);
+    const int cofs = ((lane >> 2) << 4) + (lane & 3) * 4;
+    long long p = (long long)t0 * BK + lane;
+    int img = (int)(p / ((long long)g.H * g.W));
+    int rem = (int)(p - (long long)img * g.H * g.W);
+    int oh = rem / g.W, ow = rem - (rem / g.W) * g.W;
+    // --- B (dz) rows share q
+    const int c16 = lane >> 3;
+    const int at = BNL == 128 ? (q & 1) : 0;
+    constexpr int PPW = BNL == 128 ? 32 : 16;
+    const int pb = (BNL == 128 ? (q >> 1) : q) * PPW;
+    const float scd = exp2i(sd);
+    const bool do_bias = bias_part != nullptr && blockIdx.x == (PAIR ? rank : 0u);
+    float bs[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) bs[k] = 0.f;
+    for (int i = 0; i < nst; ++i) {
+      const int s = i % S;
+      uint32_t vmask[BK / 32];
+#pragma unroll
+      for (int h = 0; h < BK / 32; ++h) {      // every stage: the coordinates advance
+        const bool ok = valid && p < g.npix && (unsigned)(oh + dy) < (unsigned)g.H &&
+                        (unsigned)(ow + dx) < (unsigned)g.W;
+        vmask[h] = __ballot_sync(0xffffffffu, ok);
+        p += 32;
+        ow += 32;
+        while (ow >= g.W) {
+          ow -= g.W;
+          if (++oh == g.H) { oh = 0; ++img; }
+        }
+      }
+      if ((i & 1) != grp) continue;
+      mbar_wait(&full[s], (i / S) & 1);
+      tc_fence_after();
+      char* st = smem + s * Cf::STAGE;
+#if !defined(WGH_NOCONV) && !defined(WGH_NOACONV)
+      {
+        const char* box = st + q * BOX;
+        const uint32_t a = lanebase + s * Cf::A_STAGE;
+#pragma unroll
+        for (int ps = 0; ps < BK / 16; ++ps) {
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            float v[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int kk = 16 * ps + 2 * k + e;
+              v[e] = ((vmask[kk >> 5] >> (kk & 31)) & 1u)
+                         ? *reinterpret_cast<const float*>(box + kk * 128 + (cofs ^ ((kk & 7) << 4)))
+                         : 0.f;
+            }
+            split_f16x2_s(v[0], v[1], scx, hi[k], lo[k]);
+          }
+          tmem_st8u(a + 8 * ps, hi);
+          tmem_st8u(a + BK / 2 + 8 * ps, lo);
+        }
+      }
+#endif
+#ifndef WGH_NOCONV
+      {
+        char* bt = st + Cf::A_BYTES;
+        char* raw = bt + (2 * at + (c16 >> 1)) * BOX;
+        char* hrow = bt + 2 * at * BOX, *lrow = hrow + BOX;
+#pragma unroll
+        for (int it = 0; it < PPW / 8; ++it) {
+          const int pr = pb + 8 * it + (lane & 7);
+          const int sw = pr & 7;
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = *reinterpret_cast<const float4*>(raw + pr * 128 + (((4 * (c16 & 1) + u) ^ sw) << 4));
+          __syncwarp();
+          uint32_t h[8], l[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            split_f16x2_s(v[u].x, v[u].y, scd, h[2 * u], l[2 * u]);
+            split_f16x2_s(v[u].z, v[u].w, scd, h[2 * u + 1], l[2 * u + 1]);
+            if (do_bias) {
+              bs[4 * u] += v[u].x; bs[4 * u + 1] += v[u].y;
+              bs[4 * u + 2] += v[u].z; bs[4 * u + 3] += v[u].w;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int off = pr * 128 + (((2 * c16 + e) ^ sw) << 4);
+            *reinterpret_cast<uint4*>(hrow + off) = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
+            *reinterpret_cast<uint4*>(lrow + off) = make_uint4(l[4 * e], l[4 * e + 1], l[4 * e + 2], l[4 * e + 3]);
+          }
+        }
+      }
+#endif
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      fence_proxy_async();                // generic-proxy writes -> the MMA's async reads
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_remote(ready_l + 8u * s); else mbar_arrive(&ready[s]);
+      }
+    }
+    if (do_bias) {
+      // fixed-order reduction of the per-thread partials of both groups
+      const int bt = tid - CA0 * 32;                        // 0 .. 255
+#pragma unroll
+      for (int k = 0; k < 16; ++k) bias_scr[bt * 16 + k] = bs[k];
+      named_sync(1, 256);
+      if (bt < BNL) {
+        const int a = bt / 64, cc = (bt % 64) / 16, k = bt % 16;
+        float t = 0.f;
+        for (int gg = 0; gg < 2; ++gg)
+          for (int w = 0; w < 4; ++w) {
+            if (BNL == 128 && (w & 1) != a) continue;
+            for (int l8 = 0; l8 < 8; ++l8)
+              t += bias_scr[((gg * 4 + w) * 32 + cc * 8 + l8) * 16 + k];
+          }
+        bias_part[(long long)blockIdx.z * g.Cout + nl0 + bt] = t;
       }
     }
   } else if (warp < CB0 && SSA) {
