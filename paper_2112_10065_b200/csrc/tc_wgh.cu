@@ -248,7 +248,8 @@ wgh_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUten
     // warp converts A for lane quadrant q (as the A converters below) AND
     // splits dz rows share q in place (as the B converters below), so one
     // group's work on stage i + 1 overlaps the other's hand-off of stage i
-    const int cw = warp - CA0, grp = cw >> 2, q = cw & 3;
+    // (q = warp % 4: a warp reaches only its own TMEM lane quadrant)
+    const int cw = warp - CA0, grp = cw >> 2, q = warp & 3;
     // --- A (x^T) for lane quadrant q
     const bool valid = (m0 / 32 + q) < chunks;
     const uint32_t lanebase = tmem + ((uint32_t)(q * 32) << 16) + Cf::A_COL;
