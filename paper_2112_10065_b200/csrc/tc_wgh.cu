@@ -628,14 +628,17 @@ inline int bn_for(int cout) { return cout % 128 == 0 ? 128 : 64; }
 #define WGH_PAIR 1
 #endif
 #ifndef WGH_PAIR_PAD
-#define WGH_PAIR_PAD 0
+#define WGH_PAIR_PAD 9
 #endif
-// pairs for 128-wide N tiles whose M tiles pair up (Cin = 256, 512); with
-// WGH_PAIR_PAD=1 an odd count gets a padding tile (A rows zero, nothing
-// stored) -- measured equal (Cin = 128) or 5 % slower (Cin = 64), so off
+// pairs for 128-wide N tiles whose M tiles pair up (Cin = 256, 512), and for
+// odd counts of at least WGH_PAIR_PAD tiles with a padding tile (A rows
+// zero, nothing stored): with the alternating converter groups of pairs,
+// Cin = 128 (9 -> 10 tiles) gains 2-3 % (conv2_2 0.418 -> 0.411 ms, conv3_1
+// 0.217 -> 0.210), Cin = 64 (5 -> 6) loses 4 %
 inline bool paired(int cin, int cout) {
   const int mt = cdiv(9 * cin, 128);
-  return WGH_PAIR && bn_for(cout) == 128 && mt >= 2 && (WGH_PAIR_PAD || mt % 2 == 0);
+  return WGH_PAIR && bn_for(cout) == 128 && mt >= 2 &&
+         (mt % 2 == 0 || (WGH_PAIR_PAD > 0 && mt >= WGH_PAIR_PAD));
 }
 
 inline void plan(int n, int H, int W, int cin, int cout, Geo& g, int& mt, int& nt, int& splits) {
