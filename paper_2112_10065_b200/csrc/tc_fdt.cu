@@ -53,6 +53,11 @@
 #ifndef FDT_ALT
 #define FDT_ALT 1
 #endif
+// 12 converter warps for 64-wide tiles (three stage groups) measured 8-15 %
+// slower: the 96-register cap of 18 warps spills
+#ifndef FDT_NCONV64
+#define FDT_NCONV64 8
+#endif
 
 namespace bpx {
 namespace fdt {
@@ -71,7 +76,9 @@ template <int BN, int S_, bool PAIR = false>
 struct Cfg {
   static_assert(BN == 128 || BN == 64, "tile");
   static constexpr int S = S_;
-  static constexpr int NCONV = 8;
+  // converter warps: two per TMEM lane quadrant (FDT_NCONV64 for 64-wide tiles)
+  static constexpr int NCONV = (BN == 64 && FDT_ALT) ? FDT_NCONV64 : 8;
+  static constexpr int NGRP = NCONV / 4;                  // stage groups (ALT)
   static constexpr int NDRAIN = BN / 16;                  // 64 accumulator columns per thread
   static constexpr int DR0 = CV0 + NCONV;
   static constexpr int NTHREADS = 32 * (2 + NCONV + NDRAIN);
@@ -244,7 +251,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     for (int s = 0; s < NBS; ++s) mbar_init(&bfull[s], 1);
     for (int s = 0; s < S; ++s) {
       // one arrival per converter warp that wrote the stage
-      mbar_init(&aready[s], (PAIR ? 2 * NCONV : NCONV) / (FDT_ALT ? 2 : 1));
+      mbar_init(&aready[s], (PAIR ? 2 * NCONV : NCONV) / (FDT_ALT ? Cf::NGRP : 1));
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -514,7 +521,7 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 #if FDT_ALT
           // the two warps of a lane quadrant take alternate stages, all 64
           // channels each: stage i + 1's copy overlaps stage i's
-          if ((i & 1) != c2) continue;
+          if (i % Cf::NGRP != c2) continue;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t hi[16], lo[16];
