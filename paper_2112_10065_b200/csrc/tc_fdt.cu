@@ -53,6 +53,8 @@
 #ifndef FDT_ALT
 #define FDT_ALT 1
 #endif
+// (a halo split by one converter group alone, overlapping the other group's
+// last tap of the previous chunk, measured neutral: not kept)
 // 12 converter warps for 64-wide tiles (three stage groups) measured 8-15 %
 // slower: the 96-register cap of 18 warps spills
 #ifndef FDT_NCONV64
@@ -537,20 +539,26 @@ fdt_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
               lo[4 * k] = vl.x; lo[4 * k + 1] = vl.y; lo[4 * k + 2] = vl.z; lo[4 * k + 3] = vl.w;
             }
             if (hh == 0) {
+              PROF_START();
               if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);   // TMEM A slot free
+              PROF_ADD(8, pw);
               tc_fence_after();
             }
             const uint32_t a = lanebase + s * Cf::A_STAGE + 16 * hh;
             tmem_st16u(a, hi);
             tmem_st16u(a + KS / 2, lo);
           }
+          PROF_START();
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
+          PROF_ADD(10, pw);
+          PROF_START();
           if (lane == 0) {
             if (RB) mbar_wait(&bfull[tap], 0u); else mbar_wait(&bfull[s], (i / S) & 1);
             if (PAIR) mbar_arrive_remote(aready_l + 8u * s); else mbar_arrive(&aready[s]);
           }
           __syncwarp();
+          PROF_ADD(9, pw);
           continue;
 #endif
           // this thread's 32 channels: fp16 chunks 4 c2 .. 4 c2 + 3 of the

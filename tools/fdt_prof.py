@@ -15,6 +15,7 @@ from paper_2112_10065_b200.network import vgg16          # noqa: E402
 
 NAMES = {0: "mma_total", 1: "mma_wait_accfree", 2: "mma_wait_aready", 4: "stages",
          6: "conv_wait_hfull", 7: "conv_split", 8: "conv_wait_tmem", 9: "conv_wait_bfull",
+         10: "conv_wait_st",
          11: "tma_wait_hempty", 12: "tma_wait_empty", 14: "drain_wait_accfull",
          15: "drain_epilogue"}
 
@@ -47,6 +48,6 @@ for name in layers:
         v = list(out)
         n = max(v[4], 1)
         tot = max(v[0], 1)
-        parts = "  ".join(f"{NAMES[k]} {100 * v[k] / tot:5.1f}%" for k in (1, 2, 6, 7, 8, 9, 11, 12,
-                                                                         14, 15))
+        parts = "  ".join(f"{NAMES[k]} {100 * v[k] / tot:5.1f}%" for k in (1, 2, 6, 7, 8, 9, 10,
+                                                                         11, 12, 14, 15))
         print(f"{name} {op}: MMA-issuer cycles/stage {tot / n:6.0f} | {parts}")
