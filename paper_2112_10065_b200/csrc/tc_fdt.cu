@@ -30,7 +30,7 @@
 //                    64 input channels (w viewed [Cout][9][Cin]).
 // Each k-step (16 channels) issues a_lo*b_hi + a_hi*b_lo + a_hi*b_hi as
 // kind::f16 MMAs: twice the tf32 rate and, at 64-wide N tiles, half the
-// TMEM A reads per product.  Partial sums accumulate in 128-K chunks in
+// TMEM A reads per product.  Partial sums accumulate in 256-K chunks in
 // ping-pong TMEM and are promoted into round-to-nearest fp32 registers by
 // the drain warps (the tensor core's fp32 accumulation truncates), which
 // undo both scales (exact powers of two) before the epilogue.  The kernel is
@@ -68,7 +68,14 @@ using namespace tcx;
 constexpr int TMA_WARP = 0, MMA_WARP = 1, CV0 = 2;   // A converters from warp 2
 constexpr int KS = 64;                               // channels per stage
 constexpr int NCH = 2;                               // 32-channel halo halves per stage
-constexpr int PCH = 128 / KS;                        // stages per promotion chunk (K = 128)
+// promotion chunk: K = 256 per RN fp32 promotion of the truncating tensor
+// core accumulator.  fp64 error (tools/fdt_prec.py, VGG shapes): K = 128
+// 4.5e-7, 256 8.6e-7, 512 1.7e-6 against the 2e-6 gate; 256 is 2-5 % faster
+// than 128 (conv1_2 fwd 0.478 -> 0.456 ms, B200 same-box) at 2.3x margin
+#ifndef FDT_PCHK
+#define FDT_PCHK 256
+#endif
+constexpr int PCH = FDT_PCHK / KS;                   // stages per promotion chunk
 
 // BN output channels per tile, S stages; PAIR: a cluster of two CTAs runs
 // M tiles 2m, 2m+1 as one M = 256 MMA (cta_group::2), each CTA holding its
