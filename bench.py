@@ -217,7 +217,7 @@ def _ncu_traffic(dom):
 
 # engines on the fp16 tensor-core path (fp16x3: three kind::f16 MMAs per
 # fp32-accurate product) vs the 3xTF32 ones (three kind::tf32 MMAs)
-F16X3_ENGINES = {"fdt", "wgh"}
+F16X3_ENGINES = {"fdt", "wgh", "wgc", "wg1"}
 
 
 def _roofline(dom, peaks, peak_src, step_ms, flops_step, gemm_ms):
