@@ -13,7 +13,7 @@ def rnd(*shape, seed=0, scale=1.0):
 
 def relu_input(*shape, seed=0):
     return torch.relu(rnd(*shape, seed=seed))
-for shape in [(1, 224, 64, 64), (4, 224, 64, 64)]:
+for shape in [(1, 224, 64, 64), (4, 224, 64, 64), (16, 224, 64, 64)]:
     n, h, cin, cout = shape
     x = relu_input(n, h, h, cin, seed=40); dz = rnd(n, h, h, cout, seed=41)
     _, dw_ref, db_ref = vgg_ref.conv_grads(x, torch.zeros(cout, 3, 3, cin), dz)
